@@ -1,0 +1,166 @@
+/*
+ * pgrid.h -- C ABI of the B200-native topology-based power-grid transient
+ * solver (arxiv 1409.7166, "An Efficient Topology-Based Algorithm for Transient
+ * Analysis of Power Grid"; PAPER.md).  Library: paper_1409_7166_b200/lib/libpgb200.so
+ *
+ * Method (§II-A Eq. (2) and §IV Eqs. (12)-(15), Algorithm 1): at every
+ * backward-Euler step solve (C/h + G + hL) x(t+h) = rhs directly on the netlist
+ * graph by nodal relaxation -- never assembling G.  Each node is updated from
+ * its neighbours' voltages, branch conductances, pad conductance to Vdd,
+ * capacitor history C_i/h x_i(t) and its PWL current load (Eq. (13)), with SOR
+ * relaxation omega (Eq. (15)).  Inductors use the backward-Euler companion
+ * model (Eq. (10)): conductance h/L (series R-L: 1/(R + L/h)) plus a history
+ * current updated after every step.
+ *
+ * Conventions (all entry points):
+ *  - Return 0 (PG_OK) on success or a negative PG_E* code; pg_last_error()
+ *    then returns a thread-local, NUL-terminated description.  No entry point
+ *    aborts the process; on error the grid object is left unchanged (create
+ *    functions set *out = NULL).
+ *  - `mem` says where caller buffers live: PG_MEM_HOST (pageable or pinned host
+ *    memory) or PG_MEM_DEVICE (CUDA device memory of the current device).
+ *    Inputs are COPIED into library-owned device memory; the caller keeps
+ *    ownership of every buffer it passes and may free it after the call.
+ *  - Node index of a mesh node (layer l, row y, column x) is
+ *    (l * ny + y) * nx + x ("natural layout"); layer 0 is the bottom (device)
+ *    layer, layer `layers-1` the top (pad) layer.
+ *  - All values are SI: siemens, farads, henries, amperes, volts, seconds.
+ *  - Work is enqueued on the grid's stream (pg_set_stream; default: the legacy
+ *    default stream) and every entry point returns after its results are
+ *    complete in the caller's buffers.
+ *  - A pg_grid is not thread-safe; distinct grids may be used concurrently.
+ */
+#ifndef PGRID_H
+#define PGRID_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PG_API __attribute__((visibility("default")))
+
+typedef struct pg_grid pg_grid;
+
+enum { PG_MEM_HOST = 0, PG_MEM_DEVICE = 1 };
+
+enum {
+  PG_OK = 0,
+  PG_EINVAL = -1,    /* bad argument (sizes, indices, nonpositive values, omega outside (0,2)) */
+  PG_ECUDA = -2,     /* CUDA runtime / launch error (message carries cudaGetErrorString) */
+  PG_ENOCONV = -3,   /* a time step hit max_sweeps without meeting tol (results still written) */
+  PG_ENOMEM = -4,    /* device allocation failed */
+  PG_ESTATE = -5     /* call not valid for this grid (e.g. RLC data on a CSR grid) */
+};
+
+enum {
+  PG_METHOD_RBSOR = 0,  /* red-black ordered Gauss-Seidel / SOR (Eq. (13)+(15) in red-black numbering) */
+  PG_METHOD_JACOBI = 1  /* weighted Jacobi (comparison baseline) */
+};
+
+/* Layered-mesh grid (structure-of-arrays store).  PAPER.md §II-A: "C is a
+ * diagonal matrix whose (i,i) element is the capacitance between node i and
+ * ground ... G0 is ... the conductance between node i and source"; Fig. 2
+ * node model (R and L branches to neighbours).
+ *   gx[n]  conductance (S) of the in-layer segment (l,y,x)-(l,y,x+1); entries
+ *          with x = nx-1 must be 0.  >= 0.
+ *   gy[n]  conductance of (l,y,x)-(l,y+1,x); entries with y = ny-1 must be 0.
+ *   gz[n]  conductance 1/R of the via (l,y,x)-(l+1,y,x); layer layers-1 must be 0.
+ *   lz[n]  via series inductance (H, >= 0) or NULL (RC grid).  A via with
+ *          lz > 0 is a series R-L branch (R = 1/gz).
+ *   cap[n] node-to-ground capacitance (F, >= 0).
+ *   pad_node[n_pads], pad_g[n_pads]: pad branches from node to the Vdd source
+ *          node, conductance 1/R (> 0); pad_l[n_pads] series inductance or NULL.
+ *          A node may carry several pads.
+ *   n = layers * ny * nx.  layers, ny, nx >= 1.
+ * Every node must have a path to a pad (Lemma 1 / topological assumption 3);
+ * this is not checked here (an isolated node without capacitance makes the
+ * diagonal zero and is reported as PG_EINVAL by pg_transient).            */
+PG_API int pg_create_mesh(int32_t layers, int32_t ny, int32_t nx,
+                          const double *gx, const double *gy, const double *gz,
+                          const double *lz, const double *cap, int64_t n_pads,
+                          const int64_t *pad_node, const double *pad_g,
+                          const double *pad_l, double vdd, int mem, pg_grid **out);
+
+/* Irregular RC grid given as a branch list (CSR store built natively:
+ * parallel branches kept, self-loops dropped, nodes 2-coloured by BFS when the
+ * graph is bipartite, greedily multi-coloured otherwise; the sweep visits the
+ * colours in order -- Eq. (13) under that numbering).
+ *   bu[m], bv[m]: branch end nodes in [0, n); bg[m]: conductance (>= 0).
+ *   cap[n], pads as in pg_create_mesh (RC pads only).  n >= 1.          */
+PG_API int pg_create_csr(int64_t n, int64_t m, const int64_t *bu, const int64_t *bv,
+                         const double *bg, const double *cap, int64_t n_pads,
+                         const int64_t *pad_node, const double *pad_g, double vdd,
+                         int mem, pg_grid **out);
+
+/* PWL current loads (§II-A "modeled as piecewise linear ideal current
+ * sources"; load convention: current drawn from the node to ground).  Source k
+ * sits on node[k] with breakpoints t[ptr[k]..ptr[k+1]) (strictly increasing,
+ * seconds) and values i[...] (A); linear between breakpoints, first/last value
+ * held outside.  ptr has n_src+1 entries, ptr[0] = 0, every source >= 1 point.
+ * Replaces any previous set.  n_src = 0 clears the loads.                    */
+PG_API int pg_set_sources(pg_grid *g, int64_t n_src, const int64_t *node,
+                          const int64_t *ptr, const double *t, const double *i, int mem);
+
+/* Initial condition x(0) (n values; Algorithm 1 input "initial capacitor
+ * voltages").  Default after create: every node at vdd, inductor currents 0
+ * (the exact DC operating point of an unloaded grid).  Inductor currents are
+ * reset to 0 by this call.                                                  */
+PG_API int pg_set_voltages(pg_grid *g, const double *v, int mem);
+
+/* Voltages after the last completed pg_transient step (or x(0)); n values. */
+PG_API int pg_get_voltages(pg_grid *g, double *v, int mem);
+
+/* Enqueue all work of this grid on `stream` (a cudaStream_t, may be NULL). */
+PG_API int pg_set_stream(pg_grid *g, void *stream);
+
+/* Tuning knobs (key, value); unknown keys -> PG_EINVAL.
+ *   "fuse"   sweeps fused per sweep-kernel launch (temporal blocking), 1..8
+ *   "batch"  sweep launches enqueued between host convergence polls, >= 1
+ *   "graph"  1: drive each step's sweep batches from a captured CUDA graph  */
+PG_API int pg_set_option(pg_grid *g, const char *key, int64_t value);
+
+typedef struct {
+  int64_t steps_done;      /* time steps completed */
+  int64_t sweeps_total;    /* relaxation sweeps performed (sum over steps) */
+  int64_t sweeps_max;      /* max sweeps in one step */
+  int64_t failed_step;     /* first step that hit max_sweeps (0: none) */
+  int64_t kernel_launches; /* kernels launched by this call */
+  double last_delta;       /* max |dV| of the final sweep of the last step (V) */
+  double device_ms;        /* device time of the call (CUDA events) */
+} pg_stats;
+
+/* Algorithm 1: backward-Euler transient from x(0) at t = 0 for `steps` steps
+ * of length h (> 0).  Each step: fused RHS kernel (PWL loads at t+h, C/h x(t),
+ * pad and inductor history) -> relaxation sweeps from V(s-1) until
+ * max_i |V_i^(k) - V_i^(k-1)| < tol (Algorithm 1 line 8, infinity norm) or
+ * max_sweeps -> inductor companion-current update.  tol <= 0 runs exactly
+ * max_sweeps sweeps per step.  omega in (0, 2) (Eq. (15); 1 = Gauss-Seidel).
+ * method: PG_METHOD_RBSOR or PG_METHOD_JACOBI.  When the fused sweep kernel
+ * checks convergence every F sweeps (option "fuse"), a step may run up to
+ * F-1 sweeps past the first sweep below tol.
+ * Probes: probe_out[(s) * n_probe + p] = V(s h) at node probe_node[p] for
+ * s = 0..steps (probe_out holds (steps+1)*n_probe doubles in `mem`);
+ * n_probe = 0 disables recording.  sweeps_out (nullable, HOST, steps+1
+ * int64) receives per-step sweep counts.  stats (nullable, host) is filled
+ * on success and on PG_ENOCONV.                                             */
+PG_API int pg_transient(pg_grid *g, double h, int64_t steps, double tol, double omega,
+                        int method, int64_t max_sweeps, int64_t n_probe,
+                        const int64_t *probe_node, double *probe_out, int mem,
+                        int64_t *sweeps_out, pg_stats *stats);
+
+/* Number of nodes / dimensions (layers, ny, nx are 0 for CSR grids). */
+PG_API int pg_info(const pg_grid *g, int64_t *n, int32_t *layers, int32_t *ny, int32_t *nx,
+                   int32_t *n_colors);
+
+/* Free all device memory of the grid.  NULL is a no-op. */
+PG_API void pg_destroy(pg_grid *g);
+
+/* Description of the last error on this thread ("" if none). */
+PG_API const char *pg_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PGRID_H */

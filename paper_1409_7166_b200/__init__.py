@@ -1,0 +1,11 @@
+"""B200-native topology-based power-grid transient analysis (arxiv 1409.7166).
+
+The hot path (RHS, red-black SOR / Jacobi / multi-colour CSR relaxation sweeps
+with fused convergence reduction, inductor companion update, time-step driver)
+lives in the sm_100a library ``lib/libpgb200.so`` behind the C ABI of
+``include/pgrid.h``; this package is its thin Python binding.
+"""
+from ._lib import PgError, PgNoConvergence, load  # noqa: F401
+from .api import Grid, TransientResult  # noqa: F401
+
+__all__ = ["Grid", "TransientResult", "PgError", "PgNoConvergence", "load"]

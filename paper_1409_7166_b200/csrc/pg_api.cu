@@ -1,0 +1,589 @@
+// C ABI (include/pgrid.h): netlist store construction and the Algorithm 1
+// time-step driver.  All numerics run in the kernels of pg_kernels.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "pg_internal.h"
+
+namespace pgb {
+static thread_local std::string g_err;
+void set_error(const std::string &msg) { g_err = msg; }
+int cuda_fail(cudaError_t e, const char *what) {
+  set_error(std::string(what) + ": " + cudaGetErrorString(e));
+  return PG_ECUDA;
+}
+
+__global__ void k_fill_real(double *x, int64_t np, int32_t NX, int32_t NXP, double v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < np;
+       i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = (NXP == 0 || (i % NXP) < NX) ? v : 0.0;
+}
+}  // namespace pgb
+
+using namespace pgb;
+
+#define CK(call)                                          \
+  do {                                                    \
+    cudaError_t _e = (call);                              \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call);   \
+  } while (0)
+
+#define REQUIRE(cond, msg)    \
+  do {                        \
+    if (!(cond)) {            \
+      set_error(msg);         \
+      return PG_EINVAL;       \
+    }                         \
+  } while (0)
+
+namespace {
+
+template <class T>
+int dalloc(T **p, int64_t count) {
+  *p = nullptr;
+  if (count <= 0) return PG_OK;
+  cudaError_t e = cudaMalloc((void **)p, sizeof(T) * (size_t)count);
+  if (e != cudaSuccess) {
+    *p = nullptr;
+    set_error(std::string("cudaMalloc of ") + std::to_string(sizeof(T) * (size_t)count) +
+              " bytes failed: " + cudaGetErrorString(e));
+    return PG_ENOMEM;
+  }
+  return PG_OK;
+}
+
+template <class T>
+int to_host(const T *src, int64_t count, int mem, std::vector<T> &out) {
+  out.resize((size_t)std::max<int64_t>(count, 0));
+  if (count <= 0) return PG_OK;
+  if (mem == PG_MEM_HOST) {
+    std::memcpy(out.data(), src, sizeof(T) * (size_t)count);
+    return PG_OK;
+  }
+  CK(cudaMemcpy(out.data(), src, sizeof(T) * (size_t)count, cudaMemcpyDeviceToHost));
+  return PG_OK;
+}
+
+template <class T>
+int upload(T *dst, const std::vector<T> &v) {
+  if (v.empty()) return PG_OK;
+  CK(cudaMemcpy(dst, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+  return PG_OK;
+}
+
+void free_grid(pg_grid *g) {
+  if (!g) return;
+  void *ptrs[] = {g->gx, g->gy, g->gz, g->lz, g->gze, g->iz, g->rowptr, g->col, g->val, g->perm,
+                  g->iperm, g->V[0], g->V[1], g->x0, g->cap, g->invd, g->b, g->pad_idx,
+                  g->pad_grp, g->pad_g, g->pad_l, g->pad_ge, g->pad_i, g->src_idx, g->src_grp,
+                  g->src_ptr, g->pwl_t, g->pwl_i, g->ctl, g->dev_sweeps};
+  for (void *p : ptrs)
+    if (p) cudaFree(p);
+  if (g->ctl_host) cudaFreeHost(g->ctl_host);
+  if (g->done_host) cudaFreeHost(g->done_host);
+  delete g;
+}
+
+struct GridGuard {
+  pg_grid *g;
+  ~GridGuard() { free_grid(g); }
+};
+
+int64_t storage_index(const pg_grid *g, int64_t k, const std::vector<int64_t> *iperm_host) {
+  if (g->kind == 0) {
+    const int64_t per_layer = (int64_t)g->md.NY * g->md.NX;
+    const int64_t l = k / per_layer, r = k % per_layer;
+    const int64_t y = r / g->md.NX, x = r % g->md.NX;
+    return l * g->md.layer_stride + y * g->md.NXP + x;
+  }
+  return (*iperm_host)[(size_t)k];
+}
+
+// group sorted storage indices: returns group start offsets (ngrp+1)
+std::vector<int64_t> groups_of(const std::vector<int64_t> &sidx) {
+  std::vector<int64_t> grp;
+  for (size_t k = 0; k < sidx.size(); ++k)
+    if (k == 0 || sidx[k] != sidx[k - 1]) grp.push_back((int64_t)k);
+  grp.push_back((int64_t)sidx.size());
+  return grp;
+}
+
+int common_init(pg_grid *g) {
+  CK(cudaGetDevice(&g->dev));
+  CK(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, g->dev));
+  int rc;
+  if ((rc = dalloc(&g->V[0], g->np)) || (rc = dalloc(&g->V[1], g->np)) || (rc = dalloc(&g->x0, g->np)) ||
+      (rc = dalloc(&g->invd, g->np)) || (rc = dalloc(&g->b, g->np)) || (rc = dalloc(&g->ctl, 1)))
+    return rc;
+  CK(cudaMemset(g->V[0], 0, sizeof(double) * g->np));
+  CK(cudaMemset(g->V[1], 0, sizeof(double) * g->np));
+  CK(cudaMemset(g->b, 0, sizeof(double) * g->np));
+  CK(cudaMemset(g->invd, 0, sizeof(double) * g->np));
+  CK(cudaMemset(g->ctl, 0, sizeof(DevCtl)));
+  CK(cudaMallocHost((void **)&g->ctl_host, sizeof(DevCtl)));
+  CK(cudaMallocHost((void **)&g->done_host, sizeof(int32_t) * 8));
+  const int B = 256;
+  const int grid = (int)std::min<int64_t>((g->np + B - 1) / B, (int64_t)g->num_sms * 16);
+  k_fill_real<<<std::max(grid, 1), B>>>(g->x0, g->np, g->kind == 0 ? g->md.NX : 0,
+                                        g->kind == 0 ? g->md.NXP : 0, g->vdd);
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(g->V[0], g->x0, sizeof(double) * g->np, cudaMemcpyDeviceToDevice));
+  CK(cudaDeviceSynchronize());
+  return PG_OK;
+}
+
+int set_pads(pg_grid *g, int64_t n_pads, const int64_t *pad_node, const double *pad_g,
+             const double *pad_l, int mem, const std::vector<int64_t> *iperm_host) {
+  std::vector<int64_t> node;
+  std::vector<double> pg, pl;
+  int rc;
+  if ((rc = to_host(pad_node, n_pads, mem, node)) || (rc = to_host(pad_g, n_pads, mem, pg))) return rc;
+  if (pad_l && (rc = to_host(pad_l, n_pads, mem, pl))) return rc;
+  std::vector<int64_t> sidx((size_t)n_pads);
+  for (int64_t k = 0; k < n_pads; ++k) {
+    REQUIRE(node[k] >= 0 && node[k] < g->n, "pad node index out of range");
+    REQUIRE(pg[k] > 0.0 && std::isfinite(pg[k]), "pad conductance must be finite and > 0");
+    if (pad_l) REQUIRE(pl[k] >= 0.0 && std::isfinite(pl[k]), "pad inductance must be finite and >= 0");
+    sidx[k] = storage_index(g, node[k], iperm_host);
+  }
+  std::vector<int64_t> order((size_t)n_pads);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return sidx[a] < sidx[b]; });
+  std::vector<int64_t> s2(n_pads);
+  std::vector<double> g2(n_pads), l2(pad_l ? n_pads : 0);
+  for (int64_t k = 0; k < n_pads; ++k) {
+    s2[k] = sidx[order[k]];
+    g2[k] = pg[order[k]];
+    if (pad_l) l2[k] = pl[order[k]];
+  }
+  std::vector<int64_t> grp = groups_of(s2);
+  g->npad = n_pads;
+  g->npad_grp = (int64_t)grp.size() - 1;
+  if ((rc = dalloc(&g->pad_idx, n_pads)) || (rc = dalloc(&g->pad_grp, (int64_t)grp.size())) ||
+      (rc = dalloc(&g->pad_g, n_pads)) || (rc = dalloc(&g->pad_ge, n_pads)))
+    return rc;
+  if ((rc = upload(g->pad_idx, s2)) || (rc = upload(g->pad_grp, grp)) || (rc = upload(g->pad_g, g2))) return rc;
+  if (pad_l && n_pads > 0) {
+    if ((rc = dalloc(&g->pad_l, n_pads)) || (rc = dalloc(&g->pad_i, n_pads))) return rc;
+    if ((rc = upload(g->pad_l, l2))) return rc;
+    CK(cudaMemset(g->pad_i, 0, sizeof(double) * n_pads));
+    g->rlc = true;
+  }
+  return PG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+PG_API const char *pg_last_error(void) { return g_err.c_str(); }
+
+PG_API int pg_create_mesh(int32_t layers, int32_t ny, int32_t nx, const double *gx, const double *gy,
+                          const double *gz, const double *lz, const double *cap, int64_t n_pads,
+                          const int64_t *pad_node, const double *pad_g, const double *pad_l,
+                          double vdd, int mem, pg_grid **out) {
+  if (out) *out = nullptr;
+  REQUIRE(out != nullptr, "out is NULL");
+  REQUIRE(layers >= 1 && ny >= 1 && nx >= 1, "layers, ny, nx must be >= 1");
+  REQUIRE(layers <= kMaxLayers, "at most 8 layers per mesh grid (split taller stacks)");
+  REQUIRE(mem == PG_MEM_HOST || mem == PG_MEM_DEVICE, "mem must be PG_MEM_HOST or PG_MEM_DEVICE");
+  REQUIRE(gx && gy && gz && cap, "gx, gy, gz, cap are required");
+  REQUIRE(n_pads >= 0 && (n_pads == 0 || (pad_node && pad_g)), "bad pad arrays");
+  REQUIRE(std::isfinite(vdd), "vdd must be finite");
+  const int64_t n = (int64_t)layers * ny * nx;
+  if (mem == PG_MEM_HOST) {  // value checks (device inputs are trusted)
+    for (int64_t k = 0; k < n; ++k) {
+      const int64_t x = k % nx, y = (k / nx) % ny, l = k / ((int64_t)nx * ny);
+      REQUIRE(gx[k] >= 0 && gy[k] >= 0 && gz[k] >= 0 && cap[k] >= 0 && std::isfinite(cap[k]),
+              "conductances and capacitances must be >= 0");
+      REQUIRE(x < nx - 1 || gx[k] == 0.0, "gx must be 0 in the last column");
+      REQUIRE(y < ny - 1 || gy[k] == 0.0, "gy must be 0 in the last row");
+      REQUIRE(l < layers - 1 || gz[k] == 0.0, "gz must be 0 in the top layer");
+      if (lz) REQUIRE(lz[k] >= 0.0 && std::isfinite(lz[k]), "lz must be finite and >= 0");
+    }
+  }
+  pg_grid *g = new pg_grid();
+  GridGuard guard{g};
+  g->kind = 0;
+  g->n = n;
+  g->vdd = vdd;
+  g->md.L = layers;
+  g->md.NY = ny;
+  g->md.NX = nx;
+  g->md.NXP = (nx + 15) / 16 * 16;
+  g->md.layer_stride = (int64_t)ny * g->md.NXP;
+  g->md.np = (int64_t)layers * g->md.layer_stride;
+  g->np = g->md.np;
+  int rc;
+  if ((rc = common_init(g))) return rc;
+  const cudaMemcpyKind kind = mem == PG_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  auto put = [&](double **dst, const double *src) -> int {
+    int r = dalloc(dst, g->np);
+    if (r) return r;
+    CK(cudaMemset(*dst, 0, sizeof(double) * g->np));
+    CK(cudaMemcpy2D(*dst, sizeof(double) * g->md.NXP, src, sizeof(double) * nx, sizeof(double) * nx,
+                    (size_t)layers * ny, kind));
+    return PG_OK;
+  };
+  if ((rc = put(&g->gx, gx)) || (rc = put(&g->gy, gy)) || (rc = put(&g->gz, gz)) || (rc = put(&g->cap, cap)))
+    return rc;
+  if ((rc = dalloc(&g->gze, g->np))) return rc;
+  CK(cudaMemcpy(g->gze, g->gz, sizeof(double) * g->np, cudaMemcpyDeviceToDevice));
+  if (lz) {
+    if ((rc = put(&g->lz, lz)) || (rc = dalloc(&g->iz, g->np))) return rc;
+    CK(cudaMemset(g->iz, 0, sizeof(double) * g->np));
+    g->rlc = true;
+  }
+  if ((rc = set_pads(g, n_pads, pad_node, pad_g, pad_l, mem, nullptr))) return rc;
+  CK(cudaDeviceSynchronize());
+  guard.g = nullptr;
+  *out = g;
+  return PG_OK;
+}
+
+PG_API int pg_create_csr(int64_t n, int64_t m, const int64_t *bu, const int64_t *bv, const double *bg,
+                         const double *cap, int64_t n_pads, const int64_t *pad_node,
+                         const double *pad_g, double vdd, int mem, pg_grid **out) {
+  if (out) *out = nullptr;
+  REQUIRE(out != nullptr, "out is NULL");
+  REQUIRE(n >= 1, "n must be >= 1");
+  REQUIRE(n < (int64_t)INT32_MAX, "CSR grids are limited to 2^31-1 nodes");
+  REQUIRE(m >= 0 && (m == 0 || (bu && bv && bg)), "bad branch arrays");
+  REQUIRE(cap != nullptr, "cap is required");
+  REQUIRE(mem == PG_MEM_HOST || mem == PG_MEM_DEVICE, "mem must be PG_MEM_HOST or PG_MEM_DEVICE");
+  REQUIRE(n_pads >= 0 && (n_pads == 0 || (pad_node && pad_g)), "bad pad arrays");
+  std::vector<int64_t> u, v;
+  std::vector<double> gg, c;
+  int rc;
+  if ((rc = to_host(bu, m, mem, u)) || (rc = to_host(bv, m, mem, v)) || (rc = to_host(bg, m, mem, gg)) ||
+      (rc = to_host(cap, n, mem, c)))
+    return rc;
+  for (int64_t k = 0; k < n; ++k) REQUIRE(c[k] >= 0 && std::isfinite(c[k]), "cap must be finite and >= 0");
+  CsrHost H;
+  std::string err;
+  if (build_csr(n, m, u.data(), v.data(), gg.data(), H, err) != 0) {
+    set_error(err);
+    return PG_EINVAL;
+  }
+  pg_grid *g = new pg_grid();
+  GridGuard guard{g};
+  g->kind = 1;
+  g->n = n;
+  g->np = n;
+  g->vdd = vdd;
+  g->ncolor = (int32_t)H.color_ptr.size() - 1;
+  g->color_ptr = H.color_ptr;
+  if ((rc = common_init(g))) return rc;
+  std::vector<double> cp((size_t)n);
+  for (int64_t k = 0; k < n; ++k) cp[H.iperm[k]] = c[k];
+  if ((rc = dalloc(&g->rowptr, n + 1)) || (rc = dalloc(&g->col, (int64_t)H.col.size())) ||
+      (rc = dalloc(&g->val, (int64_t)H.val.size())) || (rc = dalloc(&g->perm, n)) ||
+      (rc = dalloc(&g->iperm, n)) || (rc = dalloc(&g->cap, n)))
+    return rc;
+  if ((rc = upload(g->rowptr, H.rowptr)) || (rc = upload(g->col, H.col)) || (rc = upload(g->val, H.val)) ||
+      (rc = upload(g->perm, H.perm)) || (rc = upload(g->iperm, H.iperm)) || (rc = upload(g->cap, cp)))
+    return rc;
+  if ((rc = set_pads(g, n_pads, pad_node, pad_g, nullptr, mem, &H.iperm))) return rc;
+  CK(cudaDeviceSynchronize());
+  guard.g = nullptr;
+  *out = g;
+  return PG_OK;
+}
+
+PG_API void pg_destroy(pg_grid *g) { free_grid(g); }
+
+PG_API int pg_set_stream(pg_grid *g, void *stream) {
+  REQUIRE(g != nullptr, "grid is NULL");
+  g->stream = (cudaStream_t)stream;
+  return PG_OK;
+}
+
+PG_API int pg_set_option(pg_grid *g, const char *key, int64_t value) {
+  REQUIRE(g != nullptr && key != nullptr, "grid/key is NULL");
+  const std::string k(key);
+  if (k == "fuse") {
+    REQUIRE(value >= 1 && value <= 8, "fuse must be in 1..8");
+    g->fuse = (int)value;
+  } else if (k == "batch") {
+    REQUIRE(value >= 1 && value <= 1024, "batch must be in 1..1024");
+    g->batch = (int)value;
+  } else if (k == "graph") {
+    g->graph = value != 0;
+  } else {
+    set_error("unknown option: " + k);
+    return PG_EINVAL;
+  }
+  return PG_OK;
+}
+
+PG_API int pg_info(const pg_grid *g, int64_t *n, int32_t *layers, int32_t *ny, int32_t *nx,
+                   int32_t *n_colors) {
+  REQUIRE(g != nullptr, "grid is NULL");
+  if (n) *n = g->n;
+  if (layers) *layers = g->kind == 0 ? g->md.L : 0;
+  if (ny) *ny = g->kind == 0 ? g->md.NY : 0;
+  if (nx) *nx = g->kind == 0 ? g->md.NX : 0;
+  if (n_colors) *n_colors = g->kind == 0 ? 2 : g->ncolor;
+  return PG_OK;
+}
+
+PG_API int pg_set_sources(pg_grid *g, int64_t n_src, const int64_t *node, const int64_t *ptr,
+                          const double *t, const double *i, int mem) {
+  REQUIRE(g != nullptr, "grid is NULL");
+  REQUIRE(n_src >= 0, "n_src must be >= 0");
+  REQUIRE(mem == PG_MEM_HOST || mem == PG_MEM_DEVICE, "bad mem");
+  for (int64_t *p : {g->src_idx, g->src_grp, g->src_ptr})
+    if (p) cudaFree(p);
+  for (double *p : {g->pwl_t, g->pwl_i})
+    if (p) cudaFree(p);
+  g->src_idx = g->src_grp = g->src_ptr = nullptr;
+  g->pwl_t = g->pwl_i = nullptr;
+  g->nsrc = g->nsrc_grp = g->npts = 0;
+  if (n_src == 0) return PG_OK;
+  REQUIRE(node && ptr && t && i, "source arrays are NULL");
+  std::vector<int64_t> nd, pp;
+  int rc;
+  if ((rc = to_host(node, n_src, mem, nd)) || (rc = to_host(ptr, n_src + 1, mem, pp))) return rc;
+  REQUIRE(pp[0] == 0, "ptr[0] must be 0");
+  for (int64_t k = 0; k < n_src; ++k) {
+    REQUIRE(pp[k + 1] > pp[k], "every source needs at least one breakpoint");
+    REQUIRE(nd[k] >= 0 && nd[k] < g->n, "source node index out of range");
+  }
+  const int64_t npts = pp[n_src];
+  std::vector<double> tt, ii;
+  if ((rc = to_host(t, npts, mem, tt)) || (rc = to_host(i, npts, mem, ii))) return rc;
+  for (int64_t k = 0; k < n_src; ++k)
+    for (int64_t q = pp[k] + 1; q < pp[k + 1]; ++q)
+      REQUIRE(tt[q] > tt[q - 1], "PWL breakpoint times must be strictly increasing");
+  std::vector<int64_t> iperm_h;
+  if (g->kind == 1) {
+    iperm_h.resize((size_t)g->n);
+    CK(cudaMemcpy(iperm_h.data(), g->iperm, sizeof(int64_t) * g->n, cudaMemcpyDeviceToHost));
+  }
+  std::vector<int64_t> sidx((size_t)n_src);
+  for (int64_t k = 0; k < n_src; ++k) sidx[k] = storage_index(g, nd[k], &iperm_h);
+  std::vector<int64_t> order((size_t)n_src);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return sidx[a] < sidx[b]; });
+  std::vector<int64_t> s2(n_src), p2(n_src + 1);
+  std::vector<double> t2((size_t)npts), i2((size_t)npts);
+  int64_t off = 0;
+  for (int64_t k = 0; k < n_src; ++k) {
+    const int64_t o = order[k];
+    s2[k] = sidx[o];
+    p2[k] = off;
+    for (int64_t q = pp[o]; q < pp[o + 1]; ++q, ++off) {
+      t2[off] = tt[q];
+      i2[off] = ii[q];
+    }
+  }
+  p2[n_src] = off;
+  std::vector<int64_t> grp = groups_of(s2);
+  if ((rc = dalloc(&g->src_idx, n_src)) || (rc = dalloc(&g->src_grp, (int64_t)grp.size())) ||
+      (rc = dalloc(&g->src_ptr, n_src + 1)) || (rc = dalloc(&g->pwl_t, npts)) || (rc = dalloc(&g->pwl_i, npts)))
+    return rc;
+  if ((rc = upload(g->src_idx, s2)) || (rc = upload(g->src_grp, grp)) || (rc = upload(g->src_ptr, p2)) ||
+      (rc = upload(g->pwl_t, t2)) || (rc = upload(g->pwl_i, i2)))
+    return rc;
+  g->nsrc = n_src;
+  g->nsrc_grp = (int64_t)grp.size() - 1;
+  g->npts = npts;
+  return PG_OK;
+}
+
+PG_API int pg_set_voltages(pg_grid *g, const double *v, int mem) {
+  REQUIRE(g != nullptr && v != nullptr, "grid/v is NULL");
+  REQUIRE(mem == PG_MEM_HOST || mem == PG_MEM_DEVICE, "bad mem");
+  double *tmp = nullptr;
+  int rc;
+  if ((rc = dalloc(&tmp, g->n))) return rc;
+  cudaError_t e = cudaMemcpyAsync(tmp, v, sizeof(double) * g->n,
+                                  mem == PG_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                                  g->stream);
+  if (e == cudaSuccess) e = launch_scatter_user(g, tmp, g->x0);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(g->V[0], g->x0, sizeof(double) * g->np, cudaMemcpyDeviceToDevice, g->stream);
+  if (e == cudaSuccess) e = launch_reset_state(g);
+  if (e == cudaSuccess && g->iz) e = cudaMemsetAsync(g->iz, 0, sizeof(double) * g->np, g->stream);
+  if (e == cudaSuccess && g->pad_i) e = cudaMemsetAsync(g->pad_i, 0, sizeof(double) * g->npad, g->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+  cudaFree(tmp);
+  if (e != cudaSuccess) return cuda_fail(e, "pg_set_voltages");
+  return PG_OK;
+}
+
+PG_API int pg_get_voltages(pg_grid *g, double *v, int mem) {
+  REQUIRE(g != nullptr && v != nullptr, "grid/v is NULL");
+  REQUIRE(mem == PG_MEM_HOST || mem == PG_MEM_DEVICE, "bad mem");
+  if (mem == PG_MEM_DEVICE) {
+    CK(launch_gather_user(g, v));
+    CK(cudaStreamSynchronize(g->stream));
+    return PG_OK;
+  }
+  double *tmp = nullptr;
+  int rc;
+  if ((rc = dalloc(&tmp, g->n))) return rc;
+  cudaError_t e = launch_gather_user(g, tmp);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(v, tmp, sizeof(double) * g->n, cudaMemcpyDeviceToHost, g->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+  cudaFree(tmp);
+  if (e != cudaSuccess) return cuda_fail(e, "pg_get_voltages");
+  return PG_OK;
+}
+
+PG_API int pg_transient(pg_grid *g, double h, int64_t steps, double tol, double omega, int method,
+                        int64_t max_sweeps, int64_t n_probe, const int64_t *probe_node,
+                        double *probe_out, int mem, int64_t *sweeps_out, pg_stats *stats) {
+  REQUIRE(g != nullptr, "grid is NULL");
+  REQUIRE(h > 0.0 && std::isfinite(h), "h must be finite and > 0");
+  REQUIRE(steps >= 0, "steps must be >= 0");
+  REQUIRE(omega > 0.0 && omega < 2.0, "omega must be in (0, 2) (Eq. (15) convergence range)");
+  REQUIRE(method == PG_METHOD_RBSOR || method == PG_METHOD_JACOBI, "unknown method");
+  REQUIRE(max_sweeps >= 1, "max_sweeps must be >= 1");
+  REQUIRE(!std::isnan(tol), "tol is NaN");
+  REQUIRE(n_probe >= 0 && (n_probe == 0 || (probe_node && probe_out)), "bad probe arrays");
+  REQUIRE(mem == PG_MEM_HOST || mem == PG_MEM_DEVICE, "bad mem");
+
+  int rc;
+  // ---- probes
+  std::vector<int64_t> pn;
+  if ((rc = to_host(probe_node, n_probe, mem, pn))) return rc;
+  std::vector<int64_t> iperm_h;
+  if (g->kind == 1 && n_probe > 0) {
+    iperm_h.resize((size_t)g->n);
+    CK(cudaMemcpy(iperm_h.data(), g->iperm, sizeof(int64_t) * g->n, cudaMemcpyDeviceToHost));
+  }
+  std::vector<int64_t> pidx((size_t)n_probe);
+  for (int64_t k = 0; k < n_probe; ++k) {
+    REQUIRE(pn[k] >= 0 && pn[k] < g->n, "probe node index out of range");
+    pidx[k] = storage_index(g, pn[k], &iperm_h);
+  }
+  int64_t *d_pidx = nullptr;
+  double *d_pout = nullptr;
+  struct Tmp {
+    int64_t **a;
+    double **b;
+    bool own_b;
+    ~Tmp() {
+      if (*a) cudaFree(*a);
+      if (own_b && *b) cudaFree(*b);
+    }
+  } tmp{&d_pidx, &d_pout, mem == PG_MEM_HOST};
+  if (n_probe > 0) {
+    if ((rc = dalloc(&d_pidx, n_probe))) return rc;
+    if ((rc = upload(d_pidx, pidx))) return rc;
+    if (mem == PG_MEM_HOST) {
+      if ((rc = dalloc(&d_pout, (steps + 1) * n_probe))) return rc;
+    } else {
+      d_pout = probe_out;
+    }
+  }
+  if (g->dev_sweeps_cap < steps + 1) {
+    if (g->dev_sweeps) cudaFree(g->dev_sweeps);
+    g->dev_sweeps = nullptr;
+    g->dev_sweeps_cap = 0;
+    if ((rc = dalloc(&g->dev_sweeps, steps + 1))) return rc;
+    g->dev_sweeps_cap = steps + 1;
+  }
+  cudaStream_t st = g->stream;
+  cudaEvent_t ev0, ev1, poll[2];
+  CK(cudaEventCreate(&ev0));
+  CK(cudaEventCreate(&ev1));
+  CK(cudaEventCreateWithFlags(&poll[0], cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&poll[1], cudaEventDisableTiming));
+  struct Ev {
+    cudaEvent_t *e;
+    ~Ev() {
+      for (int k = 0; k < 4; ++k) cudaEventDestroy(e[k]);
+    }
+  };
+  cudaEvent_t evs[4] = {ev0, ev1, poll[0], poll[1]};
+  Ev evguard{evs};
+
+  int64_t launches = 0;
+  const int F = sweeps_per_launch(g, method);
+  const int flips = (g->kind == 0 || method == PG_METHOD_JACOBI) ? 1 : 0;
+  const int64_t max_launch = (max_sweeps + F - 1) / F;
+
+  CK(cudaEventRecord(ev0, st));
+  CK(cudaMemcpyAsync(g->V[0], g->x0, sizeof(double) * g->np, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemsetAsync(g->dev_sweeps, 0, sizeof(int64_t) * (steps + 1), st));
+  if (g->iz) CK(cudaMemsetAsync(g->iz, 0, sizeof(double) * g->np, st));
+  if (g->pad_i) CK(cudaMemsetAsync(g->pad_i, 0, sizeof(double) * g->npad, st));
+  CK(launch_reset_state(g));
+  CK(launch_setup(g, h));
+  launches += 4;
+  if (n_probe > 0) {
+    CK(launch_probe(g, d_pidx, n_probe, d_pout));
+    ++launches;
+  }
+  for (int64_t s = 1; s <= steps; ++s) {
+    CK(launch_rhs(g, h, s));
+    launches += 1 + (g->npad > 0) + (g->nsrc > 0);
+    int64_t j = 0;
+    int pending = -1;  // poll slot of the previous batch
+    int slot = 0;
+    while (j < max_launch) {
+      const int64_t nb = std::min<int64_t>(g->batch, max_launch - j);
+      for (int64_t k = 0; k < nb; ++k) {
+        const int nsw = (int)std::min<int64_t>(F, max_sweeps - (j + k) * F);
+        CK(launch_sweep(g, method, omega, tol, (int)(j + k), nsw, &launches));
+      }
+      j += nb;
+      if (!(tol > 0.0) || j >= max_launch) continue;
+      CK(cudaMemcpyAsync(&g->done_host[slot], &g->ctl->done, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      CK(cudaEventRecord(poll[slot], st));
+      if (pending >= 0) {
+        CK(cudaEventSynchronize(poll[pending]));
+        if (g->done_host[pending]) break;
+      }
+      pending = slot;
+      slot ^= 1;
+    }
+    CK(launch_step_end(g, s, (int)j, flips, F, max_sweeps, tol));
+    ++launches;
+    if (g->rlc) {
+      CK(launch_inductor_update(g, h));
+      launches += 2;
+    }
+    if (n_probe > 0) {
+      CK(launch_probe(g, d_pidx, n_probe, d_pout + s * n_probe));
+      ++launches;
+    }
+  }
+  CK(cudaEventRecord(ev1, st));
+  CK(cudaMemcpyAsync(g->ctl_host, g->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, st));
+  if (n_probe > 0 && mem == PG_MEM_HOST)
+    CK(cudaMemcpyAsync(probe_out, d_pout, sizeof(double) * (steps + 1) * n_probe, cudaMemcpyDeviceToHost, st));
+  if (sweeps_out)
+    CK(cudaMemcpyAsync(sweeps_out, g->dev_sweeps, sizeof(int64_t) * (steps + 1), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, ev0, ev1));
+  const DevCtl &c = *g->ctl_host;
+  if (stats) {
+    stats->steps_done = steps;
+    stats->sweeps_total = c.sweeps_total;
+    stats->sweeps_max = c.sweeps_max;
+    stats->failed_step = c.failed;
+    stats->kernel_launches = launches;
+    stats->last_delta = c.last_delta;
+    stats->device_ms = ms;
+  }
+  if (c.diag_bad) {
+    set_error("a node has a non-positive diagonal d_i (no capacitance and no conductive path; Lemma 1)");
+    return PG_EINVAL;
+  }
+  if (c.failed) {
+    set_error("step " + std::to_string(c.failed) + " did not reach tol within max_sweeps");
+    return PG_ENOCONV;
+  }
+  return PG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,740 @@
+// Device kernels of the B200 power-grid transient solver (sm_100a).
+//
+// Hot path per backward-Euler step (Algorithm 1):
+//   k_rhs_*            fused RHS: C_i/h x_i(t) + pad G0 Vdd (+ companion history)
+//                      - PWL loads I_i(t+h)                       (Eq. (2) / (12))
+//   k_rb_sweep         red-black SOR sweep, both colours in ONE streaming pass
+//                      (Eq. (13) in red-black numbering + Eq. (15)), fused
+//                      warp-shuffle max|dV| reduction                  (line 7-8)
+//   k_jacobi_mesh      weighted Jacobi sweep (comparison)
+//   k_csr_sweep        multi-colour Gauss-Seidel/SOR on the CSR store (irregular grids)
+//   k_ind_update_*     companion inductor currents i(t+h) = g_e v + alpha i(t)  (Eq. (10))
+//   k_step_end         device-side bookkeeping of the step (sweep count, buffer parity)
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "pg_internal.h"
+
+namespace pgb {
+
+#define FULLMASK 0xffffffffu
+
+__device__ __forceinline__ double2 ld2(const double *p) {
+  return __ldg(reinterpret_cast<const double2 *>(p));
+}
+__device__ __forceinline__ void st2(double *p, double a, double b) {
+  *reinterpret_cast<double2 *>(p) = make_double2(a, b);
+}
+__device__ __forceinline__ unsigned long long d2u(double x) {
+  return static_cast<unsigned long long>(__double_as_longlong(x));
+}
+__device__ __forceinline__ double u2d(unsigned long long x) {
+  return __longlong_as_double(static_cast<long long>(x));
+}
+
+// ------------------------------------------------------------------ convergence
+// Evaluated identically by every CTA of a sweep launch (uniform), so a converged
+// step turns the remaining queued launches into no-ops.
+__device__ __forceinline__ bool sweep_skip(DevCtl *c, int j, double tol, bool first_of_sweep) {
+  if (*(volatile int32_t *)&c->done) return true;
+  if (j > 0 && first_of_sweep) {
+    double prev = u2d(*(volatile unsigned long long *)&c->dmax[(j - 1) & (kRing - 1)]);
+    if (prev < tol) {
+      if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && threadIdx.y == 0) {
+        c->done = 1;
+        c->launches_done = j;
+      }
+      return true;
+    }
+  }
+  return false;
+}
+
+__device__ __forceinline__ void zero_next_slot(DevCtl *c, int j, bool first_of_sweep) {
+  if (first_of_sweep && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && threadIdx.y == 0)
+    c->dmax[(j + 1) & (kRing - 1)] = 0ull;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(FULLMASK, v, o));
+  return v;
+}
+
+// ------------------------------------------------------------- red-black sweep
+struct Row {
+  double v0, v1;     // V at x = 2p, 2p+1
+  double gx0, gx1;   // east segments
+  double gy0, gy1;   // south segments (to y+1)
+  double gz0, gz1;   // via up (to l+1)
+  double gd0, gd1;   // via down (from l-1)
+  double b0, b1;     // right-hand side
+  double id0, id1;   // 1 / d_i
+};
+
+__device__ __forceinline__ void zero_row(Row &r) {
+  r.v0 = r.v1 = r.gx0 = r.gx1 = r.gy0 = r.gy1 = r.gz0 = r.gz1 = 0.0;
+  r.gd0 = r.gd1 = r.b0 = r.b1 = r.id0 = r.id1 = 0.0;
+}
+
+__device__ __forceinline__ void load_row(Row &r, const SweepArgs &a, const double *Vin, int l, int y,
+                                         int64_t px, bool pvalid) {
+  if (pvalid && y >= 0 && y < a.d.NY) {
+    const int64_t o = (int64_t)l * a.d.layer_stride + (int64_t)y * a.d.NXP + px;
+    double2 t;
+    t = ld2(Vin + o);    r.v0 = t.x;  r.v1 = t.y;
+    t = ld2(a.gx + o);   r.gx0 = t.x; r.gx1 = t.y;
+    t = ld2(a.gy + o);   r.gy0 = t.x; r.gy1 = t.y;
+    t = ld2(a.gz + o);   r.gz0 = t.x; r.gz1 = t.y;
+    if (l > 0) {
+      t = ld2(a.gz + o - a.d.layer_stride); r.gd0 = t.x; r.gd1 = t.y;
+    } else {
+      r.gd0 = r.gd1 = 0.0;
+    }
+    t = ld2(a.b + o);    r.b0 = t.x;  r.b1 = t.y;
+    t = ld2(a.invd + o); r.id0 = t.x; r.id1 = t.y;
+  } else {
+    zero_row(r);
+  }
+}
+
+// One full red-black SOR sweep in a single streaming pass over y.
+// CTA = (32 lanes) x (L layers); lane i owns x-pair p = 30*bx - 1 + i of its
+// layer; lanes 0/31 are halo pairs.  Iteration y updates red(y) then black(y-1):
+// red(y) needs black_old at y-1, y, y+1 (registers / shuffles / smem for l+-1);
+// black(y-1) needs red_new at y-2, y-1, y.  Reads V from Vin, writes Vout
+// (ping-pong), so CTAs never race and the result equals the sequential
+// red-then-black sweep exactly.
+__global__ void __launch_bounds__(256) k_rb_sweep(SweepArgs a) {
+  __shared__ double sb[2][kMaxLayers][kLanes];
+  __shared__ double sr[2][kMaxLayers][kLanes];
+  __shared__ double wmax[kMaxLayers];
+  const int lane = threadIdx.x, l = threadIdx.y, L = a.d.L;
+  if (sweep_skip(a.ctl, a.launch_idx, a.tol, true)) return;
+  zero_next_slot(a.ctl, a.launch_idx, true);
+
+  const int par = (*(volatile int32_t *)&a.ctl->base + a.launch_idx) & 1;
+  const double *Vin = par ? a.V1 : a.V0;
+  double *Vout = par ? a.V0 : a.V1;
+  const int p = blockIdx.x * kInterior - 1 + lane;
+  const bool pvalid = p >= 0 && 2 * (int64_t)p < a.d.NXP;
+  const bool interior = lane >= 1 && lane <= kInterior && pvalid;
+  const int64_t px = 2 * (int64_t)p;
+  const bool x0ok = px < a.d.NX, x1ok = px + 1 < a.d.NX;
+  const int ys = blockIdx.y * a.rows_per_cta;
+  const int ye = min(ys + a.rows_per_cta, a.d.NY);
+  const double w = a.omega;
+
+  Row rm2, rm1, r0, rp1, rp2;
+  zero_row(rm2);
+  load_row(rm1, a, Vin, l, ys - 2, px, pvalid);
+  load_row(r0, a, Vin, l, ys - 1, px, pvalid);
+  load_row(rp1, a, Vin, l, ys, px, pvalid);
+  double dmax = 0.0;
+  int it = 0;
+  for (int y = ys - 1; y <= ye; ++y, ++it) {
+    load_row(rp2, a, Vin, l, y + 2, px, pvalid);
+    const int er = (l + y) & 1;  // red element of the pair at row y (warp-uniform)
+    const int cur = it & 1;
+    // ---- red(y): publish black_old(y) for the layers l+-1
+    sb[cur][l][lane] = er ? r0.v0 : r0.v1;
+    __syncthreads();
+    {
+      const double up_v1 = __shfl_up_sync(FULLMASK, r0.v1, 1);
+      const double up_gx1 = __shfl_up_sync(FULLMASK, r0.gx1, 1);
+      const double dn_v0 = __shfl_down_sync(FULLMASK, r0.v0, 1);
+      const double VU = (l + 1 < L) ? sb[cur][l + 1][lane] : 0.0;
+      const double VD = (l > 0) ? sb[cur][l - 1][lane] : 0.0;
+      double Vc, s, id;
+      bool xok;
+      if (er == 0) {
+        Vc = r0.v0; id = r0.id0; xok = x0ok;
+        s = r0.b0;
+        s = fma(up_gx1, up_v1, s);
+        s = fma(r0.gx0, r0.v1, s);
+        s = fma(rm1.gy0, rm1.v0, s);
+        s = fma(r0.gy0, rp1.v0, s);
+        s = fma(r0.gz0, VU, s);
+        s = fma(r0.gd0, VD, s);
+      } else {
+        Vc = r0.v1; id = r0.id1; xok = x1ok;
+        s = r0.b1;
+        s = fma(r0.gx0, r0.v0, s);
+        s = fma(r0.gx1, dn_v0, s);
+        s = fma(rm1.gy1, rm1.v1, s);
+        s = fma(r0.gy1, rp1.v1, s);
+        s = fma(r0.gz1, VU, s);
+        s = fma(r0.gd1, VD, s);
+      }
+      double vn = fma(w, s * id - Vc, Vc);
+      if (!xok) vn = Vc;
+      if (er == 0) r0.v0 = vn; else r0.v1 = vn;
+      if (interior && xok && y >= ys && y < ye) dmax = fmax(dmax, fabs(vn - Vc));
+      sr[cur][l][lane] = vn;
+    }
+    // ---- black(y-1): red_new of l+-1 at row y-1 was published last iteration
+    if (y - 1 >= ys) {
+      const int pv = cur ^ 1;
+      const double up_v1 = __shfl_up_sync(FULLMASK, rm1.v1, 1);
+      const double up_gx1 = __shfl_up_sync(FULLMASK, rm1.gx1, 1);
+      const double dn_v0 = __shfl_down_sync(FULLMASK, rm1.v0, 1);
+      const double RU = (l + 1 < L) ? sr[pv][l + 1][lane] : 0.0;
+      const double RD = (l > 0) ? sr[pv][l - 1][lane] : 0.0;
+      double Vc, s, id;
+      bool xok;
+      if (er == 0) {  // black element of row y-1 is element er
+        Vc = rm1.v0; id = rm1.id0; xok = x0ok;
+        s = rm1.b0;
+        s = fma(up_gx1, up_v1, s);
+        s = fma(rm1.gx0, rm1.v1, s);
+        s = fma(rm2.gy0, rm2.v0, s);
+        s = fma(rm1.gy0, r0.v0, s);
+        s = fma(rm1.gz0, RU, s);
+        s = fma(rm1.gd0, RD, s);
+      } else {
+        Vc = rm1.v1; id = rm1.id1; xok = x1ok;
+        s = rm1.b1;
+        s = fma(rm1.gx0, rm1.v0, s);
+        s = fma(rm1.gx1, dn_v0, s);
+        s = fma(rm2.gy1, rm2.v1, s);
+        s = fma(rm1.gy1, r0.v1, s);
+        s = fma(rm1.gz1, RU, s);
+        s = fma(rm1.gd1, RD, s);
+      }
+      double vn = fma(w, s * id - Vc, Vc);
+      if (!xok) vn = Vc;
+      if (er == 0) rm1.v0 = vn; else rm1.v1 = vn;
+      if (interior && xok) dmax = fmax(dmax, fabs(vn - Vc));
+      if (interior)
+        st2(Vout + (int64_t)l * a.d.layer_stride + (int64_t)(y - 1) * a.d.NXP + px, rm1.v0, rm1.v1);
+    }
+    rm2 = rm1;
+    rm1 = r0;
+    r0 = rp1;
+    rp1 = rp2;
+  }
+  dmax = warp_max(dmax);
+  if (lane == 0) wmax[l] = dmax;
+  __syncthreads();
+  if (l == 0 && lane == 0) {
+    double m = 0.0;
+    for (int k = 0; k < L; ++k) m = fmax(m, wmax[k]);
+    atomicMax(&a.ctl->dmax[a.launch_idx & (kRing - 1)], d2u(m));
+  }
+}
+
+// ------------------------------------------------------------ Jacobi (mesh)
+__global__ void __launch_bounds__(256) k_jacobi_mesh(SweepArgs a) {
+  __shared__ double wmax[8];
+  if (sweep_skip(a.ctl, a.launch_idx, a.tol, true)) return;
+  zero_next_slot(a.ctl, a.launch_idx, true);
+  const MeshDims d = a.d;
+  const int par = (*(volatile int32_t *)&a.ctl->base + a.launch_idx) & 1;
+  const double *Vin = par ? a.V1 : a.V0;
+  double *Vout = par ? a.V0 : a.V1;
+  const int64_t pairs = d.np / 2;
+  const double w = a.omega;
+  double dmax = 0.0;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < pairs;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = 2 * q;
+    const int64_t l = o / d.layer_stride;
+    const int64_t rem = o - l * d.layer_stride;
+    const int64_t y = rem / d.NXP;
+    const int64_t x = rem - y * d.NXP;
+    const double2 v = ld2(Vin + o), gx = ld2(a.gx + o), gy = ld2(a.gy + o), gz = ld2(a.gz + o);
+    const double2 bb = ld2(a.b + o), id = ld2(a.invd + o);
+    const double VW = x > 0 ? __ldg(Vin + o - 1) : 0.0, gW = x > 0 ? __ldg(a.gx + o - 1) : 0.0;
+    const double VE = x + 2 < d.NXP ? __ldg(Vin + o + 2) : 0.0;
+    double2 VN = make_double2(0, 0), gN = make_double2(0, 0), VS = make_double2(0, 0);
+    double2 VU = make_double2(0, 0), VD = make_double2(0, 0), gD = make_double2(0, 0);
+    if (y > 0) { VN = ld2(Vin + o - d.NXP); gN = ld2(a.gy + o - d.NXP); }
+    if (y + 1 < d.NY) VS = ld2(Vin + o + d.NXP);
+    if (l + 1 < d.L) VU = ld2(Vin + o + d.layer_stride);
+    if (l > 0) { VD = ld2(Vin + o - d.layer_stride); gD = ld2(a.gz + o - d.layer_stride); }
+    double s0 = bb.x, s1 = bb.y;
+    s0 = fma(gW, VW, s0);     s1 = fma(gx.x, v.x, s1);
+    s0 = fma(gx.x, v.y, s0);  s1 = fma(gx.y, VE, s1);
+    s0 = fma(gN.x, VN.x, s0); s1 = fma(gN.y, VN.y, s1);
+    s0 = fma(gy.x, VS.x, s0); s1 = fma(gy.y, VS.y, s1);
+    s0 = fma(gz.x, VU.x, s0); s1 = fma(gz.y, VU.y, s1);
+    s0 = fma(gD.x, VD.x, s0); s1 = fma(gD.y, VD.y, s1);
+    double n0 = fma(w, s0 * id.x - v.x, v.x);
+    double n1 = fma(w, s1 * id.y - v.y, v.y);
+    if (x >= d.NX) n0 = v.x; else dmax = fmax(dmax, fabs(n0 - v.x));
+    if (x + 1 >= d.NX) n1 = v.y; else dmax = fmax(dmax, fabs(n1 - v.y));
+    st2(Vout + o, n0, n1);
+  }
+  dmax = warp_max(dmax);
+  const int wid = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) wmax[wid] = dmax;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) m = fmax(m, wmax[k]);
+    atomicMax(&a.ctl->dmax[a.launch_idx & (kRing - 1)], d2u(m));
+  }
+}
+
+// ------------------------------------------------------------------ CSR sweeps
+struct CsrArgs {
+  const int64_t *rowptr;
+  const int32_t *col;
+  const double *val, *b, *invd;
+  double *V0, *V1;  // GS: in place on V[base]; Jacobi: V[(base+j)&1] -> the other
+  int64_t r0, r1;   // rows of this colour (GS) / all rows (Jacobi)
+  double omega, tol;
+  int32_t launch_idx;
+  int32_t first;    // first colour of the sweep
+  DevCtl *ctl;
+};
+
+__global__ void __launch_bounds__(256) k_csr_sweep(CsrArgs a) {
+  __shared__ double wmax[8];
+  if (sweep_skip(a.ctl, a.launch_idx, a.tol, a.first != 0)) return;
+  zero_next_slot(a.ctl, a.launch_idx, a.first != 0);
+  double *V = (*(volatile int32_t *)&a.ctl->base) ? a.V1 : a.V0;
+  double dmax = 0.0;
+  for (int64_t i = a.r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.r1;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double s = a.b[i];
+    const int64_t k1 = a.rowptr[i + 1];
+    for (int64_t k = a.rowptr[i]; k < k1; ++k) s = fma(__ldg(a.val + k), V[__ldg(a.col + k)], s);
+    const double vc = V[i];
+    const double vn = fma(a.omega, s * a.invd[i] - vc, vc);
+    V[i] = vn;
+    dmax = fmax(dmax, fabs(vn - vc));
+  }
+  dmax = warp_max(dmax);
+  if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = dmax;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) m = fmax(m, wmax[k]);
+    atomicMax(&a.ctl->dmax[a.launch_idx & (kRing - 1)], d2u(m));
+  }
+}
+
+__global__ void __launch_bounds__(256) k_csr_jacobi(CsrArgs a) {
+  __shared__ double wmax[8];
+  if (sweep_skip(a.ctl, a.launch_idx, a.tol, true)) return;
+  zero_next_slot(a.ctl, a.launch_idx, true);
+  const int par = (*(volatile int32_t *)&a.ctl->base + a.launch_idx) & 1;
+  const double *Vin = par ? a.V1 : a.V0;
+  double *Vout = par ? a.V0 : a.V1;
+  double dmax = 0.0;
+  for (int64_t i = a.r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.r1;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double s = __ldg(a.b + i);
+    const int64_t k1 = a.rowptr[i + 1];
+    for (int64_t k = a.rowptr[i]; k < k1; ++k) s = fma(__ldg(a.val + k), __ldg(Vin + __ldg(a.col + k)), s);
+    const double vc = __ldg(Vin + i);
+    const double vn = fma(a.omega, s * __ldg(a.invd + i) - vc, vc);
+    Vout[i] = vn;
+    dmax = fmax(dmax, fabs(vn - vc));
+  }
+  dmax = warp_max(dmax);
+  if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = dmax;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) m = fmax(m, wmax[k]);
+    atomicMax(&a.ctl->dmax[a.launch_idx & (kRing - 1)], d2u(m));
+  }
+}
+
+// ------------------------------------------------------------------ RHS (fused)
+// b_i = (C_i/h) x_i(t) - [RLC] sum_vias alpha i(t)   (+ pads / loads below)
+__global__ void k_rhs_dense(int64_t np, const double *__restrict__ cap, double inv_h,
+                            double *V0, double *V1, DevCtl *ctl, double *__restrict__ b,
+                            const double *__restrict__ lz, const double *__restrict__ gze,
+                            const double *__restrict__ iz, int64_t layer_stride, int32_t L) {
+  const double *V = ctl->base ? V1 : V0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ctl->done = 0;
+    ctl->launches_done = 0;
+    ctl->dmax[0] = 0ull;
+  }
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < np;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double bb = cap[i] * inv_h * V[i];
+    if (lz != nullptr) {
+      const int64_t l = i / layer_stride;
+      if (l + 1 < L) bb -= lz[i] * inv_h * gze[i] * iz[i];           // current leaving down->up
+      if (l > 0) {
+        const int64_t j = i - layer_stride;
+        bb += lz[j] * inv_h * gze[j] * iz[j];                          // current arriving from below
+      }
+    }
+    b[i] = bb;
+  }
+}
+
+__global__ void k_rhs_pads(int64_t ngrp, const int64_t *__restrict__ grp, const int64_t *__restrict__ idx,
+                           const double *__restrict__ ge, const double *__restrict__ pl,
+                           const double *__restrict__ pi, double vdd, double inv_h, double *b) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < ngrp;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    double bb = 0.0;
+    for (int64_t k = grp[q]; k < grp[q + 1]; ++k) {
+      bb += ge[k] * vdd;
+      if (pl != nullptr) bb -= pl[k] * inv_h * ge[k] * pi[k];
+    }
+    b[idx[grp[q]]] += bb;
+  }
+}
+
+__device__ __forceinline__ double pwl_eval(const double *t, const double *v, int64_t s, int64_t e,
+                                           double tt) {
+  if (tt <= t[s]) return v[s];
+  if (tt >= t[e - 1]) return v[e - 1];
+  for (int64_t k = s; k + 1 < e; ++k) {
+    if (tt <= t[k + 1]) {
+      const double w = (tt - t[k]) / (t[k + 1] - t[k]);
+      return v[k] + w * (v[k + 1] - v[k]);
+    }
+  }
+  return v[e - 1];
+}
+
+__global__ void k_rhs_src(int64_t ngrp, const int64_t *__restrict__ grp, const int64_t *__restrict__ idx,
+                          const int64_t *__restrict__ ptr, const double *__restrict__ pt,
+                          const double *__restrict__ pv, double tt, double *b) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < ngrp;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    double bb = 0.0;
+    for (int64_t k = grp[q]; k < grp[q + 1]; ++k) bb += pwl_eval(pt, pv, ptr[k], ptr[k + 1], tt);
+    b[idx[grp[q]]] -= bb;
+  }
+}
+
+// -------------------------------------------------------------- per-h setup
+__global__ void k_setup_gze(int64_t np, const double *gz, const double *lz, double h, double *gze) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < np;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double g = gz[i];
+    gze[i] = (lz != nullptr && lz[i] > 0.0 && g > 0.0) ? 1.0 / (1.0 / g + lz[i] / h) : g;
+  }
+}
+
+__global__ void k_setup_pad_ge(int64_t npad, const double *pg, const double *pl, double h, double *ge) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < npad;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    ge[k] = (pl != nullptr && pl[k] > 0.0) ? 1.0 / (1.0 / pg[k] + pl[k] / h) : pg[k];
+  }
+}
+
+// d_i = sum of branch conductances + C_i/h (pads added by k_diag_pads)
+__global__ void k_diag_mesh(MeshDims d, const double *gx, const double *gy, const double *gze,
+                            const double *cap, double inv_h, double *out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.np;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t l = i / d.layer_stride;
+    const int64_t rem = i - l * d.layer_stride;
+    const int64_t y = rem / d.NXP;
+    const int64_t x = rem - y * d.NXP;
+    double s = gx[i] + gy[i] + gze[i];
+    if (x > 0) s += gx[i - 1];
+    if (y > 0) s += gy[i - d.NXP];
+    if (l > 0) s += gze[i - d.layer_stride];
+    s += cap[i] * inv_h;
+    out[i] = s;
+  }
+}
+
+__global__ void k_diag_csr(int64_t n, const int64_t *rowptr, const double *val, const double *cap,
+                           double inv_h, double *out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int64_t k = rowptr[i]; k < rowptr[i + 1]; ++k) s += val[k];
+    out[i] = s + cap[i] * inv_h;
+  }
+}
+
+__global__ void k_diag_pads(int64_t ngrp, const int64_t *grp, const int64_t *idx, const double *ge,
+                            double *d) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < ngrp;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int64_t k = grp[q]; k < grp[q + 1]; ++k) s += ge[k];
+    d[idx[grp[q]]] += s;
+  }
+}
+
+// invd = 1/d for real nodes (mesh padding -> 0); flags d <= 0 on real nodes
+__global__ void k_invert(int64_t np, double *d, int32_t NX, int32_t NXP, DevCtl *ctl) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < np;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const bool real = NXP == 0 || (i % NXP) < NX;
+    const double v = d[i];
+    if (real && !(v > 0.0)) ctl->diag_bad = 1;
+    d[i] = real && v > 0.0 ? 1.0 / v : 0.0;
+  }
+}
+
+// ----------------------------------------------------- companion current update
+// i(t+h) = g_e (v_a - v_b)(t+h) + (L/h) g_e i(t)  (backward Euler on R i + L di/dt = v)
+__global__ void k_ind_update_mesh(MeshDims d, const double *V0, const double *V1, const DevCtl *ctl,
+                                  const double *gze, const double *lz, double inv_h, double *iz) {
+  const double *V = ctl->base ? V1 : V0;
+  const int64_t n = d.np - d.layer_stride;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double L = lz[i];
+    if (L > 0.0) {
+      const double ge = gze[i];
+      iz[i] = ge * (V[i] - V[i + d.layer_stride]) + L * inv_h * ge * iz[i];
+    }
+  }
+}
+
+__global__ void k_ind_update_pads(int64_t npad, const int64_t *idx, const double *ge, const double *pl,
+                                  const double *V0, const double *V1, const DevCtl *ctl, double vdd,
+                                  double inv_h, double *pi) {
+  const double *V = ctl->base ? V1 : V0;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < npad;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const double L = pl[k];
+    if (L > 0.0) pi[k] = ge[k] * (V[idx[k]] - vdd) + L * inv_h * ge[k] * pi[k];
+  }
+}
+
+// ------------------------------------------------------------------ bookkeeping
+__global__ void k_step_end(DevCtl *c, int64_t s, int32_t launched, int32_t flips, int32_t fused,
+                           int64_t max_sweeps, double tol, int64_t *rec) {
+  const int64_t ran = c->done ? c->launches_done : launched;
+  int64_t sw = ran * fused;
+  if (sw > max_sweeps) sw = max_sweeps;
+  if (flips) c->base ^= (int32_t)(ran & 1);
+  rec[s] = sw;
+  c->sweeps_total += sw;
+  if (sw > c->sweeps_max) c->sweeps_max = sw;
+  const double last = ran > 0 ? u2d(c->dmax[(ran - 1) & (kRing - 1)]) : 0.0;
+  c->last_delta = last;
+  const bool conv = c->done || (ran > 0 && last < tol);
+  if (!conv && tol > 0.0 && c->failed == 0) c->failed = (int32_t)s;
+}
+
+__global__ void k_probe(const double *V0, const double *V1, const DevCtl *c, const int64_t *idx,
+                        int64_t n, double *out) {
+  const double *V = c->base ? V1 : V0;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    out[k] = V[idx[k]];
+}
+
+__global__ void k_gather_mesh(MeshDims d, const double *V0, const double *V1, const DevCtl *c,
+                              int64_t n, double *dst) {
+  const double *V = c == nullptr ? V0 : (c->base ? V1 : V0);
+  const int64_t per_layer = (int64_t)d.NY * d.NX;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t l = k / per_layer;
+    const int64_t r = k - l * per_layer;
+    const int64_t y = r / d.NX;
+    const int64_t x = r - y * d.NX;
+    dst[k] = V[l * d.layer_stride + y * d.NXP + x];
+  }
+}
+
+__global__ void k_scatter_mesh(MeshDims d, const double *src, int64_t n, double *dst) {
+  const int64_t per_layer = (int64_t)d.NY * d.NX;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t l = k / per_layer;
+    const int64_t r = k - l * per_layer;
+    const int64_t y = r / d.NX;
+    const int64_t x = r - y * d.NX;
+    dst[l * d.layer_stride + y * d.NXP + x] = src[k];
+  }
+}
+
+__global__ void k_gather_perm(const int64_t *iperm, const double *V0, const double *V1,
+                              const DevCtl *c, int64_t n, double *dst) {
+  const double *V = c == nullptr ? V0 : (c->base ? V1 : V0);
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    dst[k] = V[iperm[k]];
+}
+
+__global__ void k_scatter_perm(const int64_t *iperm, const double *src, int64_t n, double *dst) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    dst[iperm[k]] = src[k];
+}
+
+__global__ void k_reset_state(DevCtl *c) {
+  c->base = 0;
+  c->done = 0;
+  c->failed = 0;
+  c->sweeps_total = 0;
+  c->sweeps_max = 0;
+  c->last_delta = 0.0;
+  c->launches_done = 0;
+  for (int k = 0; k < kRing; ++k) c->dmax[k] = 0ull;
+}
+
+// ================================================================= launchers
+static inline int grid_for(int64_t work, int block, int num_sms) {
+  int64_t g = (work + block - 1) / block;
+  const int64_t cap = (int64_t)num_sms * 16;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+int sweeps_per_launch(pg_grid *g, int method) {
+  (void)g;
+  (void)method;
+  return 1;
+}
+
+cudaError_t launch_setup(pg_grid *g, double h) {
+  const double inv_h = 1.0 / h;
+  const int B = 256;
+  if (g->kind == 0) {
+    k_setup_gze<<<grid_for(g->np, B, g->num_sms), B, 0, g->stream>>>(g->np, g->gz, g->lz, h, g->gze);
+    k_diag_mesh<<<grid_for(g->np, B, g->num_sms), B, 0, g->stream>>>(g->md, g->gx, g->gy, g->gze,
+                                                                      g->cap, inv_h, g->invd);
+  } else {
+    k_diag_csr<<<grid_for(g->np, B, g->num_sms), B, 0, g->stream>>>(g->np, g->rowptr, g->val, g->cap,
+                                                                     inv_h, g->invd);
+  }
+  if (g->npad > 0) {
+    k_setup_pad_ge<<<grid_for(g->npad, B, g->num_sms), B, 0, g->stream>>>(g->npad, g->pad_g, g->pad_l,
+                                                                            h, g->pad_ge);
+    k_diag_pads<<<grid_for(g->npad_grp, B, g->num_sms), B, 0, g->stream>>>(
+        g->npad_grp, g->pad_grp, g->pad_idx, g->pad_ge, g->invd);
+  }
+  k_invert<<<grid_for(g->np, B, g->num_sms), B, 0, g->stream>>>(
+      g->np, g->invd, g->kind == 0 ? g->md.NX : 0, g->kind == 0 ? g->md.NXP : 0, g->ctl);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rhs(pg_grid *g, double h, int64_t s) {
+  const double inv_h = 1.0 / h;
+  const int B = 256;
+  const bool rlc_vias = g->kind == 0 && g->lz != nullptr;
+  k_rhs_dense<<<grid_for(g->np, B, g->num_sms), B, 0, g->stream>>>(
+      g->np, g->cap, inv_h, g->V[0], g->V[1], g->ctl, g->b, rlc_vias ? g->lz : nullptr, g->gze,
+      g->iz, g->kind == 0 ? g->md.layer_stride : 1, g->kind == 0 ? g->md.L : 1);
+  if (g->npad > 0)
+    k_rhs_pads<<<grid_for(g->npad_grp, B, g->num_sms), B, 0, g->stream>>>(
+        g->npad_grp, g->pad_grp, g->pad_idx, g->pad_ge, g->pad_l, g->pad_i, g->vdd, inv_h, g->b);
+  if (g->nsrc > 0)
+    k_rhs_src<<<grid_for(g->nsrc_grp, B, g->num_sms), B, 0, g->stream>>>(
+        g->nsrc_grp, g->src_grp, g->src_idx, g->src_ptr, g->pwl_t, g->pwl_i, (double)s * h, g->b);
+  return cudaGetLastError();
+}
+
+static int rows_per_cta(const pg_grid *g, int strips) {
+  // target ~8 CTAs (x L warps) per SM; at least 8 rows (halo overhead 2/H)
+  const int64_t target = (int64_t)g->num_sms * 8;
+  int64_t chunks = (target + strips - 1) / strips;
+  if (chunks < 1) chunks = 1;
+  int64_t H = (g->md.NY + chunks - 1) / chunks;
+  if (H < 8) H = 8;
+  if (H > g->md.NY) H = g->md.NY;
+  return (int)H;
+}
+
+cudaError_t launch_sweep(pg_grid *g, int method, double omega, double tol, int j, int nsweeps,
+                         int64_t *launches) {
+  if (g->kind == 0) {
+    SweepArgs a;
+    a.d = g->md;
+    a.gx = g->gx; a.gy = g->gy; a.gz = g->gze; a.b = g->b; a.invd = g->invd;
+    a.omega = omega; a.tol = tol; a.ctl = g->ctl; a.launch_idx = j; a.nsweeps = nsweeps;
+    // ping-pong: launch j reads V[(base + j) & 1] with `base` the device-side parity
+    // at step start (known only on the device; the kernel reads it).
+    a.V0 = g->V[0];
+    a.V1 = g->V[1];
+    if (method == PG_METHOD_RBSOR) {
+      const int pairs = g->md.NXP / 2;
+      const int strips = (pairs + kInterior - 1) / kInterior;
+      const int H = rows_per_cta(g, strips);
+      a.rows_per_cta = H;
+      dim3 grid(strips, (g->md.NY + H - 1) / H);
+      dim3 block(kLanes, g->md.L);
+      k_rb_sweep<<<grid, block, 0, g->stream>>>(a);
+    } else {
+      a.rows_per_cta = 0;
+      k_jacobi_mesh<<<grid_for(g->np / 2, 256, g->num_sms), 256, 0, g->stream>>>(a);
+    }
+    ++*launches;
+  } else {
+    CsrArgs a;
+    a.rowptr = g->rowptr; a.col = g->col; a.val = g->val; a.b = g->b; a.invd = g->invd;
+    a.omega = omega; a.tol = tol; a.launch_idx = j; a.ctl = g->ctl;
+    a.V0 = g->V[0];
+    a.V1 = g->V[1];
+    if (method == PG_METHOD_RBSOR) {
+      for (int c = 0; c < g->ncolor; ++c) {
+        a.r0 = g->color_ptr[c];
+        a.r1 = g->color_ptr[c + 1];
+        a.first = c == 0;
+        const int64_t rows = a.r1 - a.r0;
+        k_csr_sweep<<<grid_for(rows, 256, g->num_sms), 256, 0, g->stream>>>(a);
+        ++*launches;
+      }
+    } else {
+      a.r0 = 0;
+      a.r1 = g->np;
+      a.first = 1;
+      k_csr_jacobi<<<grid_for(g->np, 256, g->num_sms), 256, 0, g->stream>>>(a);
+      ++*launches;
+    }
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_step_end(pg_grid *g, int64_t s, int launched, int flips, int fused,
+                            int64_t max_sweeps, double tol) {
+  k_step_end<<<1, 1, 0, g->stream>>>(g->ctl, s, launched, flips, fused, max_sweeps, tol, g->dev_sweeps);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_inductor_update(pg_grid *g, double h) {
+  const double inv_h = 1.0 / h;
+  const int B = 256;
+  if (g->kind == 0 && g->lz != nullptr && g->md.L > 1)
+    k_ind_update_mesh<<<grid_for(g->np - g->md.layer_stride, B, g->num_sms), B, 0, g->stream>>>(
+        g->md, g->V[0], g->V[1], g->ctl, g->gze, g->lz, inv_h, g->iz);
+  if (g->npad > 0 && g->pad_l != nullptr)
+    k_ind_update_pads<<<grid_for(g->npad, B, g->num_sms), B, 0, g->stream>>>(
+        g->npad, g->pad_idx, g->pad_ge, g->pad_l, g->V[0], g->V[1], g->ctl, g->vdd, inv_h, g->pad_i);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_probe(pg_grid *g, const int64_t *probe_idx, int64_t n_probe, double *out) {
+  if (n_probe <= 0) return cudaSuccess;
+  k_probe<<<grid_for(n_probe, 256, g->num_sms), 256, 0, g->stream>>>(g->V[0], g->V[1], g->ctl,
+                                                                      probe_idx, n_probe, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reset_state(pg_grid *g) {
+  k_reset_state<<<1, 1, 0, g->stream>>>(g->ctl);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_user(pg_grid *g, double *dst) {
+  if (g->kind == 0)
+    k_gather_mesh<<<grid_for(g->n, 256, g->num_sms), 256, 0, g->stream>>>(g->md, g->V[0], g->V[1],
+                                                                          g->ctl, g->n, dst);
+  else
+    k_gather_perm<<<grid_for(g->n, 256, g->num_sms), 256, 0, g->stream>>>(g->iperm, g->V[0], g->V[1],
+                                                                          g->ctl, g->n, dst);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scatter_user(pg_grid *g, const double *src, double *dst) {
+  if (g->kind == 0)
+    k_scatter_mesh<<<grid_for(g->n, 256, g->num_sms), 256, 0, g->stream>>>(g->md, src, g->n, dst);
+  else
+    k_scatter_perm<<<grid_for(g->n, 256, g->num_sms), 256, 0, g->stream>>>(g->iperm, src, g->n, dst);
+  return cudaGetLastError();
+}
+
+}  // namespace pgb
