@@ -1,0 +1,345 @@
+"""Benchmark: topology-based power-grid transient (arxiv 1409.7166) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--workload cfgK] [--tsteps T] [--omega w] [--method rbsor|jacobi]
+
+One bench "step" = one full pass of the hot path over the workload: a
+pg_transient call (Algorithm 1: per backward-Euler time step the fused RHS
+kernel, red-black SOR sweeps to tol = 1e-10 V, inductor update) over T time
+steps of the BASELINE.json configuration (N = 1: config 1, 4 x 1024 x 1024
+RC mesh, h = 5 ps, 500 steps).  Inputs are seeded synthetic grids with the
+BASELINE.json distributions; they are resident in HBM before
+the timed region (the ~235 MB per-sweep working set exceeds the 126 MB L2).
+
+Metric: node-sweeps per second (GNode-sweeps/s), whole job; ms per time step
+is reported in `config`.  `roofline` is for the dominant kernel (k_rb_sweep):
+algorithmic bytes per launch (56 B per node: V read + write, gx, gy, gz, b,
+1/d) / its CUDA-event duration inside the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "node-updates/sec (GNode-sweeps/s) and ms per time step; fraction of HBM roofline"
+UNIT = "GNode-sweeps/s"
+BYTES_PER_NODE_SWEEP = 56  # V r/w 16 + gx, gy, gz 24 + b 8 + invd 8
+DEFAULT_OMEGA = {0: 1.9, 1: 1.98, 2: 1.98, 3: 1.99, 4: 1.99}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", type=int, default=None, help="BASELINE.json config index")
+    ap.add_argument("--tsteps", type=int, default=None, help="time steps per bench step")
+    ap.add_argument("--omega", type=float, default=None)
+    ap.add_argument("--tol", type=float, default=1e-10)
+    ap.add_argument("--method", default="rbsor", choices=["rbsor", "jacobi"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                s, m = float(parts[0]), float(parts[1])
+            except ValueError:
+                continue
+            smax = m
+            sm.append(s)
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        load = [s for s in sm if smax and s > 0.5 * smax] or sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ workloads
+def make_grid(cfg: int):
+    import gridgen
+    return gridgen.config_grid(cfg)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """dram bytes per launch of k_rb_sweep from the committed ncu capture, if any."""
+    p = os.path.join(ROOT, "profiles", "rb_sweep_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------- oracle arm
+def oracle_sample(cfg: int, g=None, seconds: float = 12.0, omega: float = 1.98):
+    """Time the oracle (as it stands) on a bounded sample of the workload:
+    the full grid, time step 1, fixed natural-order SOR sweeps (single thread)."""
+    import numpy as np
+    from oracle import netlist, nodal, pwl
+    if g is None:
+        g = make_grid(cfg)
+    nl = netlist.from_grid(g)
+    o = nodal.NodalOracle(nl)
+    It = pwl.node_currents_table(nl, g.h, 1)
+    # calibrate sweeps to ~seconds of work
+    t0 = time.perf_counter()
+    o.transient(g.h, 1, tol=0.0, omega=omega, Itab=It, max_sweeps=2)
+    per = (time.perf_counter() - t0) / 2
+    k = max(2, int(seconds / max(per, 1e-9)))
+    t0 = time.perf_counter()
+    o.transient(g.h, 1, tol=0.0, omega=omega, Itab=It, max_sweeps=k)
+    dt = time.perf_counter() - t0
+    return {"value": g.n * k / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"config{cfg} full grid ({g.n} nodes), time step 1, {k} fixed natural-order "
+                      f"SOR sweeps (omega={omega}) in the plain-C oracle, single thread, {dt:.1f} s"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    cfg = args.workload if args.workload is not None else 1
+    g = make_grid(cfg)
+    omega = args.omega or DEFAULT_OMEGA.get(cfg, 1.9)
+    per_step = max(2.0, 60.0 / max(1, args.steps + args.warmup))
+    for _ in range(args.warmup):
+        oracle_sample(cfg, g, seconds=min(per_step, 5.0), omega=omega)
+    vals = []
+    t_all = 0.0
+    for _ in range(args.steps):
+        r = oracle_sample(cfg, g, seconds=per_step, omega=omega)
+        vals.append(r["value"])
+    v = statistics.mean(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded BASELINE.json recipe)",
+            "config": {"workload": f"config{cfg}", "nodes": g.n},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": r["sample"]},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- b200 arm
+def run_b200(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_1409_7166_b200 as P
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = args.workload if args.workload is not None else 1
+    g = make_grid(cfg)
+    T = args.tsteps or g.steps
+    omega = args.omega or DEFAULT_OMEGA.get(cfg, 1.9)
+    tol = args.tol
+    stream = torch.cuda.current_stream()
+    mk = P.Grid.from_mesh_grid if hasattr(g, "gx") else P.Grid.from_edge_grid
+    G = mk(g, device=True)
+    G.set_stream(stream)
+    G.set_option("timing", 1)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        G.transient(g.h, T, tol=tol, omega=omega, method=args.method, max_sweeps=200000)
+    clocks = ClockSampler(local)
+    barrier()
+    clocks.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    sweeps = launches = 0
+    sweep_ms = 0.0
+    sweep_launches = 0
+    sweeps_per_tstep = []
+    for _ in range(args.steps):
+        r = G.transient(g.h, T, tol=tol, omega=omega, method=args.method, max_sweeps=200000)
+        sweeps += int(r.stats.sweeps_total)
+        launches += int(r.stats.kernel_launches)
+        sweep_ms += float(r.stats.sweep_ms)
+        sweep_launches += int(r.stats.sweep_launches)
+        sweeps_per_tstep.append(r.sweeps[1:])
+    ev1.record(stream)
+    barrier()
+    ck = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    node_sweeps = float(g.n) * sweeps
+    tot = torch.tensor([node_sweeps], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tot)
+    value = float(tot.item()) / (ms_max * 1e-3) / 1e9
+
+    # roofline of the sweep kernel (per launch, 1 sweep per launch)
+    peak, peak_src = peaks()
+    avg_launch_ms = sweep_ms / max(sweep_launches, 1)
+    sweeps_per_launch = sweeps / max(sweep_launches, 1)
+    achieved = BYTES_PER_NODE_SWEEP * g.n * sweeps_per_launch / (avg_launch_ms * 1e-3) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": ncu_traffic(), "kernel": "k_rb_sweep",
+            "bytes_per_node_sweep": BYTES_PER_NODE_SWEEP, "avg_launch_us": avg_launch_ms * 1e3,
+            "sweep_share_of_step": sweep_ms / ms if ms > 0 else None, "peak_source": peak_src}
+
+    # e2e: public C-ABI call with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        pin = {}
+        for name in ("gx", "gy", "gz", "cap", "lz"):
+            a = getattr(g, name, None)
+            if a is not None:
+                pt = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+                pin[name] = pt.numpy()
+        h2d = sum(v.nbytes for v in pin.values()) + g.pad_node.nbytes + g.pad_g.nbytes
+        s = g.sources
+        h2d += s.node.nbytes + s.ptr.nbytes + s.t.nbytes + s.i.nbytes
+        out = torch.empty(g.n, dtype=torch.float64).pin_memory().numpy()
+        d2h = out.nbytes
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        e_sweeps = 0
+        for _ in range(max(1, min(args.steps, 2))):
+            if hasattr(g, "gx"):
+                H = P.Grid.mesh(g.layers, g.ny, g.nx, pin["gx"], pin["gy"], pin["gz"], pin["cap"],
+                                g.pad_node, g.pad_g, g.vdd, pin.get("lz"), g.pad_l)
+            else:
+                H = P.Grid.from_edge_grid(g)
+            H.set_stream(stream)
+            H.set_sources(s.node, s.ptr, s.t, s.i)
+            rr = H.transient(g.h, T, tol=tol, omega=omega, method=args.method, max_sweeps=200000)
+            H.voltages(out)
+            H.close()
+            e_sweeps += int(rr.stats.sweeps_total)
+        e1.record(stream)
+        barrier()
+        ems = e0.elapsed_time(e1)
+        te = torch.tensor([ems], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        nrep = max(1, min(args.steps, 2))
+        e2e = {"value": float(g.n) * e_sweeps * world / (float(te.item()) * 1e-3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": float(te.item()) / nrep}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        try:
+            cpu = oracle_sample(cfg, g, seconds=12.0, omega=omega)
+        except Exception as e:  # never let the baseline kill the line
+            cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": f"failed: {e}"}
+
+    spt = np.concatenate(sweeps_per_tstep) if sweeps_per_tstep else np.zeros(1)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded BASELINE.json recipe, gridgen)",
+            "config": {"workload": f"config{cfg}", "nodes": g.n,
+                       "mesh": [g.layers, g.ny, g.nx] if hasattr(g, "gx") else None,
+                       "h_s": g.h, "time_steps_per_bench_step": T, "tol_V": tol, "omega": omega,
+                       "method": args.method, "ms_per_time_step": ms_max / args.steps / T,
+                       "sweeps_per_time_step_mean": float(spt.mean()),
+                       "sweeps_per_time_step_max": int(spt.max()),
+                       "l2": "per-sweep working set ~56 B/node x n > 126 MB L2 (no flush needed)",
+                       "parallelism": "replicas" if world > 1 else "1 GPU"},
+            "clocks": ck, "e2e": e2e, "gpu_launches": launches, "roofline": roof,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    G.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -118,7 +118,14 @@ PG_API int pg_set_stream(pg_grid *g, void *stream);
 /* Tuning knobs (key, value); unknown keys -> PG_EINVAL.
  *   "fuse"   sweeps fused per sweep-kernel launch (temporal blocking), 1..8
  *   "batch"  sweep launches enqueued between host convergence polls, >= 1
- *   "graph"  1: drive each step's sweep batches from a captured CUDA graph  */
+ *   "graph"  1: drive each step's sweep batches from a captured CUDA graph
+ *   "kernel" mesh sweep kernel: 3 (default) optimised TMA-staged ring,
+ *            1 generic TMA ring, 2 cp.async-staged ring, 0 register streaming
+ *   "rows"   rows per CTA of the mesh sweep (0: auto)
+ *   "stages" shared-memory ring stages of the staged sweeps (0: auto;
+ *            kernel 3: 16 selects the deep ring for <= 4 layers, else 8)
+ *   "timing" 1: time every sweep launch with CUDA events (stats.sweep_ms);
+ *            adds one host synchronisation per time step                  */
 PG_API int pg_set_option(pg_grid *g, const char *key, int64_t value);
 
 typedef struct {
@@ -129,6 +136,8 @@ typedef struct {
   int64_t kernel_launches; /* kernels launched by this call */
   double last_delta;       /* max |dV| of the final sweep of the last step (V) */
   double device_ms;        /* device time of the call (CUDA events) */
+  double sweep_ms;         /* device time of the sweep launches that ran (option "timing") */
+  int64_t sweep_launches;  /* sweep-kernel launches that did work (option "timing") */
 } pg_stats;
 
 /* Algorithm 1: backward-Euler transient from x(0) at t = 0 for `steps` steps

@@ -85,6 +85,7 @@ void free_grid(pg_grid *g) {
                   g->src_ptr, g->pwl_t, g->pwl_i, g->ctl, g->dev_sweeps};
   for (void *p : ptrs)
     if (p) cudaFree(p);
+  for (cudaEvent_t e : g->tev) cudaEventDestroy(e);
   if (g->ctl_host) cudaFreeHost(g->ctl_host);
   if (g->done_host) cudaFreeHost(g->done_host);
   delete g;
@@ -315,6 +316,18 @@ PG_API int pg_set_option(pg_grid *g, const char *key, int64_t value) {
     g->batch = (int)value;
   } else if (k == "graph") {
     g->graph = value != 0;
+  } else if (k == "timing") {
+    g->timing = value != 0;
+  } else if (k == "rows") {
+    REQUIRE(value >= 0 && value <= (1 << 20), "rows must be >= 0");
+    g->rows = (int)value;
+  } else if (k == "stages") {
+    REQUIRE(value == 0 || (value >= 6 && value <= 16), "stages must be 0 (auto) or 6..16");
+    g->stages = (int)value;
+  } else if (k == "kernel") {
+    REQUIRE(value >= 0 && value <= 3,
+            "kernel must be 0 (register streaming), 1 (TMA ring), 2 (cp.async ring) or 3 (optimised TMA ring)");
+    g->kernel = (int)value;
   } else {
     set_error("unknown option: " + k);
     return PG_EINVAL;
@@ -522,17 +535,29 @@ PG_API int pg_transient(pg_grid *g, double h, int64_t steps, double tol, double 
     CK(launch_probe(g, d_pidx, n_probe, d_pout));
     ++launches;
   }
+  double sweep_ms = 0.0;
+  int64_t sweep_launches = 0;
+  auto tev = [&](int64_t k) -> cudaEvent_t {
+    while ((int64_t)g->tev.size() <= k) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+      g->tev.push_back(e);
+    }
+    return g->tev[(size_t)k];
+  };
   for (int64_t s = 1; s <= steps; ++s) {
     CK(launch_rhs(g, h, s));
     launches += 1 + (g->npad > 0) + (g->nsrc > 0);
     int64_t j = 0;
     int pending = -1;  // poll slot of the previous batch
     int slot = 0;
+    if (g->timing) CK(cudaEventRecord(tev(0), st));
     while (j < max_launch) {
       const int64_t nb = std::min<int64_t>(g->batch, max_launch - j);
       for (int64_t k = 0; k < nb; ++k) {
         const int nsw = (int)std::min<int64_t>(F, max_sweeps - (j + k) * F);
         CK(launch_sweep(g, method, omega, tol, (int)(j + k), nsw, &launches));
+        if (g->timing) CK(cudaEventRecord(tev(j + k + 1), st));
       }
       j += nb;
       if (!(tol > 0.0) || j >= max_launch) continue;
@@ -547,6 +572,18 @@ PG_API int pg_transient(pg_grid *g, double h, int64_t steps, double tol, double 
     }
     CK(launch_step_end(g, s, (int)j, flips, F, max_sweeps, tol));
     ++launches;
+    if (g->timing) {
+      CK(cudaMemcpyAsync(g->ctl_host, g->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      // launches that did work: all queued ones unless convergence was detected earlier
+      const int64_t ran = g->ctl_host->done ? g->ctl_host->launches_done : j;
+      if (ran > 0) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, tev(0), tev(ran)));
+        sweep_ms += ms;
+        sweep_launches += ran;
+      }
+    }
     if (g->rlc) {
       CK(launch_inductor_update(g, h));
       launches += 2;
@@ -574,6 +611,8 @@ PG_API int pg_transient(pg_grid *g, double h, int64_t steps, double tol, double 
     stats->kernel_launches = launches;
     stats->last_delta = c.last_delta;
     stats->device_ms = ms;
+    stats->sweep_ms = sweep_ms;
+    stats->sweep_launches = sweep_launches;
   }
   if (c.diag_bad) {
     set_error("a node has a non-positive diagonal d_i (no capacitance and no conductive path; Lemma 1)");

@@ -1,5 +1,6 @@
 // Internal declarations of the B200 power-grid transient library (not ABI).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -105,6 +106,15 @@ struct pg_grid {
   int fuse = 1;
   int batch = 8;
   int graph = 0;
+  int timing = 0;                      // per-launch events for the sweep kernel
+  int kernel = 3;                      // mesh sweep: 0 register streaming, 1 TMA ring, 2 cp.async ring, 3 optimised TMA
+  int rows = 0;                        // rows per CTA (0: auto)
+  int stages = 0;                      // TMA ring stages (0: auto)
+  size_t tma_smem_set = 0;             // dynamic smem attribute currently set
+  const void *tma_kernel_set = nullptr;  // ... and for which kernel
+  int tma_state = 0;                   // 0 unknown, 1 usable, -1 unavailable
+  CUtensorMap tmap[7];                 // V0, V1, gx, gy, gze, b, invd (encoded once)
+  std::vector<cudaEvent_t> tev;        // timing event pool
 };
 
 namespace pgb {
@@ -124,6 +134,12 @@ cudaError_t launch_reset_state(pg_grid *g);
 cudaError_t launch_gather_user(pg_grid *g, double *dst_user_order);
 cudaError_t launch_scatter_user(pg_grid *g, const double *src_user_order, double *dst_storage);
 int sweeps_per_launch(pg_grid *g, int method);
+bool tma_available(pg_grid *g);
+cudaError_t launch_rb_sweep_tma(pg_grid *g, double omega, double tol, int launch_idx, int rows_per_cta);
+int tma_stages_for(const pg_grid *g);
+cudaError_t launch_rb_sweep_v3(pg_grid *g, double omega, double tol, int launch_idx, int rows_per_cta);
+int v3_ctas_per_sm(const pg_grid *g);
+int rows_per_cta_for(const pg_grid *g, int ctas_per_sm);
 
 // host CSR construction (pg_csr_build.cpp)
 struct CsrHost {

@@ -13,9 +13,12 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "pg_internal.h"
 
 namespace pgb {
+int tma_ctas_per_sm(int L);
 
 #define FULLMASK 0xffffffffu
 
@@ -595,6 +598,9 @@ cudaError_t launch_setup(pg_grid *g, double h) {
   const int B = 256;
   if (g->kind == 0) {
     k_setup_gze<<<grid_for(g->np, B, g->num_sms), B, 0, g->stream>>>(g->np, g->gz, g->lz, h, g->gze);
+    // no via above the top layer (the staged sweeps rely on it)
+    cudaMemsetAsync(g->gze + (int64_t)(g->md.L - 1) * g->md.layer_stride, 0,
+                    sizeof(double) * g->md.layer_stride, g->stream);
     k_diag_mesh<<<grid_for(g->np, B, g->num_sms), B, 0, g->stream>>>(g->md, g->gx, g->gy, g->gze,
                                                                       g->cap, inv_h, g->invd);
   } else {
@@ -628,9 +634,12 @@ cudaError_t launch_rhs(pg_grid *g, double h, int64_t s) {
   return cudaGetLastError();
 }
 
-static int rows_per_cta(const pg_grid *g, int strips) {
-  // target ~8 CTAs (x L warps) per SM; at least 8 rows (halo overhead 2/H)
-  const int64_t target = (int64_t)g->num_sms * 8;
+int rows_per_cta_for(const pg_grid *g, int ctas_per_sm) {
+  if (g->rows > 0) return std::min(g->rows, std::max(g->md.NY, 1));
+  // target ~ctas_per_sm x (a few waves) CTAs; at least 8 rows (halo overhead 2/H)
+  const int pairs = g->md.NXP / 2;
+  const int strips = (pairs + kInterior - 1) / kInterior;
+  const int64_t target = (int64_t)g->num_sms * ctas_per_sm * 2;
   int64_t chunks = (target + strips - 1) / strips;
   if (chunks < 1) chunks = 1;
   int64_t H = (g->md.NY + chunks - 1) / chunks;
@@ -651,9 +660,28 @@ cudaError_t launch_sweep(pg_grid *g, int method, double omega, double tol, int j
     a.V0 = g->V[0];
     a.V1 = g->V[1];
     if (method == PG_METHOD_RBSOR) {
+      if (g->kernel == 3 && tma_available(g)) {
+        int H = g->rows;
+        if (H <= 0) {  // one wave: strips x chunks <= SMs x resident CTAs
+          const int strips = (g->md.NXP / 2 + kInterior - 1) / kInterior;
+          int chunks = (g->num_sms * v3_ctas_per_sm(g)) / strips;
+          if (chunks < 1) chunks = 1;
+          H = (g->md.NY + chunks - 1) / chunks;
+          if (H < 8) H = 8;
+        }
+        if (H > g->md.NY) H = g->md.NY;
+        cudaError_t e = launch_rb_sweep_v3(g, omega, tol, j, H);
+        ++*launches;
+        return e;
+      }
+      if (g->kernel >= 1 && tma_available(g)) {
+        cudaError_t e = launch_rb_sweep_tma(g, omega, tol, j, rows_per_cta_for(g, tma_ctas_per_sm(g->md.L)));
+        ++*launches;
+        return e;
+      }
       const int pairs = g->md.NXP / 2;
       const int strips = (pairs + kInterior - 1) / kInterior;
-      const int H = rows_per_cta(g, strips);
+      const int H = rows_per_cta_for(g, 4);
       a.rows_per_cta = H;
       dim3 grid(strips, (g->md.NY + H - 1) / H);
       dim3 block(kLanes, g->md.L);

@@ -44,8 +44,10 @@ def oracle_run(g, steps, tol, omega, method="gs", order="redblack", max_sweeps=2
     return r, nl
 
 
-def gpu_run(P, g, steps, tol, omega, method="rbsor", max_sweeps=200000, device=False):
+def gpu_run(P, g, steps, tol, omega, method="rbsor", max_sweeps=200000, device=False, kernel=None):
     G = P.Grid.from_mesh_grid(g, device=device) if hasattr(g, "gx") else P.Grid.from_edge_grid(g, device=device)
+    if kernel is not None:
+        G.set_option("kernel", kernel)
     n = g.n
     r = G.transient(g.h, steps, tol=tol, omega=omega, method=method, max_sweeps=max_sweeps,
                     probes=np.arange(n, dtype=np.int64), raise_on_noconv=False)
@@ -62,13 +64,15 @@ def mk(L, NY, NX, seed, rlc=False):
                              src_start=20e-12, src_width=40e-12, rlc=rlc)
 
 
+@pytest.mark.parametrize("kernel", [0, 1, 2, 3])
 @pytest.mark.parametrize("shape", SHAPES)
 @pytest.mark.parametrize("omega", [1.0, 1.7])
-def test_rb_sweep_iterates_equal_oracle(pgb, shape, omega):
+def test_rb_sweep_iterates_equal_oracle(pgb, shape, omega, kernel):
+    # kernel 0: register streaming; 1: TMA ring; 2: cp.async ring; 3: optimised TMA ring (default)
     g = mk(*shape, seed=sum(shape))
     steps, k = 6, 5
     ro, _ = oracle_run(g, steps, tol=0.0, omega=omega, max_sweeps=k)
-    rg, V = gpu_run(pgb, g, steps, tol=0.0, omega=omega, max_sweeps=k)
+    rg, V = gpu_run(pgb, g, steps, tol=0.0, omega=omega, max_sweeps=k, kernel=kernel)
     assert np.all(rg.sweeps[1:] == k)
     np.testing.assert_allclose(rg.probes, ro.V[:, :g.n], rtol=0, atol=ATOL_ITER)
     np.testing.assert_allclose(V, ro.V[-1, :g.n], rtol=0, atol=ATOL_ITER)
