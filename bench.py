@@ -32,7 +32,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "node-updates/sec (GNode-sweeps/s) and ms per time step; fraction of HBM roofline"
 UNIT = "GNode-sweeps/s"
-BYTES_PER_NODE_SWEEP = 56  # V r/w 16 + gx, gy, gz 24 + b 8 + invd 8
+BYTES_PER_NODE_PASS = 56  # V r/w 16 + gx, gy, gz 24 + b 8 + invd 8 (one streaming pass, F sweeps)
 DEFAULT_OMEGA = {0: 1.9, 1: 1.98, 2: 1.98, 3: 1.99, 4: 1.99}
 
 
@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--omega", type=float, default=None)
     ap.add_argument("--tol", type=float, default=1e-10)
     ap.add_argument("--method", default="rbsor", choices=["rbsor", "jacobi"])
+    ap.add_argument("--opt", action="append", default=[],
+                    help="library option key=value (pg_set_option), e.g. fuse=2, lag=3, kernel=4")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -129,12 +131,15 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic():
-    """dram bytes per launch of k_rb_sweep from the committed ncu capture, if any."""
+def ncu_traffic(F: int):
+    """dram bytes per launch of the sweep kernel (F sweeps per launch) from the
+    committed ncu capture of the same configuration, if any."""
     p = os.path.join(ROOT, "profiles", "rb_sweep_traffic.json")
     try:
         with open(p) as f:
-            return json.load(f).get("dram_bytes_per_launch")
+            d = json.load(f)
+        e = d.get(f"F{F}") if isinstance(d.get(f"F{F}"), dict) else None
+        return None if e is None else e.get("dram_bytes_per_launch")
     except Exception:
         return None
 
@@ -150,11 +155,14 @@ def oracle_sample(cfg: int, g=None, seconds: float = 12.0, omega: float = 1.98):
     nl = netlist.from_grid(g)
     o = nodal.NodalOracle(nl)
     It = pwl.node_currents_table(nl, g.h, 1)
-    # calibrate sweeps to ~seconds of work
+    # calibrate sweeps to ~seconds of work (difference of two runs removes setup)
     t0 = time.perf_counter()
-    o.transient(g.h, 1, tol=0.0, omega=omega, Itab=It, max_sweeps=2)
-    per = (time.perf_counter() - t0) / 2
-    k = max(2, int(seconds / max(per, 1e-9)))
+    o.transient(g.h, 1, tol=0.0, omega=omega, Itab=It, max_sweeps=1)
+    t1 = time.perf_counter()
+    o.transient(g.h, 1, tol=0.0, omega=omega, Itab=It, max_sweeps=4)
+    t2 = time.perf_counter()
+    per = max((t2 - t1) - (t1 - t0), 1e-9) / 3
+    k = max(2, int(seconds / per))
     t0 = time.perf_counter()
     o.transient(g.h, 1, tol=0.0, omega=omega, Itab=It, max_sweeps=k)
     dt = time.perf_counter() - t0
@@ -211,6 +219,9 @@ def run_b200(args):
     G = mk(g, device=True)
     G.set_stream(stream)
     G.set_option("timing", 1)
+    opts = dict(kv.split("=", 1) for kv in args.opt)
+    for k, v in opts.items():
+        G.set_option(k, int(v))
 
     def barrier():
         torch.cuda.synchronize()
@@ -250,14 +261,18 @@ def run_b200(args):
         dist.all_reduce(tot)
     value = float(tot.item()) / (ms_max * 1e-3) / 1e9
 
-    # roofline of the sweep kernel (per launch, 1 sweep per launch)
+    # roofline of the sweep kernel: one launch = one streaming pass over the
+    # grid performing F sweeps; algorithmic bytes per launch = 56 B x n
     peak, peak_src = peaks()
     avg_launch_ms = sweep_ms / max(sweep_launches, 1)
-    sweeps_per_launch = sweeps / max(sweep_launches, 1)
-    achieved = BYTES_PER_NODE_SWEEP * g.n * sweeps_per_launch / (avg_launch_ms * 1e-3) / 1e9
+    F = int(r.stats.sweeps_per_launch)
+    achieved = BYTES_PER_NODE_PASS * g.n / (avg_launch_ms * 1e-3) / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": ncu_traffic(), "kernel": "k_rb_sweep",
-            "bytes_per_node_sweep": BYTES_PER_NODE_SWEEP, "avg_launch_us": avg_launch_ms * 1e3,
+            "frac": achieved / peak, "traffic": ncu_traffic(F),
+            "kernel": "k_rb_sweep_fused" if F > 1 else "k_rb_sweep_fused<F=1>",
+            "bytes_per_node_per_launch": BYTES_PER_NODE_PASS, "sweeps_per_launch": F,
+            "bytes_per_node_sweep": BYTES_PER_NODE_PASS / F, "avg_launch_us": avg_launch_ms * 1e3,
+            "kernel_node_sweeps_per_s": g.n * F / (avg_launch_ms * 1e-3) / 1e9,
             "sweep_share_of_step": sweep_ms / ms if ms > 0 else None, "peak_source": peak_src}
 
     # e2e: public C-ABI call with host buffers (pinned), copies inside the timed region
@@ -286,6 +301,8 @@ def run_b200(args):
             else:
                 H = P.Grid.from_edge_grid(g)
             H.set_stream(stream)
+            for k, v in opts.items():
+                H.set_option(k, int(v))
             H.set_sources(s.node, s.ptr, s.t, s.i)
             rr = H.transient(g.h, T, tol=tol, omega=omega, method=args.method, max_sweeps=200000)
             H.voltages(out)
@@ -319,7 +336,7 @@ def run_b200(args):
             "config": {"workload": f"config{cfg}", "nodes": g.n,
                        "mesh": [g.layers, g.ny, g.nx] if hasattr(g, "gx") else None,
                        "h_s": g.h, "time_steps_per_bench_step": T, "tol_V": tol, "omega": omega,
-                       "method": args.method, "ms_per_time_step": ms_max / args.steps / T,
+                       "method": args.method, "options": opts, "ms_per_time_step": ms_max / args.steps / T,
                        "sweeps_per_time_step_mean": float(spt.mean()),
                        "sweeps_per_time_step_max": int(spt.max()),
                        "l2": "per-sweep working set ~56 B/node x n > 126 MB L2 (no flush needed)",

@@ -116,14 +116,14 @@ PG_API int pg_get_voltages(pg_grid *g, double *v, int mem);
 PG_API int pg_set_stream(pg_grid *g, void *stream);
 
 /* Tuning knobs (key, value); unknown keys -> PG_EINVAL.
- *   "fuse"   sweeps fused per sweep-kernel launch (temporal blocking), 1..8
+ *   "fuse"   F, sweeps fused per launch of the temporally blocked mesh sweep,
+ *            1..4 (default 2); Jacobi and CSR sweeps always run 1 per launch
+ *   "lag"    wavefront lag D (rows) between fused sweep levels: 3 (default) or 4
  *   "batch"  sweep launches enqueued between host convergence polls, >= 1
- *   "graph"  1: drive each step's sweep batches from a captured CUDA graph
- *   "kernel" mesh sweep kernel: 3 (default) optimised TMA-staged ring,
- *            1 generic TMA ring, 2 cp.async-staged ring, 0 register streaming
  *   "rows"   rows per CTA of the mesh sweep (0: auto)
- *   "stages" shared-memory ring stages of the staged sweeps (0: auto;
- *            kernel 3: 16 selects the deep ring for <= 4 layers, else 8)
+ *   "stages" shared-memory ring stages S of the mesh sweep (0: auto =
+ *            D (F-1) + 6); a (F, S, D) variant that is not compiled falls
+ *            back to the default S, then to smaller F
  *   "timing" 1: time every sweep launch with CUDA events (stats.sweep_ms);
  *            adds one host synchronisation per time step                  */
 PG_API int pg_set_option(pg_grid *g, const char *key, int64_t value);
@@ -138,6 +138,7 @@ typedef struct {
   double device_ms;        /* device time of the call (CUDA events) */
   double sweep_ms;         /* device time of the sweep launches that ran (option "timing") */
   int64_t sweep_launches;  /* sweep-kernel launches that did work (option "timing") */
+  int64_t sweeps_per_launch; /* F: sweeps fused per sweep launch (convergence tested every F sweeps) */
 } pg_stats;
 
 /* Algorithm 1: backward-Euler transient from x(0) at t = 0 for `steps` steps

@@ -45,6 +45,8 @@ def incidence(nl: Netlist):
 def system(nl: Netlist, h: float):
     """G = A_g^T 𝒢 A_g, C = A_c^T 𝒞 A_c, L = A_l^T 𝓛^{-1} A_l, G_s = A_g^T 𝒢 A_gs,
     L_s = -A_l^T 𝓛^{-1} A_ls, and the system matrix M = C/h + G + hL (Eq. (11))."""
+    if np.any(np.asarray(nl.lr) != 0):
+        raise ValueError("dense solves model series R-L with internal nodes (series_rl='node')")
     (Ag, Ags), (Ac, Acs), (Al, Als), (Ai, Ais) = incidence(nl)
     G = Ag.T @ np.diag(nl.rg) @ Ag
     C = Ac.T @ np.diag(nl.cv) @ Ac

@@ -36,10 +36,14 @@ def _scatter(r, a, b, cur):
 
 
 def inductor_currents_next(nl: Netlist, h: float, V_tph: np.ndarray, il_t: np.ndarray):
-    """I_b(t+h) = I_b(t) + (h/L_b)(v_a - v_b)(t+h) (backward Euler, Eq. (10))."""
+    """I_b(t+h) = I_b(t) + (h/L_b)(v_a - v_b)(t+h) (backward Euler, Eq. (10));
+    for a series R-L element (R_b > 0) backward Euler of R i + L di/dt = v:
+    I_b(t+h) = (v(t+h) + (L_b/h) I_b(t)) / (R_b + L_b/h)."""
     if nl.la.size == 0:
         return np.zeros(0)
-    return il_t + (h / nl.lv) * (_vals(V_tph, nl.vd, nl.la) - _vals(V_tph, nl.vd, nl.lb))
+    v = _vals(V_tph, nl.vd, nl.la) - _vals(V_tph, nl.vd, nl.lb)
+    R = np.asarray(nl.lr, dtype=np.float64)
+    return (v + (nl.lv / h) * il_t) / (R + nl.lv / h)
 
 
 def residual(nl: Netlist, h: float, V_tph: np.ndarray, V_t: np.ndarray,

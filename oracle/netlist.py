@@ -11,8 +11,13 @@ Endpoint encoding used throughout the oracle: ``j >= 0`` trivial node j,
 ``j == GROUND (-1)`` ground, ``j <= -2`` source node ``-j-2``.
 
 A "series R-L" element (pads and vias of the RLC grid, reading R7) is modelled
-exactly as the paper models inductors: an R branch and an L branch joined at an
-extra trivial node with no capacitance (the paper's Fig. 2 node model).
+by default exactly as the paper models inductors: an R branch and an L branch
+joined at an extra trivial node with no capacitance (the paper's Fig. 2 node
+model).  ``from_mesh(g, series_rl="element")`` instead keeps it as ONE inductor
+branch with a series resistance ``lr`` (backward Euler of R i + L di/dt = v,
+Eq. (8)'s inductor law with the resistor's voltage added; R7) -- the
+exact elimination of that internal node, pinned equal to it in
+tests/test_oracle_pins.py.
 """
 from __future__ import annotations
 
@@ -52,6 +57,12 @@ class Netlist:
     it: np.ndarray
     ii: np.ndarray
     n_mesh: int = 0             # first n_mesh trivial nodes are the grid's nodes
+    # series resistance (ohm) of each inductor branch (series R-L element); None = all 0
+    lr: np.ndarray = None
+
+    def __post_init__(self):
+        if self.lr is None:
+            self.lr = np.zeros(self.la.shape[0])
 
     @property
     def p(self) -> int:
@@ -70,8 +81,14 @@ def _f64(x):
     return np.asarray(x, dtype=np.float64)
 
 
-def from_mesh(g) -> Netlist:
-    """Netlist of a ``gridgen.MeshGrid`` (RC or RLC)."""
+def from_mesh(g, series_rl: str = "node") -> Netlist:
+    """Netlist of a ``gridgen.MeshGrid`` (RC or RLC).  ``series_rl``: "node"
+    (R branch + L branch through an internal node, the paper's element-wise
+    model) or "element" (one inductor branch with series resistance)."""
+    if series_rl not in ("node", "element"):
+        raise ValueError("series_rl must be 'node' or 'element'")
+    elem = series_rl == "element"
+    lrs = []
     from gridgen import mesh_to_edges
     n = g.n
     eu, ev, eg = mesh_to_edges(g)
@@ -87,19 +104,28 @@ def from_mesh(g) -> Netlist:
         ra.append(eu[plain]); rb.append(ev[plain]); rg.append(eg[plain])
         rl = keep & is_via & (via_l > 0)
         u, v, gg, ll = eu[rl], ev[rl], eg[rl], via_l[rl]
-        mid = np.arange(nxt, nxt + u.size, dtype=np.int64)
-        nxt += u.size
-        ra.append(u); rb.append(mid); rg.append(gg)       # u -R- mid
-        la.append(mid); lb.append(v); lv.append(ll)       # mid -L- v
+        if elem:
+            la.append(u); lb.append(v); lv.append(ll); lrs.append(1.0 / gg)   # u -(R+L)- v
+        else:
+            mid = np.arange(nxt, nxt + u.size, dtype=np.int64)
+            nxt += u.size
+            ra.append(u); rb.append(mid); rg.append(gg)       # u -R- mid
+            la.append(mid); lb.append(v); lv.append(ll)       # mid -L- v
+            lrs.append(np.zeros(u.size))
     else:
         ra.append(eu[keep]); rb.append(ev[keep]); rg.append(eg[keep])
     # pads to the single Vdd source node (source node 0)
     pn = _i64(g.pad_node)
     if g.pad_l is not None:
-        mid = np.arange(nxt, nxt + pn.size, dtype=np.int64)
-        nxt += pn.size
-        ra.append(pn); rb.append(mid); rg.append(_f64(g.pad_g))
-        la.append(mid); lb.append(np.full(pn.size, src(0), dtype=np.int64)); lv.append(_f64(g.pad_l))
+        to_vdd = np.full(pn.size, src(0), dtype=np.int64)
+        if elem:
+            la.append(pn); lb.append(to_vdd); lv.append(_f64(g.pad_l)); lrs.append(1.0 / _f64(g.pad_g))
+        else:
+            mid = np.arange(nxt, nxt + pn.size, dtype=np.int64)
+            nxt += pn.size
+            ra.append(pn); rb.append(mid); rg.append(_f64(g.pad_g))
+            la.append(mid); lb.append(to_vdd); lv.append(_f64(g.pad_l))
+            lrs.append(np.zeros(pn.size))
     else:
         ra.append(pn); rb.append(np.full(pn.size, src(0), dtype=np.int64)); rg.append(_f64(g.pad_g))
     cap = g.cap.reshape(-1)
@@ -112,7 +138,8 @@ def from_mesh(g) -> Netlist:
         lb=_i64(np.concatenate(lb)) if lb else np.zeros(0, np.int64),
         lv=_f64(np.concatenate(lv)) if lv else np.zeros(0),
         ia=_i64(s.node), ib=np.full(s.count, GROUND, dtype=np.int64),
-        iptr=_i64(s.ptr), it=_f64(s.t), ii=_f64(s.i), n_mesh=n)
+        iptr=_i64(s.ptr), it=_f64(s.t), ii=_f64(s.i), n_mesh=n,
+        lr=_f64(np.concatenate(lrs)) if lrs else None)
 
 
 def from_edges(g) -> Netlist:
@@ -132,8 +159,8 @@ def from_edges(g) -> Netlist:
         iptr=_i64(s.ptr), it=_f64(s.t), ii=_f64(s.i), n_mesh=n)
 
 
-def from_grid(g) -> Netlist:
-    return from_edges(g) if hasattr(g, "eu") else from_mesh(g)
+def from_grid(g, series_rl: str = "node") -> Netlist:
+    return from_edges(g) if hasattr(g, "eu") else from_mesh(g, series_rl)
 
 
 @dataclass
@@ -150,6 +177,7 @@ class NodeLists:
     lbr: np.ndarray       # inductor branch index
     lsgn: np.ndarray      # +1 if node i is the branch's a-end (current a->b leaves i), -1 else
     cap: np.ndarray       # C_i (ground capacitors only; assumption of Eq. (12))
+    lres: np.ndarray = None  # series resistance of the inductor branch (0: pure inductor)
 
 
 def node_lists(nl: Netlist) -> NodeLists:
@@ -175,8 +203,9 @@ def node_lists(nl: Netlist) -> NodeLists:
 
     rptr, rnbr, rg, _, _ = group(nl.ra, nl.rb, nl.rg)
     lptr, lnbr, lval, lbr, lsgn = group(nl.la, nl.lb, nl.lv)
+    lres = np.asarray(nl.lr, dtype=np.float64)[lbr] if lbr.size else np.zeros(0)
     cap = np.zeros(n)
     if np.any((nl.ca >= 0) & (nl.cb >= 0)) or np.any(nl.cb < -1) or np.any(nl.ca < 0):
         raise ValueError("nodal oracle supports node-to-ground capacitors only (Eq. (12))")
     np.add.at(cap, nl.ca, nl.cv)
-    return NodeLists(rptr, rnbr, rg, lptr, lnbr, lval, lbr, lsgn, cap)
+    return NodeLists(rptr, rnbr, rg, lptr, lnbr, lval, lbr, lsgn, cap, lres)

@@ -23,15 +23,23 @@ static double v_of(int64_t j, const double *V, const double *vd) {
   return vd[-j - 2];
 }
 
+/* Companion conductance of an inductor branch over one backward-Euler step:
+ * h/L (Eq. (14)); with a series resistance R (series R-L element, DESIGN.md
+ * R7) backward Euler of R i + L di/dt = v gives i(t+h) = v(t+h)/(R + L/h) +
+ * (L/h)/(R + L/h) i(t), i.e. conductance h/(L + R h) and history factor
+ * L/(L + R h).  R = 0 reproduces h/L and 1 exactly.                           */
+static double l_cond(double L, double R, double h) { return h / (L + R * h); }
+static double l_hist(double L, double R, double h) { return L / (L + R * h); }
+
 /* Diagonal coefficient of V_i(t+h) in Eq. (14):
  *   d_i = sum_{j in N_i^R} g_ij + h * sum_{j in N_i^L} 1/L_ij + C_i/h          */
 void oracle_diag(int64_t n, const int64_t *rptr, const double *rg,
-                 const int64_t *lptr, const double *lval, const double *cap,
-                 double h, double *d) {
+                 const int64_t *lptr, const double *lval, const double *lres,
+                 const double *cap, double h, double *d) {
   for (int64_t i = 0; i < n; ++i) {
     double s = 0.0;
     for (int64_t k = rptr[i]; k < rptr[i + 1]; ++k) s += rg[k];
-    for (int64_t k = lptr[i]; k < lptr[i + 1]; ++k) s += h / lval[k];
+    for (int64_t k = lptr[i]; k < lptr[i + 1]; ++k) s += l_cond(lval[k], lres[k], h);
     s += cap[i] / h;
     d[i] = s;
   }
@@ -45,8 +53,8 @@ void oracle_diag(int64_t n, const int64_t *rptr, const double *rg,
  * (s_ib = +1 when the branch current b leaves node i).                        */
 void oracle_known_companion(int64_t n, const int64_t *rptr, const int64_t *rnbr,
                             const double *rg, const int64_t *lptr, const int64_t *lnbr,
-                            const double *lval, const int64_t *lbr, const double *lsgn,
-                            const double *cap, const double *vd, double h,
+                            const double *lval, const double *lres, const int64_t *lbr,
+                            const double *lsgn, const double *cap, const double *vd, double h,
                             const double *Vt, const double *Iload_tph,
                             const double *il_t, double *known) {
   for (int64_t i = 0; i < n; ++i) {
@@ -54,8 +62,8 @@ void oracle_known_companion(int64_t n, const int64_t *rptr, const int64_t *rnbr,
     for (int64_t k = rptr[i]; k < rptr[i + 1]; ++k)
       if (rnbr[k] < 0) s += rg[k] * v_of(rnbr[k], Vt, vd);
     for (int64_t k = lptr[i]; k < lptr[i + 1]; ++k) {
-      if (lnbr[k] < 0) s += (h / lval[k]) * v_of(lnbr[k], Vt, vd);
-      s -= lsgn[k] * il_t[lbr[k]];
+      if (lnbr[k] < 0) s += l_cond(lval[k], lres[k], h) * v_of(lnbr[k], Vt, vd);
+      s -= lsgn[k] * (l_hist(lval[k], lres[k], h) * il_t[lbr[k]]);
     }
     s -= Iload_tph[i];
     s += (cap[i] / h) * Vt[i];
@@ -97,7 +105,7 @@ void oracle_known_second_order(int64_t n, const int64_t *rptr, const int64_t *rn
  * max_i |V_i^(k) - V_i^(k-1)|.                                                */
 double oracle_sweep(int64_t n, const int64_t *order, const int64_t *rptr,
                     const int64_t *rnbr, const double *rg, const int64_t *lptr,
-                    const int64_t *lnbr, const double *lval, double h,
+                    const int64_t *lnbr, const double *lval, const double *lres, double h,
                     const double *d, const double *known, double omega, double *V) {
   double dmax = 0.0;
   for (int64_t q = 0; q < n; ++q) {
@@ -106,7 +114,7 @@ double oracle_sweep(int64_t n, const int64_t *order, const int64_t *rptr,
     for (int64_t k = rptr[i]; k < rptr[i + 1]; ++k)
       if (rnbr[k] >= 0) s += rg[k] * V[rnbr[k]];
     for (int64_t k = lptr[i]; k < lptr[i + 1]; ++k)
-      if (lnbr[k] >= 0) s += (h / lval[k]) * V[lnbr[k]];
+      if (lnbr[k] >= 0) s += l_cond(lval[k], lres[k], h) * V[lnbr[k]];
     double vt = s / d[i];
     double vn = omega * vt + (1.0 - omega) * V[i];
     double dv = fabs(vn - V[i]);
@@ -119,7 +127,7 @@ double oracle_sweep(int64_t n, const int64_t *order, const int64_t *rptr,
 /* One (weighted) Jacobi sweep: every node from the previous iterate. */
 double oracle_jacobi(int64_t n, const int64_t *rptr, const int64_t *rnbr,
                      const double *rg, const int64_t *lptr, const int64_t *lnbr,
-                     const double *lval, double h, const double *d,
+                     const double *lval, const double *lres, double h, const double *d,
                      const double *known, double omega, const double *Vold,
                      double *Vnew) {
   double dmax = 0.0;
@@ -128,7 +136,7 @@ double oracle_jacobi(int64_t n, const int64_t *rptr, const int64_t *rnbr,
     for (int64_t k = rptr[i]; k < rptr[i + 1]; ++k)
       if (rnbr[k] >= 0) s += rg[k] * Vold[rnbr[k]];
     for (int64_t k = lptr[i]; k < lptr[i + 1]; ++k)
-      if (lnbr[k] >= 0) s += (h / lval[k]) * Vold[lnbr[k]];
+      if (lnbr[k] >= 0) s += l_cond(lval[k], lres[k], h) * Vold[lnbr[k]];
     double vt = s / d[i];
     double vn = omega * vt + (1.0 - omega) * Vold[i];
     double dv = fabs(vn - Vold[i]);
@@ -139,12 +147,14 @@ double oracle_jacobi(int64_t n, const int64_t *rptr, const int64_t *rnbr,
 }
 
 /* Companion state update after a converged step (Eq. (10), second line):
- *   I_b(t+h) = I_b(t) + (h/L_b) (V_a(t+h) - V_c(t+h))   for branch b = a -> c */
+ *   I_b(t+h) = I_b(t) + (h/L_b) (V_a(t+h) - V_c(t+h))   for branch b = a -> c
+ * (series R-L element: I_b(t+h) = l_hist I_b(t) + l_cond (V_a - V_c)).       */
 void oracle_inductor_update(int64_t nl, const int64_t *la, const int64_t *lb,
-                            const double *lv, const double *vd, double h,
+                            const double *lv, const double *lr, const double *vd, double h,
                             const double *V, double *il) {
   for (int64_t b = 0; b < nl; ++b)
-    il[b] += (h / lv[b]) * (v_of(la[b], V, vd) - v_of(lb[b], V, vd));
+    il[b] = l_hist(lv[b], lr[b], h) * il[b] +
+            l_cond(lv[b], lr[b], h) * (v_of(la[b], V, vd) - v_of(lb[b], V, vd));
 }
 
 /* Algorithm 1 (method 0: Gauss-Seidel/SOR in `order`; method 1: Jacobi).
@@ -156,9 +166,9 @@ void oracle_inductor_update(int64_t nl, const int64_t *la, const int64_t *lb,
  * Returns 0, or -(s) if step s hit max_sweeps without meeting tol.          */
 int64_t oracle_transient(int64_t n, const int64_t *order, const int64_t *rptr,
                          const int64_t *rnbr, const double *rg, const int64_t *lptr,
-                         const int64_t *lnbr, const double *lval, const int64_t *lbr,
-                         const double *lsgn, const double *cap, int64_t nind,
-                         const int64_t *la, const int64_t *lb, const double *lv,
+                         const int64_t *lnbr, const double *lval, const double *lres,
+                         const int64_t *lbr, const double *lsgn, const double *cap, int64_t nind,
+                         const int64_t *la, const int64_t *lb, const double *lv, const double *lr,
                          const double *vd, int form, int method, double h,
                          int64_t steps, double tol, double omega, int64_t max_sweeps,
                          const double *Iload, const double *V0, const double *V1,
@@ -167,7 +177,7 @@ int64_t oracle_transient(int64_t n, const int64_t *order, const int64_t *rptr,
   double *known = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
   double *tmp = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
   int64_t status = 0;
-  oracle_diag(n, rptr, rg, lptr, lval, cap, h, d);
+  oracle_diag(n, rptr, rg, lptr, lval, lres, cap, h, d);
   memcpy(Vout, V0, sizeof(double) * (size_t)n);
   int64_t s0 = 1;
   sweeps_out[0] = 0;
@@ -180,7 +190,7 @@ int64_t oracle_transient(int64_t n, const int64_t *order, const int64_t *rptr,
     const double *Vt = Vout + (s - 1) * n;
     double *Vs = Vout + s * n;
     if (form == 0)
-      oracle_known_companion(n, rptr, rnbr, rg, lptr, lnbr, lval, lbr, lsgn, cap, vd, h,
+      oracle_known_companion(n, rptr, rnbr, rg, lptr, lnbr, lval, lres, lbr, lsgn, cap, vd, h,
                              Vt, Iload + s * n, il, known);
     else
       oracle_known_second_order(n, rptr, rnbr, rg, lptr, lnbr, lval, cap, vd, h, Vt,
@@ -192,15 +202,15 @@ int64_t oracle_transient(int64_t n, const int64_t *order, const int64_t *rptr,
     do {
       ++k;
       if (method == 0) {
-        dmax = oracle_sweep(n, order, rptr, rnbr, rg, lptr, lnbr, lval, h, d, known, omega, Vs);
+        dmax = oracle_sweep(n, order, rptr, rnbr, rg, lptr, lnbr, lval, lres, h, d, known, omega, Vs);
       } else {
-        dmax = oracle_jacobi(n, rptr, rnbr, rg, lptr, lnbr, lval, h, d, known, omega, Vs, tmp);
+        dmax = oracle_jacobi(n, rptr, rnbr, rg, lptr, lnbr, lval, lres, h, d, known, omega, Vs, tmp);
         memcpy(Vs, tmp, sizeof(double) * (size_t)n);
       }
     } while (!(dmax < tol) && k < max_sweeps); /* line 8: until ||V^(k) - V^(k-1)|| < tol */
     sweeps_out[s] = k;
     if (!(dmax < tol) && status == 0) status = -s;
-    if (form == 0 && nind > 0) oracle_inductor_update(nind, la, lb, lv, vd, h, Vs, il);
+    if (form == 0 && nind > 0) oracle_inductor_update(nind, la, lb, lv, lr, vd, h, Vs, il);
   }
   free(d);
   free(known);

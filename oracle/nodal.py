@@ -81,14 +81,21 @@ class NodalOracle:
         self._rptr, self._rnbr, self._rg = _c64(a.rptr), _c64(a.rnbr), _cd(a.rg)
         self._lptr, self._lnbr, self._lval = _c64(a.lptr), _c64(a.lnbr), _cd(a.lval)
         self._lbr, self._lsgn, self._cap = _c64(a.lbr), _cd(a.lsgn), _cd(a.cap)
+        self._lres = _cd(a.lres if a.lres is not None else np.zeros(a.lval.size))
         self._la, self._lb, self._lv = _c64(nl.la), _c64(nl.lb), _cd(nl.lv)
+        self._lr = _cd(nl.lr)
+        # a dummy valid pointer for empty arrays
+        if self._lres.size == 0:
+            self._lres = np.zeros(1)
+        if self._lr.size == 0:
+            self._lr = np.zeros(1)
         self._vd = _cd(nl.vd)
 
     # -- pieces ---------------------------------------------------------------
     def diag(self, h: float) -> np.ndarray:
         d = np.zeros(self.nl.n)
         lib().oracle_diag(ctypes.c_int64(self.nl.n), _p64(self._rptr), _pd(self._rg),
-                          _p64(self._lptr), _pd(self._lval), _pd(self._cap),
+                          _p64(self._lptr), _pd(self._lval), _pd(self._lres), _pd(self._cap),
                           ctypes.c_double(h), _pd(d))
         return d
 
@@ -99,7 +106,7 @@ class NodalOracle:
         Vt, Ip = _cd(Vt), _cd(Iload_tph)
         lib().oracle_known_companion(
             ctypes.c_int64(n), _p64(self._rptr), _p64(self._rnbr), _pd(self._rg),
-            _p64(self._lptr), _p64(self._lnbr), _pd(self._lval), _p64(self._lbr),
+            _p64(self._lptr), _p64(self._lnbr), _pd(self._lval), _pd(self._lres), _p64(self._lbr),
             _pd(self._lsgn), _pd(self._cap), _pd(self._vd), ctypes.c_double(h),
             _pd(Vt), _pd(Ip), _pd(il), _pd(out))
         return out
@@ -116,14 +123,14 @@ class NodalOracle:
             dm = lib().oracle_sweep(ctypes.c_int64(n), _p64(o) if o is not None else None,
                                     _p64(self._rptr), _p64(self._rnbr), _pd(self._rg),
                                     _p64(self._lptr), _p64(self._lnbr), _pd(self._lval),
-                                    ctypes.c_double(h), _pd(d), _pd(known),
+                                    _pd(self._lres), ctypes.c_double(h), _pd(d), _pd(known),
                                     ctypes.c_double(omega), _pd(V))
             return V, dm
         Vo = _cd(V)
         Vn = np.zeros(n)
         dm = lib().oracle_jacobi(ctypes.c_int64(n), _p64(self._rptr), _p64(self._rnbr),
                                  _pd(self._rg), _p64(self._lptr), _p64(self._lnbr),
-                                 _pd(self._lval), ctypes.c_double(h), _pd(d), _pd(known),
+                                 _pd(self._lval), _pd(self._lres), ctypes.c_double(h), _pd(d), _pd(known),
                                  ctypes.c_double(omega), _pd(Vo), _pd(Vn))
         return Vn, dm
 
@@ -141,6 +148,9 @@ class NodalOracle:
             V0 = np.full(n, float(nl.vd[0]) if nl.p else 0.0)
         V0 = _cd(V0)
         f = 0 if form == "companion" else 1
+        if f == 1 and np.any(nl.lr != 0):
+            raise ValueError("the second-order form Eq. (14) has no series R-L element; "
+                             "use series_rl='node'")
         if f == 1:
             if V1 is None:
                 raise ValueError("second-order form needs V(0) and V(1) (Algorithm 1 line 1)")
@@ -152,9 +162,9 @@ class NodalOracle:
         st = lib().oracle_transient(
             ctypes.c_int64(n), _p64(o) if o is not None else None,
             _p64(self._rptr), _p64(self._rnbr), _pd(self._rg),
-            _p64(self._lptr), _p64(self._lnbr), _pd(self._lval), _p64(self._lbr),
+            _p64(self._lptr), _p64(self._lnbr), _pd(self._lval), _pd(self._lres), _p64(self._lbr),
             _pd(self._lsgn), _pd(self._cap), ctypes.c_int64(nl.la.size),
-            _p64(self._la), _p64(self._lb), _pd(self._lv), _pd(self._vd),
+            _p64(self._la), _p64(self._lb), _pd(self._lv), _pd(self._lr), _pd(self._vd),
             ctypes.c_int(f), ctypes.c_int(0 if method == "gs" else 1),
             ctypes.c_double(h), ctypes.c_int64(steps), ctypes.c_double(tol),
             ctypes.c_double(omega), ctypes.c_int64(max_sweeps), _pd(Itab), _pd(V0),

@@ -25,7 +25,8 @@ _vp = ctypes.c_void_p
 class PgStats(ctypes.Structure):
     _fields_ = [("steps_done", _i64), ("sweeps_total", _i64), ("sweeps_max", _i64),
                 ("failed_step", _i64), ("kernel_launches", _i64), ("last_delta", _dbl),
-                ("device_ms", _dbl), ("sweep_ms", _dbl), ("sweep_launches", _i64)]
+                ("device_ms", _dbl), ("sweep_ms", _dbl), ("sweep_launches", _i64),
+                ("sweeps_per_launch", _i64)]
 
 
 # name -> (restype, argtypes); must match include/pgrid.h

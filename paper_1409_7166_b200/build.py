@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libpgb200.so")
-SOURCES = ["pg_kernels.cu", "pg_sweep_tma.cu", "pg_sweep_v3.cu", "pg_api.cu", "pg_csr_build.cpp"]
+SOURCES = ["pg_kernels.cu", "pg_sweep_fused.cu", "pg_api.cu", "pg_csr_build.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",

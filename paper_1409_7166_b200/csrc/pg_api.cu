@@ -19,10 +19,10 @@ int cuda_fail(cudaError_t e, const char *what) {
   return PG_ECUDA;
 }
 
-__global__ void k_fill_real(double *x, int64_t np, int32_t NX, int32_t NXP, double v) {
+__global__ void k_fill_real(double *x, int64_t np, MeshDims d, int32_t mesh, double v) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < np;
        i += (int64_t)gridDim.x * blockDim.x)
-    x[i] = (NXP == 0 || (i % NXP) < NX) ? v : 0.0;
+    x[i] = (!mesh || mesh_col(d, i) < d.NX) ? v : 0.0;
 }
 }  // namespace pgb
 
@@ -101,7 +101,7 @@ int64_t storage_index(const pg_grid *g, int64_t k, const std::vector<int64_t> *i
     const int64_t per_layer = (int64_t)g->md.NY * g->md.NX;
     const int64_t l = k / per_layer, r = k % per_layer;
     const int64_t y = r / g->md.NX, x = r % g->md.NX;
-    return l * g->md.layer_stride + y * g->md.NXP + x;
+    return mesh_index(g->md, l, y, x);
   }
   return (*iperm_host)[(size_t)k];
 }
@@ -131,8 +131,7 @@ int common_init(pg_grid *g) {
   CK(cudaMallocHost((void **)&g->done_host, sizeof(int32_t) * 8));
   const int B = 256;
   const int grid = (int)std::min<int64_t>((g->np + B - 1) / B, (int64_t)g->num_sms * 16);
-  k_fill_real<<<std::max(grid, 1), B>>>(g->x0, g->np, g->kind == 0 ? g->md.NX : 0,
-                                        g->kind == 0 ? g->md.NXP : 0, g->vdd);
+  k_fill_real<<<std::max(grid, 1), B>>>(g->x0, g->np, g->md, g->kind == 0, g->vdd);
   CK(cudaGetLastError());
   CK(cudaMemcpy(g->V[0], g->x0, sizeof(double) * g->np, cudaMemcpyDeviceToDevice));
   CK(cudaDeviceSynchronize());
@@ -217,19 +216,26 @@ PG_API int pg_create_mesh(int32_t layers, int32_t ny, int32_t nx, const double *
   g->md.L = layers;
   g->md.NY = ny;
   g->md.NX = nx;
-  g->md.NXP = (nx + 15) / 16 * 16;
+  g->md.NXP = (nx + 63) / 64 * 64;
+  g->md.HP = g->md.NXP / 2;
   g->md.layer_stride = (int64_t)ny * g->md.NXP;
   g->md.np = (int64_t)layers * g->md.layer_stride;
   g->np = g->md.np;
   int rc;
   if ((rc = common_init(g))) return rc;
   const cudaMemcpyKind kind = mem == PG_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  double *stage = nullptr;  // user-order staging buffer, scattered into the storage layout
+  if ((rc = dalloc(&stage, n))) return rc;
+  struct StageGuard {
+    double *p;
+    ~StageGuard() { cudaFree(p); }
+  } stage_guard{stage};
   auto put = [&](double **dst, const double *src) -> int {
     int r = dalloc(dst, g->np);
     if (r) return r;
     CK(cudaMemset(*dst, 0, sizeof(double) * g->np));
-    CK(cudaMemcpy2D(*dst, sizeof(double) * g->md.NXP, src, sizeof(double) * nx, sizeof(double) * nx,
-                    (size_t)layers * ny, kind));
+    CK(cudaMemcpy(stage, src, sizeof(double) * n, kind));
+    CK(launch_scatter_user(g, stage, *dst));
     return PG_OK;
   };
   if ((rc = put(&g->gx, gx)) || (rc = put(&g->gy, gy)) || (rc = put(&g->gz, gz)) || (rc = put(&g->cap, cap)))
@@ -309,25 +315,22 @@ PG_API int pg_set_option(pg_grid *g, const char *key, int64_t value) {
   REQUIRE(g != nullptr && key != nullptr, "grid/key is NULL");
   const std::string k(key);
   if (k == "fuse") {
-    REQUIRE(value >= 1 && value <= 8, "fuse must be in 1..8");
+    REQUIRE(value >= 1 && value <= 4, "fuse must be in 1..4");
     g->fuse = (int)value;
+  } else if (k == "lag") {
+    REQUIRE(value == 3 || value == 4, "lag must be 3 or 4");
+    g->lag = (int)value;
   } else if (k == "batch") {
     REQUIRE(value >= 1 && value <= 1024, "batch must be in 1..1024");
     g->batch = (int)value;
-  } else if (k == "graph") {
-    g->graph = value != 0;
   } else if (k == "timing") {
     g->timing = value != 0;
   } else if (k == "rows") {
     REQUIRE(value >= 0 && value <= (1 << 20), "rows must be >= 0");
     g->rows = (int)value;
   } else if (k == "stages") {
-    REQUIRE(value == 0 || (value >= 6 && value <= 16), "stages must be 0 (auto) or 6..16");
+    REQUIRE(value == 0 || (value >= 6 && value <= 17), "stages must be 0 (auto) or 6..17");
     g->stages = (int)value;
-  } else if (k == "kernel") {
-    REQUIRE(value >= 0 && value <= 3,
-            "kernel must be 0 (register streaming), 1 (TMA ring), 2 (cp.async ring) or 3 (optimised TMA ring)");
-    g->kernel = (int)value;
   } else {
     set_error("unknown option: " + k);
     return PG_EINVAL;
@@ -613,6 +616,7 @@ PG_API int pg_transient(pg_grid *g, double h, int64_t steps, double tol, double 
     stats->device_ms = ms;
     stats->sweep_ms = sweep_ms;
     stats->sweep_launches = sweep_launches;
+    stats->sweeps_per_launch = F;
   }
   if (c.diag_bad) {
     set_error("a node has a non-positive diagonal d_i (no capacitance and no conductive path; Lemma 1)");

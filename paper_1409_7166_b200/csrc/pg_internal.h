@@ -27,30 +27,32 @@ struct DevCtl {
 };
 
 constexpr int kRing = 4;
+constexpr int kMaxLayers = 8;   // CTA of the mesh sweep = 32 lanes x L warps
 
-// Red-black streaming sweep geometry: a warp covers 32 x-pairs (64 nodes) of one
-// layer row; lanes 0 and 31 are halo (recomputed, never stored).
-constexpr int kLanes = 32;
-constexpr int kInterior = 30;
-constexpr int kMaxLayers = 8;   // blockDim.y = layers <= 8 (multi-warp CTA)
-
+// Mesh storage layout ("parity-split rows"), DESIGN.md §7.  Layer-major
+// [L][NY][NXP] with row pitch NXP (a multiple of 64); inside a row the even
+// columns come first and the odd columns second:
+//     node (l, y, x)  ->  l * layer_stride + y * NXP + (x & 1) * HP + (x >> 1),
+// HP = NXP / 2.  In the red-black numbering all nodes of one colour in one
+// row and layer have the same column parity, so a warp updating a colour
+// reads and writes 32 consecutive doubles (bank-conflict-free shared memory,
+// coalesced global stores).  Padding elements (x >= NX) hold zero
+// conductances, 1/d = 0 and are never updated.
 struct MeshDims {
-  int32_t L, NY, NX, NXP;   // NXP: row pitch (even, multiple of 16)
+  int32_t L, NY, NX, NXP;   // NXP: row pitch (multiple of 64)
+  int32_t HP;               // NXP / 2: half-row pitch
   int64_t layer_stride;     // NY * NXP
   int64_t np;               // L * NY * NXP
 };
 
-struct SweepArgs {
-  MeshDims d;
-  const double *gx, *gy, *gz, *b, *invd;
-  double *V0, *V1;          // ping-pong pair; launch j of a step reads V[(base + j) & 1]
-  double omega;
-  int32_t rows_per_cta;
-  int32_t nsweeps;          // sweeps fused in this launch (1 for the basic kernel)
-  int32_t launch_idx;       // index of this launch within the time step
-  double tol;
-  DevCtl *ctl;
-};
+__host__ __device__ inline int64_t mesh_index(const MeshDims &d, int64_t l, int64_t y, int64_t x) {
+  return l * d.layer_stride + y * d.NXP + (x & 1) * d.HP + (x >> 1);
+}
+// column of storage element i (may be >= NX for padding)
+__host__ __device__ inline int64_t mesh_col(const MeshDims &d, int64_t i) {
+  const int64_t o = i % d.NXP;
+  return o >= d.HP ? 2 * (o - d.HP) + 1 : 2 * o;
+}
 
 }  // namespace pgb
 
@@ -103,11 +105,10 @@ struct pg_grid {
   int64_t dev_sweeps_cap = 0;
 
   // ---- options
-  int fuse = 1;
+  int fuse = 2;                        // F: sweeps per launch of the temporally blocked mesh sweep
+  int lag = 3;                         // wavefront lag D between fused levels (3 or 4)
   int batch = 8;
-  int graph = 0;
   int timing = 0;                      // per-launch events for the sweep kernel
-  int kernel = 3;                      // mesh sweep: 0 register streaming, 1 TMA ring, 2 cp.async ring, 3 optimised TMA
   int rows = 0;                        // rows per CTA (0: auto)
   int stages = 0;                      // TMA ring stages (0: auto)
   size_t tma_smem_set = 0;             // dynamic smem attribute currently set
@@ -134,12 +135,14 @@ cudaError_t launch_reset_state(pg_grid *g);
 cudaError_t launch_gather_user(pg_grid *g, double *dst_user_order);
 cudaError_t launch_scatter_user(pg_grid *g, const double *src_user_order, double *dst_storage);
 int sweeps_per_launch(pg_grid *g, int method);
+// temporally blocked red-black sweep (pg_sweep_fused.cu)
 bool tma_available(pg_grid *g);
-cudaError_t launch_rb_sweep_tma(pg_grid *g, double omega, double tol, int launch_idx, int rows_per_cta);
-int tma_stages_for(const pg_grid *g);
-cudaError_t launch_rb_sweep_v3(pg_grid *g, double omega, double tol, int launch_idx, int rows_per_cta);
-int v3_ctas_per_sm(const pg_grid *g);
-int rows_per_cta_for(const pg_grid *g, int ctas_per_sm);
+int fused_exact_lanes(int F);
+int fused_default_stages(int L, int F, int D);
+bool fused_variant_exists(int L, int F, int S, int D);
+int fused_ctas_per_sm(int L, int S);
+cudaError_t launch_rb_sweep_fused(pg_grid *g, double omega, double tol, int j, int nsw, int F,
+                                  int S, int D, int rows_per_cta, int y_begin, int y_end, int ypar);
 
 // host CSR construction (pg_csr_build.cpp)
 struct CsrHost {

@@ -3,8 +3,8 @@
 // Hot path per backward-Euler step (Algorithm 1):
 //   k_rhs_*            fused RHS: C_i/h x_i(t) + pad G0 Vdd (+ companion history)
 //                      - PWL loads I_i(t+h)                       (Eq. (2) / (12))
-//   k_rb_sweep         red-black SOR sweep, both colours in ONE streaming pass
-//                      (Eq. (13) in red-black numbering + Eq. (15)), fused
+//   (pg_sweep_fused.cu) k_rb_sweep_fused: F red-black SOR sweeps per streaming
+//                      pass (Eq. (13) in red-black numbering + Eq. (15)), fused
 //                      warp-shuffle max|dV| reduction                  (line 7-8)
 //   k_jacobi_mesh      weighted Jacobi sweep (comparison)
 //   k_csr_sweep        multi-colour Gauss-Seidel/SOR on the CSR store (irregular grids)
@@ -18,7 +18,6 @@
 #include "pg_internal.h"
 
 namespace pgb {
-int tma_ctas_per_sm(int L);
 
 #define FULLMASK 0xffffffffu
 
@@ -64,170 +63,19 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
-// ------------------------------------------------------------- red-black sweep
-struct Row {
-  double v0, v1;     // V at x = 2p, 2p+1
-  double gx0, gx1;   // east segments
-  double gy0, gy1;   // south segments (to y+1)
-  double gz0, gz1;   // via up (to l+1)
-  double gd0, gd1;   // via down (from l-1)
-  double b0, b1;     // right-hand side
-  double id0, id1;   // 1 / d_i
+// ------------------------------------------------------------ Jacobi (mesh)
+// Weighted Jacobi (comparison baseline): every node from the previous iterate,
+// V[(base + j) & 1] -> the other buffer.  One thread per storage element.
+struct JacobiArgs {
+  MeshDims d;
+  const double *gx, *gy, *gz, *b, *invd;
+  double *V0, *V1;
+  double omega, tol;
+  int32_t launch_idx;
+  DevCtl *ctl;
 };
 
-__device__ __forceinline__ void zero_row(Row &r) {
-  r.v0 = r.v1 = r.gx0 = r.gx1 = r.gy0 = r.gy1 = r.gz0 = r.gz1 = 0.0;
-  r.gd0 = r.gd1 = r.b0 = r.b1 = r.id0 = r.id1 = 0.0;
-}
-
-__device__ __forceinline__ void load_row(Row &r, const SweepArgs &a, const double *Vin, int l, int y,
-                                         int64_t px, bool pvalid) {
-  if (pvalid && y >= 0 && y < a.d.NY) {
-    const int64_t o = (int64_t)l * a.d.layer_stride + (int64_t)y * a.d.NXP + px;
-    double2 t;
-    t = ld2(Vin + o);    r.v0 = t.x;  r.v1 = t.y;
-    t = ld2(a.gx + o);   r.gx0 = t.x; r.gx1 = t.y;
-    t = ld2(a.gy + o);   r.gy0 = t.x; r.gy1 = t.y;
-    t = ld2(a.gz + o);   r.gz0 = t.x; r.gz1 = t.y;
-    if (l > 0) {
-      t = ld2(a.gz + o - a.d.layer_stride); r.gd0 = t.x; r.gd1 = t.y;
-    } else {
-      r.gd0 = r.gd1 = 0.0;
-    }
-    t = ld2(a.b + o);    r.b0 = t.x;  r.b1 = t.y;
-    t = ld2(a.invd + o); r.id0 = t.x; r.id1 = t.y;
-  } else {
-    zero_row(r);
-  }
-}
-
-// One full red-black SOR sweep in a single streaming pass over y.
-// CTA = (32 lanes) x (L layers); lane i owns x-pair p = 30*bx - 1 + i of its
-// layer; lanes 0/31 are halo pairs.  Iteration y updates red(y) then black(y-1):
-// red(y) needs black_old at y-1, y, y+1 (registers / shuffles / smem for l+-1);
-// black(y-1) needs red_new at y-2, y-1, y.  Reads V from Vin, writes Vout
-// (ping-pong), so CTAs never race and the result equals the sequential
-// red-then-black sweep exactly.
-__global__ void __launch_bounds__(256) k_rb_sweep(SweepArgs a) {
-  __shared__ double sb[2][kMaxLayers][kLanes];
-  __shared__ double sr[2][kMaxLayers][kLanes];
-  __shared__ double wmax[kMaxLayers];
-  const int lane = threadIdx.x, l = threadIdx.y, L = a.d.L;
-  if (sweep_skip(a.ctl, a.launch_idx, a.tol, true)) return;
-  zero_next_slot(a.ctl, a.launch_idx, true);
-
-  const int par = (*(volatile int32_t *)&a.ctl->base + a.launch_idx) & 1;
-  const double *Vin = par ? a.V1 : a.V0;
-  double *Vout = par ? a.V0 : a.V1;
-  const int p = blockIdx.x * kInterior - 1 + lane;
-  const bool pvalid = p >= 0 && 2 * (int64_t)p < a.d.NXP;
-  const bool interior = lane >= 1 && lane <= kInterior && pvalid;
-  const int64_t px = 2 * (int64_t)p;
-  const bool x0ok = px < a.d.NX, x1ok = px + 1 < a.d.NX;
-  const int ys = blockIdx.y * a.rows_per_cta;
-  const int ye = min(ys + a.rows_per_cta, a.d.NY);
-  const double w = a.omega;
-
-  Row rm2, rm1, r0, rp1, rp2;
-  zero_row(rm2);
-  load_row(rm1, a, Vin, l, ys - 2, px, pvalid);
-  load_row(r0, a, Vin, l, ys - 1, px, pvalid);
-  load_row(rp1, a, Vin, l, ys, px, pvalid);
-  double dmax = 0.0;
-  int it = 0;
-  for (int y = ys - 1; y <= ye; ++y, ++it) {
-    load_row(rp2, a, Vin, l, y + 2, px, pvalid);
-    const int er = (l + y) & 1;  // red element of the pair at row y (warp-uniform)
-    const int cur = it & 1;
-    // ---- red(y): publish black_old(y) for the layers l+-1
-    sb[cur][l][lane] = er ? r0.v0 : r0.v1;
-    __syncthreads();
-    {
-      const double up_v1 = __shfl_up_sync(FULLMASK, r0.v1, 1);
-      const double up_gx1 = __shfl_up_sync(FULLMASK, r0.gx1, 1);
-      const double dn_v0 = __shfl_down_sync(FULLMASK, r0.v0, 1);
-      const double VU = (l + 1 < L) ? sb[cur][l + 1][lane] : 0.0;
-      const double VD = (l > 0) ? sb[cur][l - 1][lane] : 0.0;
-      double Vc, s, id;
-      bool xok;
-      if (er == 0) {
-        Vc = r0.v0; id = r0.id0; xok = x0ok;
-        s = r0.b0;
-        s = fma(up_gx1, up_v1, s);
-        s = fma(r0.gx0, r0.v1, s);
-        s = fma(rm1.gy0, rm1.v0, s);
-        s = fma(r0.gy0, rp1.v0, s);
-        s = fma(r0.gz0, VU, s);
-        s = fma(r0.gd0, VD, s);
-      } else {
-        Vc = r0.v1; id = r0.id1; xok = x1ok;
-        s = r0.b1;
-        s = fma(r0.gx0, r0.v0, s);
-        s = fma(r0.gx1, dn_v0, s);
-        s = fma(rm1.gy1, rm1.v1, s);
-        s = fma(r0.gy1, rp1.v1, s);
-        s = fma(r0.gz1, VU, s);
-        s = fma(r0.gd1, VD, s);
-      }
-      double vn = fma(w, s * id - Vc, Vc);
-      if (!xok) vn = Vc;
-      if (er == 0) r0.v0 = vn; else r0.v1 = vn;
-      if (interior && xok && y >= ys && y < ye) dmax = fmax(dmax, fabs(vn - Vc));
-      sr[cur][l][lane] = vn;
-    }
-    // ---- black(y-1): red_new of l+-1 at row y-1 was published last iteration
-    if (y - 1 >= ys) {
-      const int pv = cur ^ 1;
-      const double up_v1 = __shfl_up_sync(FULLMASK, rm1.v1, 1);
-      const double up_gx1 = __shfl_up_sync(FULLMASK, rm1.gx1, 1);
-      const double dn_v0 = __shfl_down_sync(FULLMASK, rm1.v0, 1);
-      const double RU = (l + 1 < L) ? sr[pv][l + 1][lane] : 0.0;
-      const double RD = (l > 0) ? sr[pv][l - 1][lane] : 0.0;
-      double Vc, s, id;
-      bool xok;
-      if (er == 0) {  // black element of row y-1 is element er
-        Vc = rm1.v0; id = rm1.id0; xok = x0ok;
-        s = rm1.b0;
-        s = fma(up_gx1, up_v1, s);
-        s = fma(rm1.gx0, rm1.v1, s);
-        s = fma(rm2.gy0, rm2.v0, s);
-        s = fma(rm1.gy0, r0.v0, s);
-        s = fma(rm1.gz0, RU, s);
-        s = fma(rm1.gd0, RD, s);
-      } else {
-        Vc = rm1.v1; id = rm1.id1; xok = x1ok;
-        s = rm1.b1;
-        s = fma(rm1.gx0, rm1.v0, s);
-        s = fma(rm1.gx1, dn_v0, s);
-        s = fma(rm2.gy1, rm2.v1, s);
-        s = fma(rm1.gy1, r0.v1, s);
-        s = fma(rm1.gz1, RU, s);
-        s = fma(rm1.gd1, RD, s);
-      }
-      double vn = fma(w, s * id - Vc, Vc);
-      if (!xok) vn = Vc;
-      if (er == 0) rm1.v0 = vn; else rm1.v1 = vn;
-      if (interior && xok) dmax = fmax(dmax, fabs(vn - Vc));
-      if (interior)
-        st2(Vout + (int64_t)l * a.d.layer_stride + (int64_t)(y - 1) * a.d.NXP + px, rm1.v0, rm1.v1);
-    }
-    rm2 = rm1;
-    rm1 = r0;
-    r0 = rp1;
-    rp1 = rp2;
-  }
-  dmax = warp_max(dmax);
-  if (lane == 0) wmax[l] = dmax;
-  __syncthreads();
-  if (l == 0 && lane == 0) {
-    double m = 0.0;
-    for (int k = 0; k < L; ++k) m = fmax(m, wmax[k]);
-    atomicMax(&a.ctl->dmax[a.launch_idx & (kRing - 1)], d2u(m));
-  }
-}
-
-// ------------------------------------------------------------ Jacobi (mesh)
-__global__ void __launch_bounds__(256) k_jacobi_mesh(SweepArgs a) {
+__global__ void __launch_bounds__(256) k_jacobi_mesh(JacobiArgs a) {
   __shared__ double wmax[8];
   if (sweep_skip(a.ctl, a.launch_idx, a.tol, true)) return;
   zero_next_slot(a.ctl, a.launch_idx, true);
@@ -235,38 +83,31 @@ __global__ void __launch_bounds__(256) k_jacobi_mesh(SweepArgs a) {
   const int par = (*(volatile int32_t *)&a.ctl->base + a.launch_idx) & 1;
   const double *Vin = par ? a.V1 : a.V0;
   double *Vout = par ? a.V0 : a.V1;
-  const int64_t pairs = d.np / 2;
   const double w = a.omega;
   double dmax = 0.0;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < pairs;
-       q += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t o = 2 * q;
-    const int64_t l = o / d.layer_stride;
-    const int64_t rem = o - l * d.layer_stride;
-    const int64_t y = rem / d.NXP;
-    const int64_t x = rem - y * d.NXP;
-    const double2 v = ld2(Vin + o), gx = ld2(a.gx + o), gy = ld2(a.gy + o), gz = ld2(a.gz + o);
-    const double2 bb = ld2(a.b + o), id = ld2(a.invd + o);
-    const double VW = x > 0 ? __ldg(Vin + o - 1) : 0.0, gW = x > 0 ? __ldg(a.gx + o - 1) : 0.0;
-    const double VE = x + 2 < d.NXP ? __ldg(Vin + o + 2) : 0.0;
-    double2 VN = make_double2(0, 0), gN = make_double2(0, 0), VS = make_double2(0, 0);
-    double2 VU = make_double2(0, 0), VD = make_double2(0, 0), gD = make_double2(0, 0);
-    if (y > 0) { VN = ld2(Vin + o - d.NXP); gN = ld2(a.gy + o - d.NXP); }
-    if (y + 1 < d.NY) VS = ld2(Vin + o + d.NXP);
-    if (l + 1 < d.L) VU = ld2(Vin + o + d.layer_stride);
-    if (l > 0) { VD = ld2(Vin + o - d.layer_stride); gD = ld2(a.gz + o - d.layer_stride); }
-    double s0 = bb.x, s1 = bb.y;
-    s0 = fma(gW, VW, s0);     s1 = fma(gx.x, v.x, s1);
-    s0 = fma(gx.x, v.y, s0);  s1 = fma(gx.y, VE, s1);
-    s0 = fma(gN.x, VN.x, s0); s1 = fma(gN.y, VN.y, s1);
-    s0 = fma(gy.x, VS.x, s0); s1 = fma(gy.y, VS.y, s1);
-    s0 = fma(gz.x, VU.x, s0); s1 = fma(gz.y, VU.y, s1);
-    s0 = fma(gD.x, VD.x, s0); s1 = fma(gD.y, VD.y, s1);
-    double n0 = fma(w, s0 * id.x - v.x, v.x);
-    double n1 = fma(w, s1 * id.y - v.y, v.y);
-    if (x >= d.NX) n0 = v.x; else dmax = fmax(dmax, fabs(n0 - v.x));
-    if (x + 1 >= d.NX) n1 = v.y; else dmax = fmax(dmax, fabs(n1 - v.y));
-    st2(Vout + o, n0, n1);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.np;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t l = i / d.layer_stride;
+    const int64_t y = (i - l * d.layer_stride) / d.NXP;
+    const int64_t x = mesh_col(d, i);
+    const double vc = __ldg(Vin + i);
+    if (x >= d.NX) {
+      Vout[i] = vc;
+      continue;
+    }
+    double s = __ldg(a.b + i);
+    if (x + 1 < d.NX) s = fma(__ldg(a.gx + i), __ldg(Vin + mesh_index(d, l, y, x + 1)), s);
+    if (x > 0) {
+      const int64_t j = mesh_index(d, l, y, x - 1);
+      s = fma(__ldg(a.gx + j), __ldg(Vin + j), s);
+    }
+    if (y + 1 < d.NY) s = fma(__ldg(a.gy + i), __ldg(Vin + i + d.NXP), s);
+    if (y > 0) s = fma(__ldg(a.gy + i - d.NXP), __ldg(Vin + i - d.NXP), s);
+    if (l + 1 < d.L) s = fma(__ldg(a.gz + i), __ldg(Vin + i + d.layer_stride), s);
+    if (l > 0) s = fma(__ldg(a.gz + i - d.layer_stride), __ldg(Vin + i - d.layer_stride), s);
+    const double vn = fma(w, s * __ldg(a.invd + i) - vc, vc);
+    Vout[i] = vn;
+    dmax = fmax(dmax, fabs(vn - vc));
   }
   dmax = warp_max(dmax);
   const int wid = threadIdx.x >> 5;
@@ -433,11 +274,10 @@ __global__ void k_diag_mesh(MeshDims d, const double *gx, const double *gy, cons
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.np;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t l = i / d.layer_stride;
-    const int64_t rem = i - l * d.layer_stride;
-    const int64_t y = rem / d.NXP;
-    const int64_t x = rem - y * d.NXP;
+    const int64_t y = (i - l * d.layer_stride) / d.NXP;
+    const int64_t x = mesh_col(d, i);
     double s = gx[i] + gy[i] + gze[i];
-    if (x > 0) s += gx[i - 1];
+    if (x > 0) s += gx[mesh_index(d, l, y, x - 1)];
     if (y > 0) s += gy[i - d.NXP];
     if (l > 0) s += gze[i - d.layer_stride];
     s += cap[i] * inv_h;
@@ -466,10 +306,10 @@ __global__ void k_diag_pads(int64_t ngrp, const int64_t *grp, const int64_t *idx
 }
 
 // invd = 1/d for real nodes (mesh padding -> 0); flags d <= 0 on real nodes
-__global__ void k_invert(int64_t np, double *d, int32_t NX, int32_t NXP, DevCtl *ctl) {
+__global__ void k_invert(int64_t np, double *d, MeshDims md, int32_t mesh, DevCtl *ctl) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < np;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const bool real = NXP == 0 || (i % NXP) < NX;
+    const bool real = !mesh || mesh_col(md, i) < md.NX;
     const double v = d[i];
     if (real && !(v > 0.0)) ctl->diag_bad = 1;
     d[i] = real && v > 0.0 ? 1.0 / v : 0.0;
@@ -537,7 +377,7 @@ __global__ void k_gather_mesh(MeshDims d, const double *V0, const double *V1, co
     const int64_t r = k - l * per_layer;
     const int64_t y = r / d.NX;
     const int64_t x = r - y * d.NX;
-    dst[k] = V[l * d.layer_stride + y * d.NXP + x];
+    dst[k] = V[mesh_index(d, l, y, x)];
   }
 }
 
@@ -549,7 +389,7 @@ __global__ void k_scatter_mesh(MeshDims d, const double *src, int64_t n, double 
     const int64_t r = k - l * per_layer;
     const int64_t y = r / d.NX;
     const int64_t x = r - y * d.NX;
-    dst[l * d.layer_stride + y * d.NXP + x] = src[k];
+    dst[mesh_index(d, l, y, x)] = src[k];
   }
 }
 
@@ -587,10 +427,36 @@ static inline int grid_for(int64_t work, int block, int num_sms) {
   return (int)g;
 }
 
+// Resolved (F, S, D) of the temporally blocked mesh sweep: the requested
+// options if that variant is compiled, else the largest compiled F <= fuse.
+struct FusedCfg {
+  int F, S, D;
+};
+static FusedCfg fused_cfg(const pg_grid *g) {
+  const int L = g->md.L;
+  for (int F = g->fuse; F >= 1; --F) {
+    const int D = g->lag;
+    if (g->stages > 0 && fused_variant_exists(L, F, g->stages, D)) return {F, g->stages, D};
+    const int S = fused_default_stages(L, F, D);
+    if (fused_variant_exists(L, F, S, D)) return {F, S, D};
+    if (fused_variant_exists(L, F, fused_default_stages(L, F, 3), 3)) return {F, fused_default_stages(L, F, 3), 3};
+  }
+  return {1, 6, 3};
+}
+
 int sweeps_per_launch(pg_grid *g, int method) {
-  (void)g;
-  (void)method;
-  return 1;
+  return (g->kind == 0 && method == PG_METHOD_RBSOR) ? fused_cfg(g).F : 1;
+}
+
+int fused_rows_per_cta(const pg_grid *g, int F, int S, int ny) {
+  if (g->rows > 0) return std::max(1, std::min(g->rows, ny));
+  const int I = fused_exact_lanes(F);
+  const int strips = (g->md.HP + I - 1) / I;
+  int chunks = (g->num_sms * fused_ctas_per_sm(g->md.L, S)) / strips;
+  if (chunks < 1) chunks = 1;
+  int H = (ny + chunks - 1) / chunks;
+  if (H < 1) H = 1;
+  return H;
 }
 
 cudaError_t launch_setup(pg_grid *g, double h) {
@@ -613,8 +479,8 @@ cudaError_t launch_setup(pg_grid *g, double h) {
     k_diag_pads<<<grid_for(g->npad_grp, B, g->num_sms), B, 0, g->stream>>>(
         g->npad_grp, g->pad_grp, g->pad_idx, g->pad_ge, g->invd);
   }
-  k_invert<<<grid_for(g->np, B, g->num_sms), B, 0, g->stream>>>(
-      g->np, g->invd, g->kind == 0 ? g->md.NX : 0, g->kind == 0 ? g->md.NXP : 0, g->ctl);
+  k_invert<<<grid_for(g->np, B, g->num_sms), B, 0, g->stream>>>(g->np, g->invd, g->md, g->kind == 0,
+                                                                  g->ctl);
   return cudaGetLastError();
 }
 
@@ -634,62 +500,23 @@ cudaError_t launch_rhs(pg_grid *g, double h, int64_t s) {
   return cudaGetLastError();
 }
 
-int rows_per_cta_for(const pg_grid *g, int ctas_per_sm) {
-  if (g->rows > 0) return std::min(g->rows, std::max(g->md.NY, 1));
-  // target ~ctas_per_sm x (a few waves) CTAs; at least 8 rows (halo overhead 2/H)
-  const int pairs = g->md.NXP / 2;
-  const int strips = (pairs + kInterior - 1) / kInterior;
-  const int64_t target = (int64_t)g->num_sms * ctas_per_sm * 2;
-  int64_t chunks = (target + strips - 1) / strips;
-  if (chunks < 1) chunks = 1;
-  int64_t H = (g->md.NY + chunks - 1) / chunks;
-  if (H < 8) H = 8;
-  if (H > g->md.NY) H = g->md.NY;
-  return (int)H;
-}
-
 cudaError_t launch_sweep(pg_grid *g, int method, double omega, double tol, int j, int nsweeps,
                          int64_t *launches) {
   if (g->kind == 0) {
-    SweepArgs a;
+    if (method == PG_METHOD_RBSOR) {
+      if (!tma_available(g)) return cudaErrorNotSupported;
+      const FusedCfg c = fused_cfg(g);
+      const int H = fused_rows_per_cta(g, c.F, c.S, g->md.NY);
+      ++*launches;
+      return launch_rb_sweep_fused(g, omega, tol, j, nsweeps, c.F, c.S, c.D, H, 0, g->md.NY, 0);
+    }
+    JacobiArgs a;
     a.d = g->md;
     a.gx = g->gx; a.gy = g->gy; a.gz = g->gze; a.b = g->b; a.invd = g->invd;
-    a.omega = omega; a.tol = tol; a.ctl = g->ctl; a.launch_idx = j; a.nsweeps = nsweeps;
-    // ping-pong: launch j reads V[(base + j) & 1] with `base` the device-side parity
-    // at step start (known only on the device; the kernel reads it).
+    a.omega = omega; a.tol = tol; a.ctl = g->ctl; a.launch_idx = j;
     a.V0 = g->V[0];
     a.V1 = g->V[1];
-    if (method == PG_METHOD_RBSOR) {
-      if (g->kernel == 3 && tma_available(g)) {
-        int H = g->rows;
-        if (H <= 0) {  // one wave: strips x chunks <= SMs x resident CTAs
-          const int strips = (g->md.NXP / 2 + kInterior - 1) / kInterior;
-          int chunks = (g->num_sms * v3_ctas_per_sm(g)) / strips;
-          if (chunks < 1) chunks = 1;
-          H = (g->md.NY + chunks - 1) / chunks;
-          if (H < 8) H = 8;
-        }
-        if (H > g->md.NY) H = g->md.NY;
-        cudaError_t e = launch_rb_sweep_v3(g, omega, tol, j, H);
-        ++*launches;
-        return e;
-      }
-      if (g->kernel >= 1 && tma_available(g)) {
-        cudaError_t e = launch_rb_sweep_tma(g, omega, tol, j, rows_per_cta_for(g, tma_ctas_per_sm(g->md.L)));
-        ++*launches;
-        return e;
-      }
-      const int pairs = g->md.NXP / 2;
-      const int strips = (pairs + kInterior - 1) / kInterior;
-      const int H = rows_per_cta_for(g, 4);
-      a.rows_per_cta = H;
-      dim3 grid(strips, (g->md.NY + H - 1) / H);
-      dim3 block(kLanes, g->md.L);
-      k_rb_sweep<<<grid, block, 0, g->stream>>>(a);
-    } else {
-      a.rows_per_cta = 0;
-      k_jacobi_mesh<<<grid_for(g->np / 2, 256, g->num_sms), 256, 0, g->stream>>>(a);
-    }
+    k_jacobi_mesh<<<grid_for(g->np, 256, g->num_sms), 256, 0, g->stream>>>(a);
     ++*launches;
   } else {
     CsrArgs a;

@@ -44,10 +44,10 @@ def oracle_run(g, steps, tol, omega, method="gs", order="redblack", max_sweeps=2
     return r, nl
 
 
-def gpu_run(P, g, steps, tol, omega, method="rbsor", max_sweeps=200000, device=False, kernel=None):
+def gpu_run(P, g, steps, tol, omega, method="rbsor", max_sweeps=200000, device=False, options=None):
     G = P.Grid.from_mesh_grid(g, device=device) if hasattr(g, "gx") else P.Grid.from_edge_grid(g, device=device)
-    if kernel is not None:
-        G.set_option("kernel", kernel)
+    for k, v in (options or {}).items():
+        G.set_option(k, v)
     n = g.n
     r = G.transient(g.h, steps, tol=tol, omega=omega, method=method, max_sweeps=max_sweeps,
                     probes=np.arange(n, dtype=np.int64), raise_on_noconv=False)
@@ -64,18 +64,49 @@ def mk(L, NY, NX, seed, rlc=False):
                              src_start=20e-12, src_width=40e-12, rlc=rlc)
 
 
-@pytest.mark.parametrize("kernel", [0, 1, 2, 3])
+@pytest.mark.parametrize("F", [1, 2])
 @pytest.mark.parametrize("shape", SHAPES)
 @pytest.mark.parametrize("omega", [1.0, 1.7])
-def test_rb_sweep_iterates_equal_oracle(pgb, shape, omega, kernel):
-    # kernel 0: register streaming; 1: TMA ring; 2: cp.async ring; 3: optimised TMA ring (default)
+def test_rb_sweep_iterates_equal_oracle(pgb, shape, omega, F):
+    # the mesh sweep with F = 1 (one sweep per launch) and the default F = 2
     g = mk(*shape, seed=sum(shape))
     steps, k = 6, 5
     ro, _ = oracle_run(g, steps, tol=0.0, omega=omega, max_sweeps=k)
-    rg, V = gpu_run(pgb, g, steps, tol=0.0, omega=omega, max_sweeps=k, kernel=kernel)
+    rg, V = gpu_run(pgb, g, steps, tol=0.0, omega=omega, max_sweeps=k, options={"fuse": F})
     assert np.all(rg.sweeps[1:] == k)
     np.testing.assert_allclose(rg.probes, ro.V[:, :g.n], rtol=0, atol=ATOL_ITER)
     np.testing.assert_allclose(V, ro.V[-1, :g.n], rtol=0, atol=ATOL_ITER)
+
+
+FUSED_SHAPES = [(2, 6, 5), (1, 1, 1), (4, 9, 70), (2, 33, 31), (8, 5, 3), (4, 40, 150), (3, 23, 64)]
+
+
+@pytest.mark.parametrize("shape", FUSED_SHAPES)
+@pytest.mark.parametrize("F,lag,rows", [(1, 3, 0), (2, 3, 0), (3, 3, 0), (4, 3, 0), (2, 4, 0), (2, 3, 7),
+                                        (3, 3, 4), (4, 3, 64)])
+def test_fused_sweep_iterates_equal_oracle(pgb, shape, F, lag, rows):
+    # F red-black SOR sweeps per streaming pass (temporal blocking);
+    # k = 5 sweeps per step exercises the partial last launch (nsw < F)
+    g = mk(*shape, seed=3 * sum(shape) + F)
+    steps, k, omega = 4, 5, 1.6
+    ro, _ = oracle_run(g, steps, tol=0.0, omega=omega, max_sweeps=k)
+    rg, V = gpu_run(pgb, g, steps, tol=0.0, omega=omega, max_sweeps=k,
+                    options={"fuse": F, "lag": lag, "rows": rows})
+    assert np.all(rg.sweeps[1:] == k)
+    np.testing.assert_allclose(rg.probes, ro.V[:, :g.n], rtol=0, atol=ATOL_ITER)
+    np.testing.assert_allclose(V, ro.V[-1, :g.n], rtol=0, atol=ATOL_ITER)
+
+
+@pytest.mark.parametrize("F", [2, 3, 4])
+def test_fused_converged_sweep_counts(pgb, F):
+    # convergence is tested after every launch (every F sweeps): the GPU stops
+    # at the first multiple of F at or after the oracle's stopping sweep
+    g = gridgen.config_grid(0, dims=(2, 40, 48), steps=15)
+    ro, _ = oracle_run(g, 15, tol=1e-10, omega=1.9)
+    rg, _ = gpu_run(pgb, g, 15, tol=1e-10, omega=1.9, options={"fuse": F})
+    np.testing.assert_allclose(rg.probes, ro.V, rtol=0, atol=ATOL_CONV)
+    expect = -(-ro.sweeps[1:] // F) * F
+    assert np.mean(rg.sweeps[1:] == expect) > 0.9
 
 
 @pytest.mark.parametrize("shape", SHAPES[:5])
@@ -110,8 +141,11 @@ def test_config0_full_size_converged(pgb):
     rg, _ = gpu_run(pgb, g, steps, tol=1e-10, omega=omega)
     assert ro.status == 0 and rg.status == 0
     np.testing.assert_allclose(rg.probes, ro.V, rtol=0, atol=ATOL_CONV)
-    # same numbering, same arithmetic up to rounding -> same sweep counts almost everywhere
-    assert np.mean(rg.sweeps == ro.sweeps) > 0.9
+    # same numbering, same arithmetic up to rounding -> same sweep counts almost
+    # everywhere (the default sweep tests convergence every F = 2 sweeps)
+    F = int(rg.stats.sweeps_per_launch)
+    assert F == 2
+    assert np.mean(rg.sweeps[1:] == -(-ro.sweeps[1:] // F) * F) > 0.9
 
 
 def test_redblack_vs_natural_order_tight(pgb):
@@ -140,9 +174,11 @@ def test_csr_grid(pgb):
 def test_zero_current_settles_to_vdd(pgb):
     g = mk(3, 17, 40, seed=1)
     g.sources = gridgen.Sources(node=np.zeros(0, np.int64), ptr=np.zeros(1, np.int64), t=np.zeros(0), i=np.zeros(0))
-    rg, V = gpu_run(pgb, g, 10, tol=1e-12, omega=1.5)
-    assert np.abs(rg.probes - 1.0).max() <= 1e-13
-    assert np.all(rg.sweeps[1:] == 1)
+    for F in (1, 2, 3):
+        rg, V = gpu_run(pgb, g, 10, tol=1e-12, omega=1.5, options={"fuse": F})
+        assert np.abs(rg.probes - 1.0).max() <= 1e-13
+        # one launch (F sweeps) per step: the first sweep already meets tol
+        assert np.all(rg.sweeps[1:] == F)
 
 
 def test_device_inputs_equal_host_inputs(pgb):
