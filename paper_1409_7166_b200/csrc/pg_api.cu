@@ -456,6 +456,24 @@ PG_API int pg_transient(pg_grid *g, double h, int64_t steps, double tol, double 
                         int64_t max_sweeps, int64_t n_probe, const int64_t *probe_node,
                         double *probe_out, int mem, int64_t *sweeps_out, pg_stats *stats) {
   REQUIRE(g != nullptr, "grid is NULL");
+  REQUIRE(!g->slab, "slab grids are driven through a pg_group (pg_group_transient)");
+  pg_grid *gs[1] = {g};
+  return pgb::run_transient(gs, 1, nullptr, h, steps, tol, omega, method, max_sweeps, n_probe,
+                            probe_node, probe_out, mem, sweeps_out, stats);
+}
+
+}  // extern "C"
+
+namespace pgb {
+
+// Algorithm 1 over ng grids advanced in lockstep on grid 0's stream (ng > 1:
+// the slabs of a partitioned mesh, `ex` refreshes their ghost rows and makes
+// the convergence norm global after every sweep launch).
+int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, double tol,
+                  double omega, int method, int64_t max_sweeps, int64_t n_probe,
+                  const int64_t *probe_node, double *probe_out, int mem, int64_t *sweeps_out,
+                  pg_stats *stats) {
+  pg_grid *g = gs[0];
   REQUIRE(h > 0.0 && std::isfinite(h), "h must be finite and > 0");
   REQUIRE(steps >= 0, "steps must be >= 0");
   REQUIRE(omega > 0.0 && omega < 2.0, "omega must be in (0, 2) (Eq. (15) convergence range)");
@@ -463,7 +481,13 @@ PG_API int pg_transient(pg_grid *g, double h, int64_t steps, double tol, double 
   REQUIRE(max_sweeps >= 1, "max_sweeps must be >= 1");
   REQUIRE(!std::isnan(tol), "tol is NaN");
   REQUIRE(n_probe >= 0 && (n_probe == 0 || (probe_node && probe_out)), "bad probe arrays");
+  REQUIRE(n_probe == 0 || ng == 1, "probes are recorded on single grids only");
   REQUIRE(mem == PG_MEM_HOST || mem == PG_MEM_DEVICE, "bad mem");
+  for (int k = 0; k < ng; ++k) {
+    REQUIRE(gs[k] != nullptr, "grid is NULL");
+    REQUIRE(!gs[k]->slab || method == PG_METHOD_RBSOR, "slab grids support the red-black sweep only");
+    REQUIRE(gs[k]->stream == g->stream, "grids of a group must share one stream");
+  }
 
   int rc;
   // ---- probes
@@ -499,12 +523,15 @@ PG_API int pg_transient(pg_grid *g, double h, int64_t steps, double tol, double 
       d_pout = probe_out;
     }
   }
-  if (g->dev_sweeps_cap < steps + 1) {
-    if (g->dev_sweeps) cudaFree(g->dev_sweeps);
-    g->dev_sweeps = nullptr;
-    g->dev_sweeps_cap = 0;
-    if ((rc = dalloc(&g->dev_sweeps, steps + 1))) return rc;
-    g->dev_sweeps_cap = steps + 1;
+  for (int k = 0; k < ng; ++k) {
+    pg_grid *q = gs[k];
+    if (q->dev_sweeps_cap < steps + 1) {
+      if (q->dev_sweeps) cudaFree(q->dev_sweeps);
+      q->dev_sweeps = nullptr;
+      q->dev_sweeps_cap = 0;
+      if ((rc = dalloc(&q->dev_sweeps, steps + 1))) return rc;
+      q->dev_sweeps_cap = steps + 1;
+    }
   }
   cudaStream_t st = g->stream;
   cudaEvent_t ev0, ev1, poll[2];
@@ -523,17 +550,22 @@ PG_API int pg_transient(pg_grid *g, double h, int64_t steps, double tol, double 
 
   int64_t launches = 0;
   const int F = sweeps_per_launch(g, method);
+  for (int k = 1; k < ng; ++k)
+    REQUIRE(sweeps_per_launch(gs[k], method) == F, "grids of a group must use the same fuse option");
   const int flips = (g->kind == 0 || method == PG_METHOD_JACOBI) ? 1 : 0;
   const int64_t max_launch = (max_sweeps + F - 1) / F;
 
   CK(cudaEventRecord(ev0, st));
-  CK(cudaMemcpyAsync(g->V[0], g->x0, sizeof(double) * g->np, cudaMemcpyDeviceToDevice, st));
-  CK(cudaMemsetAsync(g->dev_sweeps, 0, sizeof(int64_t) * (steps + 1), st));
-  if (g->iz) CK(cudaMemsetAsync(g->iz, 0, sizeof(double) * g->np, st));
-  if (g->pad_i) CK(cudaMemsetAsync(g->pad_i, 0, sizeof(double) * g->npad, st));
-  CK(launch_reset_state(g));
-  CK(launch_setup(g, h));
-  launches += 4;
+  for (int k = 0; k < ng; ++k) {
+    pg_grid *q = gs[k];
+    CK(cudaMemcpyAsync(q->V[0], q->x0, sizeof(double) * q->np, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemsetAsync(q->dev_sweeps, 0, sizeof(int64_t) * (steps + 1), st));
+    if (q->iz) CK(cudaMemsetAsync(q->iz, 0, sizeof(double) * q->np, st));
+    if (q->pad_i) CK(cudaMemsetAsync(q->pad_i, 0, sizeof(double) * q->npad, st));
+    CK(launch_reset_state(q));
+    CK(launch_setup(q, h));
+    launches += 4;
+  }
   if (n_probe > 0) {
     CK(launch_probe(g, d_pidx, n_probe, d_pout));
     ++launches;
@@ -549,18 +581,22 @@ PG_API int pg_transient(pg_grid *g, double h, int64_t steps, double tol, double 
     return g->tev[(size_t)k];
   };
   for (int64_t s = 1; s <= steps; ++s) {
-    CK(launch_rhs(g, h, s));
-    launches += 1 + (g->npad > 0) + (g->nsrc > 0);
+    for (int k = 0; k < ng; ++k) {
+      CK(launch_rhs(gs[k], h, s));
+      launches += 1 + (gs[k]->npad > 0) + (gs[k]->nsrc > 0);
+    }
     int64_t j = 0;
     int pending = -1;  // poll slot of the previous batch
     int slot = 0;
     if (g->timing) CK(cudaEventRecord(tev(0), st));
     while (j < max_launch) {
       const int64_t nb = std::min<int64_t>(g->batch, max_launch - j);
-      for (int64_t k = 0; k < nb; ++k) {
-        const int nsw = (int)std::min<int64_t>(F, max_sweeps - (j + k) * F);
-        CK(launch_sweep(g, method, omega, tol, (int)(j + k), nsw, &launches));
-        if (g->timing) CK(cudaEventRecord(tev(j + k + 1), st));
+      for (int64_t b = 0; b < nb; ++b) {
+        const int nsw = (int)std::min<int64_t>(F, max_sweeps - (j + b) * F);
+        for (int k = 0; k < ng; ++k)
+          CK(launch_sweep(gs[k], method, omega, tol, (int)(j + b), nsw, &launches));
+        if (ex) CK(ex->after_sweep((int)(j + b), &launches));
+        if (g->timing) CK(cudaEventRecord(tev(j + b + 1), st));
       }
       j += nb;
       if (!(tol > 0.0) || j >= max_launch) continue;
@@ -573,8 +609,10 @@ PG_API int pg_transient(pg_grid *g, double h, int64_t steps, double tol, double 
       pending = slot;
       slot ^= 1;
     }
-    CK(launch_step_end(g, s, (int)j, flips, F, max_sweeps, tol));
-    ++launches;
+    for (int k = 0; k < ng; ++k) {
+      CK(launch_step_end(gs[k], s, (int)j, flips, F, max_sweeps, tol));
+      ++launches;
+    }
     if (g->timing) {
       CK(cudaMemcpyAsync(g->ctl_host, g->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
@@ -587,9 +625,11 @@ PG_API int pg_transient(pg_grid *g, double h, int64_t steps, double tol, double 
         sweep_launches += ran;
       }
     }
-    if (g->rlc) {
-      CK(launch_inductor_update(g, h));
-      launches += 2;
+    for (int k = 0; k < ng; ++k) {
+      if (gs[k]->rlc) {
+        CK(launch_inductor_update(gs[k], h));
+        launches += 2;
+      }
     }
     if (n_probe > 0) {
       CK(launch_probe(g, d_pidx, n_probe, d_pout + s * n_probe));
@@ -597,6 +637,8 @@ PG_API int pg_transient(pg_grid *g, double h, int64_t steps, double tol, double 
     }
   }
   CK(cudaEventRecord(ev1, st));
+  for (int k = 1; k < ng; ++k)
+    CK(cudaMemcpyAsync(gs[k]->ctl_host, gs[k]->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(g->ctl_host, g->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, st));
   if (n_probe > 0 && mem == PG_MEM_HOST)
     CK(cudaMemcpyAsync(probe_out, d_pout, sizeof(double) * (steps + 1) * n_probe, cudaMemcpyDeviceToHost, st));
@@ -618,9 +660,11 @@ PG_API int pg_transient(pg_grid *g, double h, int64_t steps, double tol, double 
     stats->sweep_launches = sweep_launches;
     stats->sweeps_per_launch = F;
   }
-  if (c.diag_bad) {
-    set_error("a node has a non-positive diagonal d_i (no capacitance and no conductive path; Lemma 1)");
-    return PG_EINVAL;
+  for (int k = 0; k < ng; ++k) {
+    if (gs[k]->ctl_host->diag_bad) {
+      set_error("a node has a non-positive diagonal d_i (no capacitance and no conductive path; Lemma 1)");
+      return PG_EINVAL;
+    }
   }
   if (c.failed) {
     set_error("step " + std::to_string(c.failed) + " did not reach tol within max_sweeps");
@@ -629,4 +673,4 @@ PG_API int pg_transient(pg_grid *g, double h, int64_t steps, double tol, double 
   return PG_OK;
 }
 
-}  // extern "C"
+}  // namespace pgb

@@ -104,6 +104,11 @@ struct pg_grid {
   int64_t *dev_sweeps = nullptr;       // per-step sweep counts (device)
   int64_t dev_sweeps_cap = 0;
 
+  // ---- slab of a partitioned mesh (pg_set_slab): rows [y_begin, y_end) are
+  // owned, the others are ghost rows refreshed by the group exchange
+  bool slab = false;
+  int32_t y_begin = 0, y_end = 0, ypar = 0;
+
   // ---- options
   int fuse = 2;                        // F: sweeps per launch of the temporally blocked mesh sweep
   int lag = 3;                         // wavefront lag D between fused levels (3 or 4)
@@ -143,6 +148,19 @@ bool fused_variant_exists(int L, int F, int S, int D);
 int fused_ctas_per_sm(int L, int S);
 cudaError_t launch_rb_sweep_fused(pg_grid *g, double omega, double tol, int j, int nsw, int F,
                                   int S, int D, int rows_per_cta, int y_begin, int y_end, int ypar);
+
+// Multi-grid driver (pg_api.cu): Algorithm 1 over ng grids in lockstep; `ex`
+// (may be null) runs after every sweep launch of all grids.
+struct Exchange {
+  virtual ~Exchange() = default;
+  virtual cudaError_t after_sweep(int launch_idx, int64_t *launches) = 0;
+};
+int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, double tol,
+                  double omega, int method, int64_t max_sweeps, int64_t n_probe,
+                  const int64_t *probe_node, double *probe_out, int mem, int64_t *sweeps_out,
+                  pg_stats *stats);
+// upload / download helpers (pg_api.cu)
+int dalloc_bytes(void **p, size_t bytes);
 
 // host CSR construction (pg_csr_build.cpp)
 struct CsrHost {

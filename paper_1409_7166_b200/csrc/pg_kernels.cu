@@ -506,9 +506,11 @@ cudaError_t launch_sweep(pg_grid *g, int method, double omega, double tol, int j
     if (method == PG_METHOD_RBSOR) {
       if (!tma_available(g)) return cudaErrorNotSupported;
       const FusedCfg c = fused_cfg(g);
-      const int H = fused_rows_per_cta(g, c.F, c.S, g->md.NY);
+      const int y0 = g->slab ? g->y_begin : 0, y1 = g->slab ? g->y_end : g->md.NY;
+      const int H = fused_rows_per_cta(g, c.F, c.S, y1 - y0);
       ++*launches;
-      return launch_rb_sweep_fused(g, omega, tol, j, nsweeps, c.F, c.S, c.D, H, 0, g->md.NY, 0);
+      return launch_rb_sweep_fused(g, omega, tol, j, nsweeps, c.F, c.S, c.D, H, y0, y1,
+                                   g->slab ? g->ypar : 0);
     }
     JacobiArgs a;
     a.d = g->md;

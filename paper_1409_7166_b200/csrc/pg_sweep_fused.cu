@@ -104,11 +104,14 @@ struct FusedParams {
 
 // One red-black node update (Eq. (13) + (15)) of the node at offset `me` of
 // row stage Ry (row r-1 in Rn, row r+1 in Rs); `ow`/`oe` are the offsets of
-// its west/east neighbours (other parity half of the same layer row).
-// Returns |dV|.
+// its west/east neighbours (other parity half of the same layer row).  The
+// new value is stored only if `st` (rows outside the wavefront are computed
+// from whatever the ring holds and discarded, which keeps the levels free of
+// branches so their dependency chains interleave).  Returns |dV|.
 template <int L>
 __device__ __forceinline__ double node_update(double *Ry, const double *Rn, const double *Rs, int me,
-                                              int ow, int oe, double w, bool has_down, bool ok) {
+                                              int ow, int oe, double w, bool has_down, bool ok,
+                                              bool st) {
   constexpr int LAY = L * kRow;
   constexpr int GX = 1 * LAY, GY = 2 * LAY, GZ = 3 * LAY, BB = 4 * LAY, ID = 5 * LAY;
   const double Vc = Ry[me];
@@ -120,7 +123,7 @@ __device__ __forceinline__ double node_update(double *Ry, const double *Rn, cons
   if (has_down) s2 = fma(Ry[GZ + me - kRow], Ry[me - kRow], s2);  // via down (layer l-1)
   double vn = fma(w, (s1 + s2) * Ry[ID + me] - Vc, Vc);
   vn = ok ? vn : Vc;
-  Ry[me] = vn;
+  if (st) Ry[me] = vn;
   return fabs(vn - Vc);
 }
 
@@ -185,10 +188,8 @@ __global__ void __launch_bounds__(32 * L) k_rb_sweep_fused(const __grid_constant
   }
   __syncthreads();
 
-  auto slot = [&](int r) { return (r - r_first) % S; };
-  auto stage = [&](int r) { return ring + slot(r) * SE; };
-  auto issue = [&](int r) {
-    const int s = slot(r);
+  // ring slot of row r is (r - r_first) mod S
+  auto issue_slot = [&](int r, int s) {
     double *st = ring + s * SE;
     mbar_expect_tx(&full_bar[s], STAGE_BYTES);
     tma4(st, mVin, &full_bar[s], ps, r);
@@ -198,12 +199,8 @@ __global__ void __launch_bounds__(32 * L) k_rb_sweep_fused(const __grid_constant
     tma4(st + BB, &P.mb, &full_bar[s], ps, r);
     tma4(st + ID, &P.mid, &full_bar[s], ps, r);
   };
-  auto wait_row = [&](int r) {
-    const int k = r - r_first;
-    mbar_wait(&full_bar[k % S], (uint32_t)((k / S) & 1));
-  };
   if (leader)
-    for (int r = r_first; r < r_first + S && r <= r_last; ++r) issue(r);
+    for (int r = r_first; r < r_first + S && r <= r_last; ++r) issue_slot(r, r - r_first);
 
   const double w = P.omega;
   const int pe = l * kRow + lane;        // my even-column node in an array block
@@ -217,59 +214,67 @@ __global__ void __launch_bounds__(32 * L) k_rb_sweep_fused(const __grid_constant
   double *vout_e = Vout + (int64_t)l * P.layer_stride + gp;
   double *vout_o = vout_e + P.HP;
   double dmax = 0.0;
-  // node of parity e (0 even, 1 odd column) of my pair: self / west / east offsets
-  auto upd = [&](int r, int e) -> double {
-    const int me = e ? po : pe;
-    const int ow = e ? pe : po - 1;
-    const int oe = e ? pe + 1 : po;
-    return node_update<L>(stage(r), stage(r - 1), stage(r + 1), me, ow, oe, w, has_down,
-                          e ? ok1 : ok0);
-  };
   const int last = nsw - 1;
   const int y_end_loop = r_last + D * last;
 
-  wait_row(r_first);
-  if (r_first + 1 <= r_last) wait_row(r_first + 1);
-  for (int y = r_first + 1; y <= y_end_loop; ++y) {
-    if (y + 1 <= r_last) wait_row(y + 1);
-    // ------------------------------------------------ phase A: red_f(y - D f)
+  // update of the parity-e node of my pair in row r (slots sy, sy-1, sy+1)
+  auto upd = [&](int r, int e, int sl, int sn, int ss, bool st) -> double {
+    const int me = e ? po : pe;
+    const int ow = e ? pe : po - 1;
+    const int oe = e ? pe + 1 : po;
+    return node_update<L>(ring + sl * SE, ring + sn * SE, ring + ss * SE, me, ow, oe, w, has_down,
+                          e ? ok1 : ok0, st);
+  };
+  auto wait_k = [&](int k, int s) { mbar_wait(&full_bar[s], (uint32_t)((k / S) & 1)); };
+  constexpr auto md = [](int a) { return ((a % S) + S) % S; };
+
+  wait_k(0, 0);
+  if (r_first + 1 <= r_last) wait_k(1, 1 % S);
+  // y = r_first + 1 + u (mod S): the loop is unrolled S times so every ring
+  // slot below is a compile-time constant
+  for (int y0 = r_first + 1; y0 <= y_end_loop; y0 += S) {
 #pragma unroll
-    for (int f = 0; f < F; ++f) {
-      const int r = y - D * f;
-      if (f < nsw && r > r_first && r < r_last) {
-        const double d = upd(r, (lpar + r) & 1);  // red: (l + y + x) even
-        if (f == last && r >= ys && r < ye && exact_lane) dmax = fmax(dmax, d);
-      }
-    }
-    fence_proxy_async();
-    __syncthreads();
-    if constexpr (D >= 4) {
-      // phase B(y-1) has finished everywhere: its lowest row is dead
-      const int R = y - D * (F - 1) - 3 + S;
-      if (leader && R <= r_last && R >= r_first + S) issue(R);
-    }
-    // ------------------------------------------------ phase B: black_f(y - D f - 1)
+    for (int u = 0; u < S; ++u) {
+      const int y = y0 + u;
+      if (y > y_end_loop) break;
+      if (y + 1 <= r_last) wait_k(y + 1 - r_first, md(2 + u));
+      // ---------------------------------------------- phase A: red_f(y - D f)
 #pragma unroll
-    for (int f = 0; f < F; ++f) {
-      const int r = y - D * f - 1;
-      if (f < nsw && r > r_first && r < r_last) {
-        const double d = upd(r, ((lpar + r) & 1) ^ 1);  // black
-        if (f == last && r >= ys && r < ye && exact_lane) dmax = fmax(dmax, d);
+      for (int f = 0; f < F; ++f) {
+        const int r = y - D * f;
+        const bool in = f < nsw && r > r_first && r < r_last;
+        const double d = upd(r, lpar ^ (r & 1), md(1 + u - D * f), md(u - D * f), md(2 + u - D * f), in);
+        if (f == last && in && r >= ys && r < ye && exact_lane && d > dmax) dmax = d;
       }
-    }
-    {
-      const int ro = y - D * last - 1;  // row finished by the last level
-      if (ro >= ys && ro < ye && exact_lane) {
-        const double *R = stage(ro);
-        vout_e[(int64_t)ro * P.NXP] = R[pe];
-        vout_o[(int64_t)ro * P.NXP] = R[po];
-      }
-    }
-    if constexpr (D == 3) {
-      fence_proxy_async();
+      if constexpr (D >= 4) fence_proxy_async();
       __syncthreads();
-      const int R = y - D * (F - 1) - 2 + S;
-      if (leader && R <= r_last && R >= r_first + S) issue(R);
+      if constexpr (D >= 4) {
+        // phase B(y-1) has finished everywhere: its lowest row is dead
+        const int R = y - D * (F - 1) - 3 + S;
+        if (leader && R <= r_last && R >= r_first + S) issue_slot(R, md(u - D * (F - 1) - 2));
+      }
+      // ---------------------------------------------- phase B: black_f(y - D f - 1)
+#pragma unroll
+      for (int f = 0; f < F; ++f) {
+        const int r = y - D * f - 1;
+        const bool in = f < nsw && r > r_first && r < r_last;
+        const double d = upd(r, lpar ^ (r & 1) ^ 1, md(u - D * f), md(u - 1 - D * f), md(1 + u - D * f), in);
+        if (f == last && in && r >= ys && r < ye && exact_lane && d > dmax) dmax = d;
+      }
+      if constexpr (D == 3) fence_proxy_async();
+      {
+        const int ro = y - D * last - 1;  // row finished by the last level
+        if (ro >= ys && ro < ye && exact_lane) {
+          const double *R = ring + md(u - D * last) * SE;
+          vout_e[(int64_t)ro * P.NXP] = R[pe];
+          vout_o[(int64_t)ro * P.NXP] = R[po];
+        }
+      }
+      if constexpr (D == 3) {
+        __syncthreads();
+        const int R = y - D * (F - 1) - 2 + S;
+        if (leader && R <= r_last && R >= r_first + S) issue_slot(R, md(u - D * (F - 1) - 1));
+      }
     }
   }
 #pragma unroll

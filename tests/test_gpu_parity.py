@@ -32,8 +32,9 @@ def pgb():
     return P
 
 
-def oracle_run(g, steps, tol, omega, method="gs", order="redblack", max_sweeps=200000, form="companion"):
-    nl = netlist.from_grid(g)
+def oracle_run(g, steps, tol, omega, method="gs", order="redblack", max_sweeps=200000, form="companion",
+               series_rl="node"):
+    nl = netlist.from_grid(g, series_rl)
     It = pwl.node_currents_table(nl, g.h, steps)
     o = nodal.NodalOracle(nl)
     ordr = None
@@ -131,6 +132,19 @@ def test_rlc_iterates_vs_converged(pgb, shape):
     n = g.n
     assert np.abs(ro.V[:, :n] - 1.0).max() > 1e-6
     np.testing.assert_allclose(rg.probes, ro.V[:, :n], rtol=0, atol=ATOL_CONV)
+
+
+@pytest.mark.parametrize("shape", [(2, 6, 5), (3, 4, 4), (2, 1, 6), (4, 9, 70), (8, 5, 3)])
+@pytest.mark.parametrize("F", [1, 2, 3])
+def test_rlc_iterates_equal_oracle_series_element(pgb, shape, F):
+    # the oracle's series R-L element (one branch, R7) is the GPU's
+    # companion model: fixed-sweep iterates agree to rounding
+    g = mk(*shape, seed=60 + sum(shape), rlc=True)
+    steps, k = 8, 5
+    ro, _ = oracle_run(g, steps, tol=0.0, omega=1.6, max_sweeps=k, series_rl="element")
+    rg, V = gpu_run(pgb, g, steps, tol=0.0, omega=1.6, max_sweeps=k, options={"fuse": F})
+    assert np.abs(ro.V - 1.0).max() > 1e-6
+    np.testing.assert_allclose(rg.probes, ro.V, rtol=0, atol=ATOL_ITER)
 
 
 def test_config0_full_size_converged(pgb):

@@ -349,6 +349,44 @@ def test_series_rl_is_eliminated_internal_node():
         assert abs(va - V[s, 0]) < 1e-12 and abs(vc - V[s, 2]) < 1e-12
 
 
+def test_series_rl_element_matches_internal_node_cholesky():
+    # the oracle's series R-L element (netlist series_rl="element", one inductor
+    # branch with series resistance) against the dense Cholesky solve of the
+    # paper's element-wise model with internal nodes (series_rl="node"):
+    # same voltages at the grid nodes, same branch currents
+    for g in small_rlc_grids():
+        nl_node = netlist.from_mesh(g, series_rl="node")
+        nl_el = netlist.from_mesh(g, series_rl="element")
+        assert nl_el.n == g.n and nl_node.n > g.n and np.all(nl_el.lr > 0)
+        steps = 15
+        V, il = dense.direct_companion(nl_node, g.h, steps,
+                                       pwl.node_currents_table(nl_node, g.h, steps), _v0(nl_node))
+        It = pwl.node_currents_table(nl_el, g.h, steps)
+        for order in (None, nodal.red_black_order(g.layers, g.ny, g.nx)):
+            r = nodal.NodalOracle(nl_el).transient(g.h, steps, tol=1e-15, omega=1.7, Itab=It,
+                                                   order=order)
+            assert r.status == 0
+            np.testing.assert_allclose(r.V, V[:, :g.n], rtol=0, atol=1e-10)
+            np.testing.assert_allclose(r.il, il, rtol=0, atol=1e-8 * max(1.0, np.abs(il).max()))
+            # KCL at every grid node with the series element's companion current
+            il_prev = np.zeros(nl_el.la.size)
+            for s in range(1, steps + 1):
+                res = kcl.residual(nl_el, g.h, r.V[s], r.V[s - 1], It[s], il_prev)
+                assert np.abs(res).max() <= 1e-9
+                il_prev = kcl.inductor_currents_next(nl_el, g.h, r.V[s], il_prev)
+
+
+def test_series_rl_element_rejected_where_unsupported():
+    g = small_rlc_grids()[0]
+    nl = netlist.from_mesh(g, series_rl="element")
+    with pytest.raises(ValueError):
+        dense.system(nl, g.h)
+    with pytest.raises(ValueError):
+        nodal.NodalOracle(nl).transient(g.h, 3, form="second_order", V1=_v0(nl))
+    with pytest.raises(ValueError):
+        netlist.from_mesh(g, series_rl="bogus")
+
+
 def test_zero_current_invariant():
     for g in small_grids()[:3] + small_rlc_grids()[:2]:
         g.sources = gridgen.Sources(node=np.zeros(0, np.int64), ptr=np.zeros(1, np.int64),
