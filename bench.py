@@ -1,20 +1,26 @@
 """Benchmark: topology-based power-grid transient (arxiv 1409.7166) on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                    [--workload cfgK] [--tsteps T] [--omega w] [--method rbsor|jacobi]
+                    [--workload K] [--tsteps T] [--omega w] [--method rbsor|jacobi]
+                    [--scaling weak|strong] [--opt key=value ...]
 
 One bench "step" = one full pass of the hot path over the workload: a
 pg_transient call (Algorithm 1: per backward-Euler time step the fused RHS
-kernel, red-black SOR sweeps to tol = 1e-10 V, inductor update) over T time
-steps of the BASELINE.json configuration (N = 1: config 1, 4 x 1024 x 1024
-RC mesh, h = 5 ps, 500 steps).  Inputs are seeded synthetic grids with the
-BASELINE.json distributions; they are resident in HBM before
-the timed region (the ~235 MB per-sweep working set exceeds the 126 MB L2).
+kernels, red-black SOR sweeps (F = 2 per launch) to tol = 1e-10 V, inductor
+update) over T time steps of the BASELINE.json configuration (N = 1: config 1,
+4 x 1024 x 1024 RC mesh, h = 5 ps, 500 steps).  N > 1 (torchrun, one rank per
+GPU): the mesh is split into row slabs, one per GPU, advanced by
+pg_group_transient with an NCCL ghost-row exchange and norm allreduce after
+every sweep launch; weak scaling stacks N copies of the config's rows.
+Inputs are seeded synthetic grids with the BASELINE.json distributions
+(DESIGN.md §6), resident in HBM before the timed region (the ~235 MB per-pass
+working set exceeds the 126 MB L2).
 
 Metric: node-sweeps per second (GNode-sweeps/s), whole job; ms per time step
-is reported in `config`.  `roofline` is for the dominant kernel (k_rb_sweep):
-algorithmic bytes per launch (56 B per node: V read + write, gx, gy, gz, b,
-1/d) / its CUDA-event duration inside the timed region.
+is reported in `config`.  `roofline` is for the dominant kernel
+(k_rb_sweep_fused): algorithmic bytes per launch (56 B per node: V read +
+write, gx, gy, gz, b, 1/d, once per launch of F sweeps) / its CUDA-event
+duration inside the timed region.
 """
 from __future__ import annotations
 
@@ -47,6 +53,8 @@ def parse():
     ap.add_argument("--omega", type=float, default=None)
     ap.add_argument("--tol", type=float, default=1e-10)
     ap.add_argument("--method", default="rbsor", choices=["rbsor", "jacobi"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak = config rows x N (fixed work per GPU), strong = config split")
     ap.add_argument("--opt", action="append", default=[],
                     help="library option key=value (pg_set_option), e.g. fuse=2, lag=3, kernel=4")
     ap.add_argument("--no-e2e", action="store_true")
@@ -116,8 +124,14 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ workloads
-def make_grid(cfg: int):
+def make_grid(cfg: int, world: int = 1, scaling: str = "weak"):
+    """BASELINE config `cfg`; for N > 1 ranks under weak scaling the mesh is N
+    copies of the config's row count stacked (same per-GPU work), under strong
+    scaling the config itself is split."""
     import gridgen
+    if world > 1 and scaling == "weak":
+        L, NY, NX = gridgen.CONFIGS[cfg]["dims"]
+        return gridgen.config_grid(cfg, dims=(L, NY * world, NX))
     return gridgen.config_grid(cfg)
 
 
@@ -210,18 +224,34 @@ def run_b200(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = args.workload if args.workload is not None else 1
-    g = make_grid(cfg)
+    g = make_grid(cfg, world, args.scaling)
     T = args.tsteps or g.steps
     omega = args.omega or DEFAULT_OMEGA.get(cfg, 1.9)
     tol = args.tol
     stream = torch.cuda.current_stream()
-    mk = P.Grid.from_mesh_grid if hasattr(g, "gx") else P.Grid.from_edge_grid
-    G = mk(g, device=True)
-    G.set_stream(stream)
-    G.set_option("timing", 1)
     opts = dict(kv.split("=", 1) for kv in args.opt)
+    fuse = int(opts.get("fuse", 2))
+    if world > 1:
+        # slab partition over the ranks: NCCL halo exchange + norm allreduce
+        # after every sweep launch inside the library (pg_group_transient)
+        grp = P.SlabGroup.nccl(g, rank, world, fuse=fuse, stream=stream)
+        G = grp.grids[0]
+        sp = grp.specs[0]
+        my_nodes = g.layers * (sp.y1 - sp.y0) * g.nx
+    else:
+        grp = None
+        mk = P.Grid.from_mesh_grid if hasattr(g, "gx") else P.Grid.from_edge_grid
+        G = mk(g, device=True)
+        G.set_stream(stream)
+        my_nodes = g.n
+    G.set_option("timing", 1)
     for k, v in opts.items():
         G.set_option(k, int(v))
+
+    def solve():
+        if grp is not None:
+            return grp.transient(g.h, T, tol=tol, omega=omega, max_sweeps=200000)
+        return G.transient(g.h, T, tol=tol, omega=omega, method=args.method, max_sweeps=200000)
 
     def barrier():
         torch.cuda.synchronize()
@@ -229,7 +259,7 @@ def run_b200(args):
             dist.barrier()
 
     for _ in range(args.warmup):
-        G.transient(g.h, T, tol=tol, omega=omega, method=args.method, max_sweeps=200000)
+        solve()
     clocks = ClockSampler(local)
     barrier()
     clocks.start()
@@ -241,7 +271,7 @@ def run_b200(args):
     sweep_launches = 0
     sweeps_per_tstep = []
     for _ in range(args.steps):
-        r = G.transient(g.h, T, tol=tol, omega=omega, method=args.method, max_sweeps=200000)
+        r = solve()
         sweeps += int(r.stats.sweeps_total)
         launches += int(r.stats.kernel_launches)
         sweep_ms += float(r.stats.sweep_ms)
@@ -255,7 +285,7 @@ def run_b200(args):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    node_sweeps = float(g.n) * sweeps
+    node_sweeps = float(my_nodes) * sweeps
     tot = torch.tensor([node_sweeps], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(tot)
@@ -266,18 +296,49 @@ def run_b200(args):
     peak, peak_src = peaks()
     avg_launch_ms = sweep_ms / max(sweep_launches, 1)
     F = int(r.stats.sweeps_per_launch)
-    achieved = BYTES_PER_NODE_PASS * g.n / (avg_launch_ms * 1e-3) / 1e9
+    launch_nodes = G.info()["layers"] * G.info()["ny"] * G.info()["nx"] if hasattr(g, "gx") else g.n
+    achieved = BYTES_PER_NODE_PASS * launch_nodes / (avg_launch_ms * 1e-3) / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": ncu_traffic(F),
             "kernel": "k_rb_sweep_fused" if F > 1 else "k_rb_sweep_fused<F=1>",
             "bytes_per_node_per_launch": BYTES_PER_NODE_PASS, "sweeps_per_launch": F,
             "bytes_per_node_sweep": BYTES_PER_NODE_PASS / F, "avg_launch_us": avg_launch_ms * 1e3,
-            "kernel_node_sweeps_per_s": g.n * F / (avg_launch_ms * 1e-3) / 1e9,
+            "kernel_node_sweeps_per_s": launch_nodes * F / (avg_launch_ms * 1e-3) / 1e9,
             "sweep_share_of_step": sweep_ms / ms if ms > 0 else None, "peak_source": peak_src}
 
     # e2e: public C-ABI call with host buffers (pinned), copies inside the timed region
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and grp is not None:
+        # public API with host buffers: this rank's slab built from host arrays,
+        # NCCL group set up, transient, owned voltages read back
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        barrier()
+        e0.record(stream)
+        e_sweeps = 0
+        nrep = max(1, min(args.steps, 2))
+        h2d = d2h = 0
+        for _ in range(nrep):
+            H = P.SlabGroup.nccl(g, rank, world, fuse=fuse, stream=stream, device=False)
+            for k, v in opts.items():
+                H.grids[0].set_option(k, int(v))
+            rr = H.transient(g.h, T, tol=tol, omega=omega, max_sweeps=200000)
+            Vo = H.owned_voltages(g)
+            sm = H.specs[0]
+            h2d = 8 * g.layers * (sm.hi - sm.lo) * g.nx * 4
+            d2h = 8 * g.layers * (sm.hi - sm.lo) * g.nx
+            H.close()
+            e_sweeps += int(rr.stats.sweeps_total)
+        e1.record(stream)
+        barrier()
+        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        ns = torch.tensor([float(my_nodes) * e_sweeps], dtype=torch.float64, device="cuda")
+        dist.all_reduce(ns)
+        e2e = {"value": float(ns.item()) / (float(te.item()) * 1e-3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": float(te.item()) / nrep, "per_rank_bytes": True}
+    elif not args.no_e2e:
         pin = {}
         for name in ("gx", "gy", "gz", "cap", "lz"):
             a = getattr(g, name, None)
@@ -331,16 +392,19 @@ def run_b200(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": args.scaling if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded BASELINE.json recipe, gridgen)",
-            "config": {"workload": f"config{cfg}", "nodes": g.n,
+            "config": {"workload": f"config{cfg}" + (f" x{world} rows (weak scaling)" if world > 1 and
+                                                     args.scaling == "weak" else ""), "nodes": g.n,
                        "mesh": [g.layers, g.ny, g.nx] if hasattr(g, "gx") else None,
                        "h_s": g.h, "time_steps_per_bench_step": T, "tol_V": tol, "omega": omega,
                        "method": args.method, "options": opts, "ms_per_time_step": ms_max / args.steps / T,
                        "sweeps_per_time_step_mean": float(spt.mean()),
                        "sweeps_per_time_step_max": int(spt.max()),
                        "l2": "per-sweep working set ~56 B/node x n > 126 MB L2 (no flush needed)",
-                       "parallelism": "replicas" if world > 1 else "1 GPU"},
+                       "parallelism": (f"slab{world}: rows split over {world} GPUs, NCCL ghost-row "
+                                       f"exchange + norm allreduce per sweep launch") if world > 1
+                       else "1 GPU"},
             "clocks": ck, "e2e": e2e, "gpu_launches": launches, "roofline": roof,
             "cpu_baseline": cpu,
         }

@@ -160,6 +160,56 @@ PG_API int pg_transient(pg_grid *g, double h, int64_t steps, double tol, double 
                         const int64_t *probe_node, double *probe_out, int mem,
                         int64_t *sweeps_out, pg_stats *stats);
 
+/* ---- Multi-GPU: slab partition of a mesh -------------------
+ * A global layers x NY x nx mesh is cut into blocks of rows ("slabs"), one per
+ * rank.  Rank r's slab grid is an ordinary mesh grid (pg_create_mesh) over the
+ * global rows [max(0, Y0 - G), min(NY, Y1 + G)): its owned rows [Y0, Y1) plus G
+ * ghost rows of each neighbour, built from the global arrays' rows (gy of the
+ * last local row set to 0) with the pads and loads of those rows.  The
+ * red-black sweep is exact on the owned rows when G >= 2 F (F = option
+ * "fuse"): every sweep launch recomputes 2F rows of halo from the ghost rows
+ * (Eq. (13) in the global red-black numbering, R12).       */
+
+/* Mark local rows [y_begin, y_end) as owned (updated, written, counted in the
+ * convergence norm); y0_parity = parity of the global index of local row 0.
+ * Mesh grids only (PG_ESTATE otherwise).  A slab grid is advanced only by
+ * pg_group_transient.                                                       */
+PG_API int pg_set_slab(pg_grid *g, int32_t y_begin, int32_t y_end, int32_t y0_parity);
+
+typedef struct pg_group pg_group;
+
+/* A fresh NCCL unique id (128 bytes written to id128) for pg_group_nccl; call
+ * on one rank and broadcast it.  NCCL is loaded at run time (libnccl.so.2, the
+ * copy already in the process if any); PG_ESTATE if it cannot be loaded.    */
+PG_API int pg_nccl_unique_id(void *id128);
+
+/* Join this process's slab (rank `rank` of `nranks`, ranks ordered by rows,
+ * one GPU each, current device) into an NCCL group with `ghost` rows per side.
+ * Collective: every rank calls it with the same id.  The slab must own
+ * [ghost, ny - ghost) except at the global edges (rank 0 owns from local row 0,
+ * the last rank up to its last row).                                        */
+PG_API int pg_group_nccl(pg_grid *slab, const void *id128, int32_t nranks, int32_t rank,
+                         int32_t ghost, pg_group **out);
+
+/* Single-process group of n slab grids on the current device, ordered by rows
+ * and sharing one stream: the n-rank protocol with device-to-device copies in
+ * place of NCCL (emulates n ranks on one GPU; same kernels and ordering).   */
+PG_API int pg_group_local(int32_t n, pg_grid *const *slabs, int32_t ghost, pg_group **out);
+
+/* Algorithm 1 on all slabs in lockstep (method: red-black SOR).  After every
+ * sweep launch the launch's convergence norm max|dV| is max-reduced over all
+ * slabs (ncclAllReduce of one 8-byte word) and each slab's `ghost` boundary
+ * rows are sent to its neighbours' ghost rows (ncclSend/ncclRecv of packed
+ * rows), so every rank takes the same stopping decision and the owned rows
+ * equal the single-grid iterates.  Arguments as pg_transient (no probes;
+ * voltages via pg_get_voltages on each slab, owned rows); sweeps_out / stats
+ * describe this process's first slab (identical on all ranks).  Collective.  */
+PG_API int pg_group_transient(pg_group *grp, double h, int64_t steps, double tol, double omega,
+                              int64_t max_sweeps, int64_t *sweeps_out, pg_stats *stats);
+
+/* Free the group's buffers and communicator (the slab grids stay).  NULL ok. */
+PG_API void pg_group_destroy(pg_group *grp);
+
 /* Number of nodes / dimensions (layers, ny, nx are 0 for CSR grids). */
 PG_API int pg_info(const pg_grid *g, int64_t *n, int32_t *layers, int32_t *ny, int32_t *nx,
                    int32_t *n_colors);

@@ -7,5 +7,7 @@ lives in the sm_100a library ``lib/libpgb200.so`` behind the C ABI of
 """
 from ._lib import PgError, PgNoConvergence, load  # noqa: F401
 from .api import Grid, TransientResult  # noqa: F401
+from .slab import SlabGroup, partition_rows, slab_spec  # noqa: F401
 
-__all__ = ["Grid", "TransientResult", "PgError", "PgNoConvergence", "load"]
+__all__ = ["Grid", "TransientResult", "PgError", "PgNoConvergence", "load", "SlabGroup",
+           "partition_rows", "slab_spec"]

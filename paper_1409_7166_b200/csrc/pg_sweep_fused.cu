@@ -108,10 +108,12 @@ struct FusedParams {
 // new value is stored only if `st` (rows outside the wavefront are computed
 // from whatever the ring holds and discarded, which keeps the levels free of
 // branches so their dependency chains interleave).  Returns |dV|.
+// Padding columns (x >= NX) and out-of-grid columns (TMA zero fill) have
+// V = b = 1/d = 0 and zero conductances, so the update leaves them at 0 and
+// needs no mask.
 template <int L>
 __device__ __forceinline__ double node_update(double *Ry, const double *Rn, const double *Rs, int me,
-                                              int ow, int oe, double w, bool has_down, bool ok,
-                                              bool st) {
+                                              int ow, int oe, double w, bool has_down, bool st) {
   constexpr int LAY = L * kRow;
   constexpr int GX = 1 * LAY, GY = 2 * LAY, GZ = 3 * LAY, BB = 4 * LAY, ID = 5 * LAY;
   const double Vc = Ry[me];
@@ -121,8 +123,7 @@ __device__ __forceinline__ double node_update(double *Ry, const double *Rn, cons
   double s2 = Ry[GY + me] * Rs[me];                       // south (row r+1)
   s2 = fma(Ry[GZ + me], Ry[me + kRow], s2);               // via up (layer l+1)
   if (has_down) s2 = fma(Ry[GZ + me - kRow], Ry[me - kRow], s2);  // via down (layer l-1)
-  double vn = fma(w, (s1 + s2) * Ry[ID + me] - Vc, Vc);
-  vn = ok ? vn : Vc;
+  const double vn = fma(w, (s1 + s2) * Ry[ID + me] - Vc, Vc);
   if (st) Ry[me] = vn;
   return fabs(vn - Vc);
 }
@@ -207,23 +208,18 @@ __global__ void __launch_bounds__(32 * L) k_rb_sweep_fused(const __grid_constant
   const int po = pe + 32;                // my odd-column node
   const int gp = ps + lane;              // my pair (global half-column)
   const bool exact_lane = lane >= FH && lane < FH + I && gp < P.HP;
-  const bool ok0 = gp >= 0 && 2 * gp < P.NX;
-  const bool ok1 = gp >= 0 && 2 * gp + 1 < P.NX;
   const bool has_down = l > 0;
   const int lpar = (l + P.ypar) & 1;
   double *vout_e = Vout + (int64_t)l * P.layer_stride + gp;
   double *vout_o = vout_e + P.HP;
   double dmax = 0.0;
-  const int last = nsw - 1;
-  const int y_end_loop = r_last + D * last;
 
   // update of the parity-e node of my pair in row r (slots sy, sy-1, sy+1)
   auto upd = [&](int r, int e, int sl, int sn, int ss, bool st) -> double {
     const int me = e ? po : pe;
     const int ow = e ? pe : po - 1;
     const int oe = e ? pe + 1 : po;
-    return node_update<L>(ring + sl * SE, ring + sn * SE, ring + ss * SE, me, ow, oe, w, has_down,
-                          e ? ok1 : ok0, st);
+    return node_update<L>(ring + sl * SE, ring + sn * SE, ring + ss * SE, me, ow, oe, w, has_down, st);
   };
   auto wait_k = [&](int k, int s) { mbar_wait(&full_bar[s], (uint32_t)((k / S) & 1)); };
   constexpr auto md = [](int a) { return ((a % S) + S) % S; };
@@ -231,52 +227,69 @@ __global__ void __launch_bounds__(32 * L) k_rb_sweep_fused(const __grid_constant
   wait_k(0, 0);
   if (r_first + 1 <= r_last) wait_k(1, 1 % S);
   // y = r_first + 1 + u (mod S): the loop is unrolled S times so every ring
-  // slot below is a compile-time constant
-  for (int y0 = r_first + 1; y0 <= y_end_loop; y0 += S) {
+  // slot below is a compile-time constant.  `last` (the level whose result is
+  // written and whose |dV| is the convergence norm) is a compile-time constant
+  // on the common path nsw == F.
+  auto sweep_pass = [&](const int last) {
+    const int y_end_loop = r_last + D * last;
+    for (int y0 = r_first + 1; y0 <= y_end_loop; y0 += S) {
 #pragma unroll
-    for (int u = 0; u < S; ++u) {
-      const int y = y0 + u;
-      if (y > y_end_loop) break;
-      if (y + 1 <= r_last) wait_k(y + 1 - r_first, md(2 + u));
-      // ---------------------------------------------- phase A: red_f(y - D f)
+      for (int u = 0; u < S; ++u) {
+        const int y = y0 + u;
+        if (y > y_end_loop) break;
+        if (y + 1 <= r_last) wait_k(y + 1 - r_first, md(2 + u));
+        // -------------------------------------------- phase A: red_f(y - D f)
+        double dA = 0.0;
 #pragma unroll
-      for (int f = 0; f < F; ++f) {
-        const int r = y - D * f;
-        const bool in = f < nsw && r > r_first && r < r_last;
-        const double d = upd(r, lpar ^ (r & 1), md(1 + u - D * f), md(u - D * f), md(2 + u - D * f), in);
-        if (f == last && in && r >= ys && r < ye && exact_lane && d > dmax) dmax = d;
-      }
-      if constexpr (D >= 4) fence_proxy_async();
-      __syncthreads();
-      if constexpr (D >= 4) {
-        // phase B(y-1) has finished everywhere: its lowest row is dead
-        const int R = y - D * (F - 1) - 3 + S;
-        if (leader && R <= r_last && R >= r_first + S) issue_slot(R, md(u - D * (F - 1) - 2));
-      }
-      // ---------------------------------------------- phase B: black_f(y - D f - 1)
+        for (int f = 0; f < F; ++f) {
+          const int r = y - D * f;
+          const bool in = f <= last && r > r_first && r < r_last;
+          const double d = upd(r, lpar ^ (r & 1), md(1 + u - D * f), md(u - D * f), md(2 + u - D * f), in);
+          if (f == last) dA = d;
+        }
+        {
+          const int r = y - D * last;
+          if (!(r >= ys && r < ye && exact_lane)) dA = 0.0;
+        }
+        if constexpr (D >= 4) fence_proxy_async();
+        __syncthreads();
+        if constexpr (D >= 4) {
+          // phase B(y-1) has finished everywhere: its lowest row is dead
+          const int R = y - D * (F - 1) - 3 + S;
+          if (leader && R <= r_last && R >= r_first + S) issue_slot(R, md(u - D * (F - 1) - 2));
+        }
+        // -------------------------------------------- phase B: black_f(y - D f - 1)
+        double dB = 0.0;
 #pragma unroll
-      for (int f = 0; f < F; ++f) {
-        const int r = y - D * f - 1;
-        const bool in = f < nsw && r > r_first && r < r_last;
-        const double d = upd(r, lpar ^ (r & 1) ^ 1, md(u - D * f), md(u - 1 - D * f), md(1 + u - D * f), in);
-        if (f == last && in && r >= ys && r < ye && exact_lane && d > dmax) dmax = d;
-      }
-      if constexpr (D == 3) fence_proxy_async();
-      {
+        for (int f = 0; f < F; ++f) {
+          const int r = y - D * f - 1;
+          const bool in = f <= last && r > r_first && r < r_last;
+          const double d = upd(r, lpar ^ (r & 1) ^ 1, md(u - D * f), md(u - 1 - D * f), md(1 + u - D * f), in);
+          if (f == last) dB = d;
+        }
         const int ro = y - D * last - 1;  // row finished by the last level
-        if (ro >= ys && ro < ye && exact_lane) {
+        const bool out_row = ro >= ys && ro < ye && exact_lane;
+        if (!out_row) dB = 0.0;
+        dA = dA > dB ? dA : dB;
+        dmax = dA > dmax ? dA : dmax;
+        if constexpr (D == 3) fence_proxy_async();
+        if (out_row) {
           const double *R = ring + md(u - D * last) * SE;
           vout_e[(int64_t)ro * P.NXP] = R[pe];
           vout_o[(int64_t)ro * P.NXP] = R[po];
         }
-      }
-      if constexpr (D == 3) {
-        __syncthreads();
-        const int R = y - D * (F - 1) - 2 + S;
-        if (leader && R <= r_last && R >= r_first + S) issue_slot(R, md(u - D * (F - 1) - 1));
+        if constexpr (D == 3) {
+          __syncthreads();
+          const int R = y - D * (F - 1) - 2 + S;
+          if (leader && R <= r_last && R >= r_first + S) issue_slot(R, md(u - D * (F - 1) - 1));
+        }
       }
     }
-  }
+  };
+  if (nsw == F)
+    sweep_pass(F - 1);
+  else
+    sweep_pass(nsw - 1);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
   if (lane == 0) wmax[l] = dmax;
