@@ -104,28 +104,27 @@ struct FusedParams {
 
 // One red-black node update (Eq. (13) + (15)) of the node at offset `me` of
 // row stage Ry (row r-1 in Rn, row r+1 in Rs); `ow`/`oe` are the offsets of
-// its west/east neighbours (other parity half of the same layer row).  The
-// new value is stored only if `st` (rows outside the wavefront are computed
-// from whatever the ring holds and discarded, which keeps the levels free of
-// branches so their dependency chains interleave).  Returns |dV|.
+// its west/east neighbours (other parity half of the same layer row).
+// Returns the new value; the caller stores it (the stores of all levels of a
+// phase are issued after all their loads, so the levels' dependency chains
+// overlap: the compiler cannot reorder a shared store before a later load).
 // Padding columns (x >= NX) and out-of-grid columns (TMA zero fill) have
 // V = b = 1/d = 0 and zero conductances, so the update leaves them at 0 and
 // needs no mask.
 template <int L>
-__device__ __forceinline__ double node_update(double *Ry, const double *Rn, const double *Rs, int me,
-                                              int ow, int oe, double w, bool has_down, bool st) {
+__device__ __forceinline__ double node_update(const double *Ry, const double *Rn, const double *Rs,
+                                              int me, int ow, int oe, double w, bool has_down,
+                                              double &Vc) {
   constexpr int LAY = L * kRow;
   constexpr int GX = 1 * LAY, GY = 2 * LAY, GZ = 3 * LAY, BB = 4 * LAY, ID = 5 * LAY;
-  const double Vc = Ry[me];
+  Vc = Ry[me];
   double s1 = fma(Ry[GX + ow], Ry[ow], Ry[BB + me]);      // west link g(x-1,x) + K_i (b)
   s1 = fma(Ry[GX + me], Ry[oe], s1);                      // east link g(x,x+1)
   s1 = fma(Rn[GY + me], Rn[me], s1);                      // north (row r-1)
   double s2 = Ry[GY + me] * Rs[me];                       // south (row r+1)
   s2 = fma(Ry[GZ + me], Ry[me + kRow], s2);               // via up (layer l+1)
   if (has_down) s2 = fma(Ry[GZ + me - kRow], Ry[me - kRow], s2);  // via down (layer l-1)
-  const double vn = fma(w, (s1 + s2) * Ry[ID + me] - Vc, Vc);
-  if (st) Ry[me] = vn;
-  return fabs(vn - Vc);
+  return fma(w, (s1 + s2) * Ry[ID + me] - Vc, Vc);
 }
 
 template <int L, int F, int S, int D>
@@ -214,12 +213,14 @@ __global__ void __launch_bounds__(32 * L) k_rb_sweep_fused(const __grid_constant
   double *vout_o = vout_e + P.HP;
   double dmax = 0.0;
 
-  // update of the parity-e node of my pair in row r (slots sy, sy-1, sy+1)
-  auto upd = [&](int r, int e, int sl, int sn, int ss, bool st) -> double {
+  // new value of the parity-e node of my pair in row r (slots sl, sn = row
+  // r-1, ss = row r+1); *addr receives its shared-memory address
+  auto upd = [&](int e, int sl, int sn, int ss, double &Vc, double *&addr) -> double {
     const int me = e ? po : pe;
     const int ow = e ? pe : po - 1;
     const int oe = e ? pe + 1 : po;
-    return node_update<L>(ring + sl * SE, ring + sn * SE, ring + ss * SE, me, ow, oe, w, has_down, st);
+    addr = ring + sl * SE + me;
+    return node_update<L>(ring + sl * SE, ring + sn * SE, ring + ss * SE, me, ow, oe, w, has_down, Vc);
   };
   auto wait_k = [&](int k, int s) { mbar_wait(&full_bar[s], (uint32_t)((k / S) & 1)); };
   constexpr auto md = [](int a) { return ((a % S) + S) % S; };
@@ -240,12 +241,19 @@ __global__ void __launch_bounds__(32 * L) k_rb_sweep_fused(const __grid_constant
         if (y + 1 <= r_last) wait_k(y + 1 - r_first, md(2 + u));
         // -------------------------------------------- phase A: red_f(y - D f)
         double dA = 0.0;
+        {
+          double vn[F], vc[F], *ad[F];
 #pragma unroll
-        for (int f = 0; f < F; ++f) {
-          const int r = y - D * f;
-          const bool in = f <= last && r > r_first && r < r_last;
-          const double d = upd(r, lpar ^ (r & 1), md(1 + u - D * f), md(u - D * f), md(2 + u - D * f), in);
-          if (f == last) dA = d;
+          for (int f = 0; f < F; ++f) {
+            const int r = y - D * f;
+            vn[f] = upd(lpar ^ (r & 1), md(1 + u - D * f), md(u - D * f), md(2 + u - D * f), vc[f], ad[f]);
+          }
+#pragma unroll
+          for (int f = 0; f < F; ++f) {
+            const int r = y - D * f;
+            if (f <= last && r > r_first && r < r_last) *ad[f] = vn[f];
+            if (f == last) dA = fabs(vn[f] - vc[f]);
+          }
         }
         {
           const int r = y - D * last;
@@ -260,12 +268,19 @@ __global__ void __launch_bounds__(32 * L) k_rb_sweep_fused(const __grid_constant
         }
         // -------------------------------------------- phase B: black_f(y - D f - 1)
         double dB = 0.0;
+        {
+          double vn[F], vc[F], *ad[F];
 #pragma unroll
-        for (int f = 0; f < F; ++f) {
-          const int r = y - D * f - 1;
-          const bool in = f <= last && r > r_first && r < r_last;
-          const double d = upd(r, lpar ^ (r & 1) ^ 1, md(u - D * f), md(u - 1 - D * f), md(1 + u - D * f), in);
-          if (f == last) dB = d;
+          for (int f = 0; f < F; ++f) {
+            const int r = y - D * f - 1;
+            vn[f] = upd(lpar ^ (r & 1) ^ 1, md(u - D * f), md(u - 1 - D * f), md(1 + u - D * f), vc[f], ad[f]);
+          }
+#pragma unroll
+          for (int f = 0; f < F; ++f) {
+            const int r = y - D * f - 1;
+            if (f <= last && r > r_first && r < r_last) *ad[f] = vn[f];
+            if (f == last) dB = fabs(vn[f] - vc[f]);
+          }
         }
         const int ro = y - D * last - 1;  // row finished by the last level
         const bool out_row = ro >= ys && ro < ye && exact_lane;
