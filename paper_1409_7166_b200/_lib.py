@@ -7,7 +7,9 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libpgb200.so")
+# PGB200_LIB selects another build of the same ABI (e.g. the instrumented
+# lib/libpgb200_prof.so); there is no non-CUDA implementation.
+LIB_PATH = os.environ.get("PGB200_LIB") or os.path.join(HERE, "lib", "libpgb200.so")
 
 PG_MEM_HOST = 0
 PG_MEM_DEVICE = 1

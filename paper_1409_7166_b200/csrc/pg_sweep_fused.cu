@@ -88,6 +88,17 @@ __device__ __forceinline__ void fence_proxy_async() {
 
 }  // namespace
 
+// Optional cycle instrumentation (build with -DPG_PROF; debugging only):
+// per-warp clock sums of the streaming-step phases, read by pg_debug_prof.
+#ifdef PG_PROF
+__device__ unsigned long long g_prof[8];
+#define PROF_T(var) const long long var = clock64()
+#define PROF_ADD(k, a, b) prof[k] += (unsigned long long)((b) - (a))
+#else
+#define PROF_T(var)
+#define PROF_ADD(k, a, b)
+#endif
+
 struct FusedParams {
   CUtensorMap mV0, mV1, mgx, mgy, mgz, mb, mid;
   double *V0, *V1;
@@ -231,6 +242,9 @@ __global__ void __launch_bounds__(32 * L) k_rb_sweep_fused(const __grid_constant
   // slot below is a compile-time constant.  `last` (the level whose result is
   // written and whose |dV| is the convergence norm) is a compile-time constant
   // on the common path nsw == F.
+#ifdef PG_PROF
+  unsigned long long prof[6] = {0, 0, 0, 0, 0, 0};
+#endif
   auto sweep_pass = [&](const int last) {
     const int y_end_loop = r_last + D * last;
     for (int y0 = r_first + 1; y0 <= y_end_loop; y0 += S) {
@@ -238,7 +252,9 @@ __global__ void __launch_bounds__(32 * L) k_rb_sweep_fused(const __grid_constant
       for (int u = 0; u < S; ++u) {
         const int y = y0 + u;
         if (y > y_end_loop) break;
+        PROF_T(t0);
         if (y + 1 <= r_last) wait_k(y + 1 - r_first, md(2 + u));
+        PROF_T(t1);
         // -------------------------------------------- phase A: red_f(y - D f)
         double dA = 0.0;
         {
@@ -259,8 +275,10 @@ __global__ void __launch_bounds__(32 * L) k_rb_sweep_fused(const __grid_constant
           const int r = y - D * last;
           if (!(r >= ys && r < ye && exact_lane)) dA = 0.0;
         }
+        PROF_T(t2);
         if constexpr (D >= 4) fence_proxy_async();
         __syncthreads();
+        PROF_T(t3);
         if constexpr (D >= 4) {
           // phase B(y-1) has finished everywhere: its lowest row is dead
           const int R = y - D * (F - 1) - 3 + S;
@@ -282,6 +300,7 @@ __global__ void __launch_bounds__(32 * L) k_rb_sweep_fused(const __grid_constant
             if (f == last) dB = fabs(vn[f] - vc[f]);
           }
         }
+        PROF_T(t4);
         const int ro = y - D * last - 1;  // row finished by the last level
         const bool out_row = ro >= ys && ro < ye && exact_lane;
         if (!out_row) dB = 0.0;
@@ -293,11 +312,19 @@ __global__ void __launch_bounds__(32 * L) k_rb_sweep_fused(const __grid_constant
           vout_e[(int64_t)ro * P.NXP] = R[pe];
           vout_o[(int64_t)ro * P.NXP] = R[po];
         }
+        PROF_T(t5);
         if constexpr (D == 3) {
           __syncthreads();
           const int R = y - D * (F - 1) - 2 + S;
           if (leader && R <= r_last && R >= r_first + S) issue_slot(R, md(u - D * (F - 1) - 1));
         }
+        PROF_T(t6);
+        PROF_ADD(0, t0, t1);
+        PROF_ADD(1, t1, t2);
+        PROF_ADD(2, t2, t3);
+        PROF_ADD(3, t3, t4);
+        PROF_ADD(4, t4, t5);
+        PROF_ADD(5, t5, t6);
       }
     }
   };
@@ -305,6 +332,11 @@ __global__ void __launch_bounds__(32 * L) k_rb_sweep_fused(const __grid_constant
     sweep_pass(F - 1);
   else
     sweep_pass(nsw - 1);
+#ifdef PG_PROF
+  if (lane == 0)
+    for (int k = 0; k < 6; ++k) atomicAdd(&g_prof[k], prof[k]);
+  if (lane == 0) atomicAdd(&g_prof[6], 1ull);
+#endif
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
   if (lane == 0) wmax[l] = dmax;
@@ -461,3 +493,14 @@ cudaError_t launch_rb_sweep_fused(pg_grid *g, double omega, double tol, int j, i
 }
 
 }  // namespace pgb
+
+#ifdef PG_PROF
+extern "C" PG_API int pg_debug_prof(unsigned long long *out8, int reset) {
+  cudaMemcpyFromSymbol(out8, pgb::g_prof, sizeof(unsigned long long) * 8);
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(pgb::g_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
