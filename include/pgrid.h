@@ -120,6 +120,8 @@ PG_API int pg_set_stream(pg_grid *g, void *stream);
  *            1..4 (default 2); Jacobi and CSR sweeps always run 1 per launch
  *   "lag"    wavefront lag D (rows) between fused sweep levels: 3 (default) or 4
  *   "batch"  sweep launches enqueued between host convergence polls, >= 1
+ *   "graph"  1 (default): replay full batches of sweep launches from a captured
+ *            CUDA graph (single grids, option "timing" off); 0: plain launches
  *   "rows"   rows per CTA of the mesh sweep (0: auto)
  *   "stages" shared-memory ring stages S of the mesh sweep (0: auto =
  *            D (F-1) + 6); a (F, S, D) variant that is not compiled falls
@@ -209,6 +211,26 @@ PG_API int pg_group_transient(pg_group *grp, double h, int64_t steps, double tol
 
 /* Free the group's buffers and communicator (the slab grids stay).  NULL ok. */
 PG_API void pg_group_destroy(pg_group *grp);
+
+/* DC analysis (§II-A "In DC analysis, A = G", Eq. (3)): solve
+ * G v = G0 Vdd - i(t) by the same relaxation (Eq. (13)/(15) with C/h = 0:
+ * capacitors open; a series R-L branch conducts 1/R, its inductor shorted), the
+ * loads evaluated at time t, starting from x(0) (pg_set_voltages; default Vdd).
+ * The result is read with pg_get_voltages; inductor currents are left at the
+ * DC branch currents.  Every node needs a conductive path to a pad (else
+ * PG_EINVAL: zero diagonal).  Convergence needs omega close to 2 on large
+ * grids (no C/h term on the diagonal).  Other arguments as pg_transient.   */
+PG_API int pg_dc(pg_grid *g, double t, double tol, double omega, int method, int64_t max_sweeps,
+                 pg_stats *stats);
+
+/* Relaxation factor for Eq. (15) by Young's theory (§IV-D defers the
+ * choice of omega to [Young]): `sweeps` Jacobi sweeps of the homogeneous
+ * system (C/h + G + hL) e = 0 from x(0) estimate the spectral radius rho of the
+ * Jacobi iteration matrix (ratio of successive max-norm differences, power
+ * iteration); for the red-black (2-cyclic, consistently ordered) numbering
+ * the optimal SOR factor is 2 / (1 + sqrt(1 - rho^2)) (clamped to 1.999).
+ * Leaves the grid's state as after creation / pg_set_voltages.            */
+PG_API int pg_estimate_omega(pg_grid *g, double h, int64_t sweeps, double *rho, double *omega_opt);
 
 /* Number of nodes / dimensions (layers, ny, nx are 0 for CSR grids). */
 PG_API int pg_info(const pg_grid *g, int64_t *n, int32_t *layers, int32_t *ny, int32_t *nx,

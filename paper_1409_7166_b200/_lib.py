@@ -47,6 +47,8 @@ SIGNATURES = {
     "pg_info": (_c_int, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i32), ctypes.POINTER(_i32),
                          ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),
     "pg_destroy": (None, [_vp]),
+    "pg_estimate_omega": (_c_int, [_vp, _dbl, _i64, ctypes.POINTER(_dbl), ctypes.POINTER(_dbl)]),
+    "pg_dc": (_c_int, [_vp, _dbl, _dbl, _dbl, _c_int, _i64, ctypes.POINTER(PgStats)]),
     "pg_set_slab": (_c_int, [_vp, _i32, _i32, _i32]),
     "pg_nccl_unique_id": (_c_int, [_vp]),
     "pg_group_nccl": (_c_int, [_vp, _vp, _i32, _i32, _i32, ctypes.POINTER(_vp)]),

@@ -184,6 +184,25 @@ class Grid:
         return TransientResult(probes=probe_out if npr else None, sweeps=sweeps, stats=st,
                                status=code)
 
+    def estimate_omega(self, h, sweeps=2000):
+        """(rho_Jacobi, omega_opt) by Young's formula (pg_estimate_omega)."""
+        rho, om = ctypes.c_double(), ctypes.c_double()
+        L.check(self._lib.pg_estimate_omega(self._h, float(h), int(sweeps), ctypes.byref(rho),
+                                            ctypes.byref(om)))
+        return rho.value, om.value
+
+    def dc(self, t=0.0, tol=1e-10, omega=1.9, method="rbsor", max_sweeps=1000000,
+           raise_on_noconv=True):
+        """DC operating point G v = G0 Vdd - i(t) (pg_dc); returns the stats.
+        Voltages: ``voltages()``."""
+        m = {"rbsor": L.PG_METHOD_RBSOR, "jacobi": L.PG_METHOD_JACOBI}[method]
+        st = L.PgStats()
+        code = self._lib.pg_dc(self._h, float(t), float(tol), float(omega), m, int(max_sweeps),
+                               ctypes.byref(st))
+        if code not in (L.PG_OK, L.PG_ENOCONV) or (code == L.PG_ENOCONV and raise_on_noconv):
+            L.check(code)
+        return st
+
     # ------------------------------------------------------------------ cleanup
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:

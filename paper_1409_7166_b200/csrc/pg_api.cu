@@ -86,6 +86,8 @@ void free_grid(pg_grid *g) {
   for (void *p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t e : g->tev) cudaEventDestroy(e);
+  if (g->batch_exec) cudaGraphExecDestroy(g->batch_exec);
+  if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
   if (g->ctl_host) cudaFreeHost(g->ctl_host);
   if (g->done_host) cudaFreeHost(g->done_host);
   delete g;
@@ -323,6 +325,8 @@ PG_API int pg_set_option(pg_grid *g, const char *key, int64_t value) {
   } else if (k == "batch") {
     REQUIRE(value >= 1 && value <= 1024, "batch must be in 1..1024");
     g->batch = (int)value;
+  } else if (k == "graph") {
+    g->use_graph = value != 0;
   } else if (k == "timing") {
     g->timing = value != 0;
   } else if (k == "rows") {
@@ -462,9 +466,100 @@ PG_API int pg_transient(pg_grid *g, double h, int64_t steps, double tol, double 
                             probe_node, probe_out, mem, sweeps_out, stats);
 }
 
+PG_API int pg_dc(pg_grid *g, double t, double tol, double omega, int method, int64_t max_sweeps,
+                 pg_stats *stats) {
+  REQUIRE(g != nullptr, "grid is NULL");
+  REQUIRE(!g->slab, "slab grids are driven through a pg_group");
+  REQUIRE(std::isfinite(t), "t must be finite");
+  pg_grid *gs[1] = {g};
+  return pgb::run_transient(gs, 1, nullptr, INFINITY, 1, tol, omega, method, max_sweeps, 0, nullptr,
+                            nullptr, PG_MEM_HOST, nullptr, stats, t);
+}
+
+PG_API int pg_estimate_omega(pg_grid *g, double h, int64_t sweeps, double *rho, double *omega_opt) {
+  REQUIRE(g != nullptr, "grid is NULL");
+  REQUIRE(h > 0.0 && std::isfinite(h), "h must be finite and > 0");
+  REQUIRE(sweeps >= 8, "need at least 8 Jacobi sweeps");
+  cudaStream_t st = g->stream;
+  int rc;
+  unsigned long long *hist = nullptr;
+  if ((rc = dalloc(&hist, sweeps))) return rc;
+  struct Free {
+    void *p;
+    ~Free() { cudaFree(p); }
+  } fr{hist};
+  // Jacobi (omega = 1) on the homogeneous system M e = 0 from the start vector
+  // x(0): the differences V^(k) - V^(k-1) obey the same iteration, so the
+  // ratio of successive max-norms tends to the spectral radius of
+  // J = I - D^{-1} M (power iteration; Young: omega_opt = 2 / (1 + sqrt(1 - rho^2))
+  // for the red-black (consistently ordered, 2-cyclic) numbering)
+  CK(launch_setup(g, h));
+  CK(cudaMemsetAsync(g->b, 0, sizeof(double) * g->np, st));
+  CK(cudaMemcpyAsync(g->V[0], g->x0, sizeof(double) * g->np, cudaMemcpyDeviceToDevice, st));
+  CK(launch_reset_state(g));
+  int64_t launches = 0;
+  for (int64_t j = 0; j < sweeps; ++j) {
+    CK(launch_sweep(g, PG_METHOD_JACOBI, 1.0, 0.0, (int)j, 1, &launches));
+    CK(cudaMemcpyAsync(hist + j, &g->ctl->dmax[j & (kRing - 1)], sizeof(unsigned long long),
+                       cudaMemcpyDeviceToDevice, st));
+  }
+  std::vector<unsigned long long> hh((size_t)sweeps);
+  CK(cudaMemcpyAsync(hh.data(), hist, sizeof(unsigned long long) * sweeps, cudaMemcpyDeviceToHost, st));
+  CK(launch_reset_state(g));
+  CK(cudaMemcpyAsync(g->V[0], g->x0, sizeof(double) * g->np, cudaMemcpyDeviceToDevice, st));
+  CK(cudaStreamSynchronize(st));
+  auto val = [&](int64_t k) {
+    double d;
+    std::memcpy(&d, &hh[(size_t)k], sizeof(d));
+    return d;
+  };
+  const int64_t k1 = sweeps / 2, k2 = sweeps - 1;
+  const double a = val(k1), b = val(k2);
+  double r = 0.0;
+  if (a > 0.0 && b > 0.0) r = std::pow(b / a, 1.0 / (double)(k2 - k1));
+  if (!(r >= 0.0)) r = 0.0;
+  if (r > 1.0) r = 1.0;
+  if (rho) *rho = r;
+  if (omega_opt) *omega_opt = std::min(2.0 / (1.0 + std::sqrt(std::max(0.0, 1.0 - r * r))), 1.999);
+  return PG_OK;
+}
+
 }  // extern "C"
 
 namespace pgb {
+
+// CUDA graph of one full batch of sweep launches (launch indices 0..batch-1
+// relative to ctl->jbase, then jbase += batch), captured on a private stream
+// and cached per (omega, tol, method, F, batch, stream).  Replaying it replaces
+// `batch` + 1 host launches by one graph launch (small grids are launch-bound).
+int batch_graph(pg_grid *g, int method, double omega, double tol, int F) {
+  const double key[6] = {omega, tol, (double)method, (double)F, (double)g->batch,
+                         (double)(uintptr_t)g->stream};
+  if (g->batch_exec && std::memcmp(key, g->graph_key, sizeof(key)) == 0) return PG_OK;
+  if (g->batch_exec) {
+    cudaGraphExecDestroy(g->batch_exec);
+    g->batch_exec = nullptr;
+  }
+  if (!g->cap_stream) CK(cudaStreamCreateWithFlags(&g->cap_stream, cudaStreamNonBlocking));
+  cudaStream_t user = g->stream;
+  g->stream = g->cap_stream;
+  cudaGraph_t graph = nullptr;
+  int64_t dummy = 0;
+  cudaError_t e = cudaStreamBeginCapture(g->cap_stream, cudaStreamCaptureModeThreadLocal);
+  for (int b = 0; e == cudaSuccess && b < g->batch; ++b) e = launch_sweep(g, method, omega, tol, b, F, &dummy);
+  if (e == cudaSuccess) e = launch_batch_advance(g, g->batch);
+  cudaError_t e2 = cudaStreamEndCapture(g->cap_stream, &graph);
+  g->stream = user;
+  if (e == cudaSuccess) e = e2;
+  if (e == cudaSuccess) e = cudaGraphInstantiate(&g->batch_exec, graph, 0);
+  if (graph) cudaGraphDestroy(graph);
+  if (e != cudaSuccess) {
+    g->batch_exec = nullptr;
+    return cuda_fail(e, "capturing the sweep batch graph");
+  }
+  std::memcpy(g->graph_key, key, sizeof(key));
+  return PG_OK;
+}
 
 // Algorithm 1 over ng grids advanced in lockstep on grid 0's stream (ng > 1:
 // the slabs of a partitioned mesh, `ex` refreshes their ghost rows and makes
@@ -472,9 +567,10 @@ namespace pgb {
 int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, double tol,
                   double omega, int method, int64_t max_sweeps, int64_t n_probe,
                   const int64_t *probe_node, double *probe_out, int mem, int64_t *sweeps_out,
-                  pg_stats *stats) {
+                  pg_stats *stats, double t_dc) {
   pg_grid *g = gs[0];
-  REQUIRE(h > 0.0 && std::isfinite(h), "h must be finite and > 0");
+  const bool dc = std::isinf(h);  // DC analysis (pg_dc): one solve of G v = b(t_dc)
+  REQUIRE(h > 0.0 && (std::isfinite(h) || dc), "h must be finite and > 0");
   REQUIRE(steps >= 0, "steps must be >= 0");
   REQUIRE(omega > 0.0 && omega < 2.0, "omega must be in (0, 2) (Eq. (15) convergence range)");
   REQUIRE(method == PG_METHOD_RBSOR || method == PG_METHOD_JACOBI, "unknown method");
@@ -549,6 +645,7 @@ int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, d
   Ev evguard{evs};
 
   int64_t launches = 0;
+  const bool graph_ok = g->use_graph && ng == 1 && ex == nullptr && !g->timing;
   const int F = sweeps_per_launch(g, method);
   for (int k = 1; k < ng; ++k)
     REQUIRE(sweeps_per_launch(gs[k], method) == F, "grids of a group must use the same fuse option");
@@ -582,7 +679,7 @@ int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, d
   };
   for (int64_t s = 1; s <= steps; ++s) {
     for (int k = 0; k < ng; ++k) {
-      CK(launch_rhs(gs[k], h, s));
+      CK(launch_rhs(gs[k], h, dc ? t_dc : (double)s * h));
       launches += 1 + (gs[k]->npad > 0) + (gs[k]->nsrc > 0);
     }
     int64_t j = 0;
@@ -591,12 +688,22 @@ int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, d
     if (g->timing) CK(cudaEventRecord(tev(0), st));
     while (j < max_launch) {
       const int64_t nb = std::min<int64_t>(g->batch, max_launch - j);
-      for (int64_t b = 0; b < nb; ++b) {
-        const int nsw = (int)std::min<int64_t>(F, max_sweeps - (j + b) * F);
-        for (int k = 0; k < ng; ++k)
-          CK(launch_sweep(gs[k], method, omega, tol, (int)(j + b), nsw, &launches));
-        if (ex) CK(ex->after_sweep((int)(j + b), &launches));
-        if (g->timing) CK(cudaEventRecord(tev(j + b + 1), st));
+      // a full batch (batch launches of F sweeps) of a single grid replays the
+      // captured CUDA graph; launch indices are relative to ctl->jbase
+      const bool full = nb == g->batch && (j + nb) * F <= max_sweeps;
+      if (full && graph_ok && (j > 0 || g->batch_exec != nullptr)) {
+        if ((rc = batch_graph(g, method, omega, tol, F))) return rc;
+        CK(cudaGraphLaunch(g->batch_exec, st));
+        launches += nb + 1;
+      } else {
+        for (int64_t b = 0; b < nb; ++b) {
+          const int nsw = (int)std::min<int64_t>(F, max_sweeps - (j + b) * F);
+          for (int k = 0; k < ng; ++k) CK(launch_sweep(gs[k], method, omega, tol, (int)b, nsw, &launches));
+          if (ex) CK(ex->after_sweep((int)(j + b), (int)b, &launches));
+          if (g->timing) CK(cudaEventRecord(tev(j + b + 1), st));
+        }
+        for (int k = 0; k < ng; ++k) CK(launch_batch_advance(gs[k], (int)nb));
+        launches += ng;
       }
       j += nb;
       if (!(tol > 0.0) || j >= max_launch) continue;

@@ -96,6 +96,7 @@ const NcclApi &nccl() {
 // (then launches_done launches ran).
 __device__ __forceinline__ const double *current_v(const DevCtl *c, int j, const double *V0,
                                                    const double *V1) {
+  j += c->jbase;  // j is relative to the current batch
   const int64_t ran = c->done ? c->launches_done : (int64_t)j + 1;
   return ((c->base + ran) & 1) ? V1 : V0;
 }
@@ -163,7 +164,7 @@ struct pg_group : public pgb::Exchange {
   bool has_lo(int k) const { return (kind == 0 ? k : rank) > 0; }
   bool has_hi(int k) const { return (kind == 0 ? k : rank) < nranks - 1; }
 
-  cudaError_t after_sweep(int j, int64_t *launches) override {
+  cudaError_t after_sweep(int j, int jr, int64_t *launches) override {
     cudaStream_t st = slabs[0]->stream;
     const int slot = j & (kRing - 1);
     cudaError_t e;
@@ -181,7 +182,7 @@ struct pg_group : public pgb::Exchange {
     for (size_t k = 0; k < slabs.size(); ++k) {
       pg_grid *g = slabs[k];
       k_halo_pack<<<grid_for(2 * halo, g->num_sms), 256, 0, st>>>(
-          g->md, g->V[0], g->V[1], g->ctl, j, has_lo((int)k) ? g->y_begin : -1,
+          g->md, g->V[0], g->V[1], g->ctl, jr, has_lo((int)k) ? g->y_begin : -1,
           has_hi((int)k) ? g->y_end - G : -1, G, send_lo[k], send_hi[k]);
       ++*launches;
     }
@@ -210,7 +211,7 @@ struct pg_group : public pgb::Exchange {
     for (size_t k = 0; k < slabs.size(); ++k) {
       pg_grid *g = slabs[k];
       k_halo_unpack<<<grid_for(2 * halo, g->num_sms), 256, 0, st>>>(
-          g->md, g->V[0], g->V[1], g->ctl, j, has_lo((int)k) ? g->y_begin - G : -1,
+          g->md, g->V[0], g->V[1], g->ctl, jr, has_lo((int)k) ? g->y_begin - G : -1,
           has_hi((int)k) ? g->y_end : -1, G, recv_lo[k], recv_hi[k]);
       ++*launches;
     }

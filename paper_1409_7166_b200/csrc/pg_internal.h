@@ -24,6 +24,9 @@ struct DevCtl {
   int64_t sweeps_total;
   int64_t sweeps_max;
   double last_delta;
+  int32_t jbase;           // launch index of the first launch of the current batch:
+                           // a sweep kernel's launch index is jbase + its argument,
+                           // so one captured batch (CUDA graph) serves every batch
 };
 
 constexpr int kRing = 4;
@@ -121,6 +124,10 @@ struct pg_grid {
   int tma_state = 0;                   // 0 unknown, 1 usable, -1 unavailable
   CUtensorMap tmap[7];                 // V0, V1, gx, gy, gze, b, invd (encoded once)
   std::vector<cudaEvent_t> tev;        // timing event pool
+  int use_graph = 1;                   // option "graph": replay captured sweep batches
+  cudaGraphExec_t batch_exec = nullptr;  // captured batch of `batch` full sweep launches
+  cudaStream_t cap_stream = nullptr;     // private stream the batch graph is captured on
+  double graph_key[6] = {0, 0, 0, 0, 0, 0};  // omega, tol, method, F, batch, stream of the capture
 };
 
 namespace pgb {
@@ -129,9 +136,10 @@ int cuda_fail(cudaError_t e, const char *what);
 
 // kernels / launchers (pg_kernels.cu)
 cudaError_t launch_setup(pg_grid *g, double h);
-cudaError_t launch_rhs(pg_grid *g, double h, int64_t s);
+cudaError_t launch_rhs(pg_grid *g, double h, double t);
 cudaError_t launch_sweep(pg_grid *g, int method, double omega, double tol, int launch_idx,
                          int nsweeps, int64_t *launches);
+cudaError_t launch_batch_advance(pg_grid *g, int nb);
 cudaError_t launch_step_end(pg_grid *g, int64_t s, int launched, int flips, int fused,
                             int64_t max_sweeps, double tol);
 cudaError_t launch_inductor_update(pg_grid *g, double h);
@@ -153,12 +161,13 @@ cudaError_t launch_rb_sweep_fused(pg_grid *g, double omega, double tol, int j, i
 // (may be null) runs after every sweep launch of all grids.
 struct Exchange {
   virtual ~Exchange() = default;
-  virtual cudaError_t after_sweep(int launch_idx, int64_t *launches) = 0;
+  // launch_idx: index of the launch in the time step; rel: index in its batch
+  virtual cudaError_t after_sweep(int launch_idx, int rel, int64_t *launches) = 0;
 };
 int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, double tol,
                   double omega, int method, int64_t max_sweeps, int64_t n_probe,
                   const int64_t *probe_node, double *probe_out, int mem, int64_t *sweeps_out,
-                  pg_stats *stats);
+                  pg_stats *stats, double t_dc = 0.0);
 // upload / download helpers (pg_api.cu)
 int dalloc_bytes(void **p, size_t bytes);
 

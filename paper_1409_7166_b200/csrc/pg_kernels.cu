@@ -77,6 +77,7 @@ struct JacobiArgs {
 
 __global__ void __launch_bounds__(256) k_jacobi_mesh(JacobiArgs a) {
   __shared__ double wmax[8];
+  a.launch_idx += *(volatile int32_t *)&a.ctl->jbase;
   if (sweep_skip(a.ctl, a.launch_idx, a.tol, true)) return;
   zero_next_slot(a.ctl, a.launch_idx, true);
   const MeshDims d = a.d;
@@ -135,6 +136,7 @@ struct CsrArgs {
 
 __global__ void __launch_bounds__(256) k_csr_sweep(CsrArgs a) {
   __shared__ double wmax[8];
+  a.launch_idx += *(volatile int32_t *)&a.ctl->jbase;
   if (sweep_skip(a.ctl, a.launch_idx, a.tol, a.first != 0)) return;
   zero_next_slot(a.ctl, a.launch_idx, a.first != 0);
   double *V = (*(volatile int32_t *)&a.ctl->base) ? a.V1 : a.V0;
@@ -161,6 +163,7 @@ __global__ void __launch_bounds__(256) k_csr_sweep(CsrArgs a) {
 
 __global__ void __launch_bounds__(256) k_csr_jacobi(CsrArgs a) {
   __shared__ double wmax[8];
+  a.launch_idx += *(volatile int32_t *)&a.ctl->jbase;
   if (sweep_skip(a.ctl, a.launch_idx, a.tol, true)) return;
   zero_next_slot(a.ctl, a.launch_idx, true);
   const int par = (*(volatile int32_t *)&a.ctl->base + a.launch_idx) & 1;
@@ -198,6 +201,7 @@ __global__ void k_rhs_dense(int64_t np, const double *__restrict__ cap, double i
     ctl->done = 0;
     ctl->launches_done = 0;
     ctl->dmax[0] = 0ull;
+    ctl->jbase = 0;
   }
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < np;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -359,6 +363,8 @@ __global__ void k_step_end(DevCtl *c, int64_t s, int32_t launched, int32_t flips
   if (!conv && tol > 0.0 && c->failed == 0) c->failed = (int32_t)s;
 }
 
+__global__ void k_batch_advance(DevCtl *c, int32_t nb) { c->jbase += nb; }
+
 __global__ void k_probe(const double *V0, const double *V1, const DevCtl *c, const int64_t *idx,
                         int64_t n, double *out) {
   const double *V = c->base ? V1 : V0;
@@ -415,6 +421,8 @@ __global__ void k_reset_state(DevCtl *c) {
   c->sweeps_max = 0;
   c->last_delta = 0.0;
   c->launches_done = 0;
+  c->jbase = 0;
+  c->diag_bad = 0;
   for (int k = 0; k < kRing; ++k) c->dmax[k] = 0ull;
 }
 
@@ -484,7 +492,9 @@ cudaError_t launch_setup(pg_grid *g, double h) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_rhs(pg_grid *g, double h, int64_t s) {
+// right-hand side of the step ending at time t (loads evaluated at t); h may
+// be +inf (DC analysis: capacitors open, inductor history dropped)
+cudaError_t launch_rhs(pg_grid *g, double h, double t) {
   const double inv_h = 1.0 / h;
   const int B = 256;
   const bool rlc_vias = g->kind == 0 && g->lz != nullptr;
@@ -496,7 +506,7 @@ cudaError_t launch_rhs(pg_grid *g, double h, int64_t s) {
         g->npad_grp, g->pad_grp, g->pad_idx, g->pad_ge, g->pad_l, g->pad_i, g->vdd, inv_h, g->b);
   if (g->nsrc > 0)
     k_rhs_src<<<grid_for(g->nsrc_grp, B, g->num_sms), B, 0, g->stream>>>(
-        g->nsrc_grp, g->src_grp, g->src_idx, g->src_ptr, g->pwl_t, g->pwl_i, (double)s * h, g->b);
+        g->nsrc_grp, g->src_grp, g->src_idx, g->src_ptr, g->pwl_t, g->pwl_i, t, g->b);
   return cudaGetLastError();
 }
 
@@ -543,6 +553,11 @@ cudaError_t launch_sweep(pg_grid *g, int method, double omega, double tol, int j
       ++*launches;
     }
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_batch_advance(pg_grid *g, int nb) {
+  k_batch_advance<<<1, 1, 0, g->stream>>>(g->ctl, nb);
   return cudaGetLastError();
 }
 

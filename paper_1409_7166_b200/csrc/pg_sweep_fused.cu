@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(32 * L) k_rb_sweep_fused(const __grid_constant
   const int lane = threadIdx.x, l = threadIdx.y;
   const bool leader = lane == 0 && l == 0;
   DevCtl *ctl = P.ctl;
-  const int j = P.launch_idx;
+  const int j = *(volatile int32_t *)&ctl->jbase + P.launch_idx;
   const int nsw = P.nsw;
 
   // device-side convergence control (uniform over the grid): a launch after
