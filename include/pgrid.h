@@ -123,6 +123,9 @@ PG_API int pg_set_stream(pg_grid *g, void *stream);
  *   "graph"  1 (default): replay full batches of sweep launches from a captured
  *            CUDA graph (single grids, option "timing" off); 0: plain launches
  *   "rows"   rows per CTA of the mesh sweep (0: auto)
+ *   "width"  column pairs per strip of the mesh sweep: 32 (one warp per layer
+ *            row) or 64 (two warps; halves the x-halo share, needs 2x shared
+ *            memory); 0 = auto
  *   "stages" shared-memory ring stages S of the mesh sweep (0: auto =
  *            D (F-1) + 6); a (F, S, D) variant that is not compiled falls
  *            back to the default S, then to smaller F

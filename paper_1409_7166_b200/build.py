@@ -14,7 +14,9 @@ LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libpgb200.so")
 # debugging variant with cycle instrumentation of the sweep kernel (-DPG_PROF)
 PROF_LIB = os.path.join(LIBDIR, "libpgb200_prof.so")
-SOURCES = ["pg_kernels.cu", "pg_sweep_fused.cu", "pg_api.cu", "pg_group.cu", "pg_csr_build.cpp"]
+SOURCES = ["pg_sweep_fused_i1.cu", "pg_sweep_fused_i2.cu", "pg_sweep_fused_i3.cu", "pg_sweep_fused_i4.cu",
+           "pg_sweep_fused_i5.cu", "pg_kernels.cu", "pg_sweep_fused.cu", "pg_api.cu", "pg_group.cu",
+           "pg_csr_build.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",
@@ -35,14 +37,22 @@ def build(force: bool = False, verbose: bool = False, prof: bool = False) -> str
     lib = PROF_LIB if prof else LIB
     if not force and not prof and not _stale():
         return LIB
-    extra = ["-DPG_PROF"] if prof else []
+    # experiments: extra -D flags for the instrumented build only
+    extra = (["-DPG_PROF"] + os.environ.get("PG_EXTRA_DEFS", "").split()) if prof else []
     tag = "_prof" if prof else ""
     os.makedirs(LIBDIR, exist_ok=True)
-    objs = []
-    for src in SOURCES:
+
+    def compile_one(src):
         obj = os.path.join(LIBDIR, src.rsplit(".", 1)[0] + tag + ".o")
         cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
+        return src, obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    # translation units compile in parallel (the fused-sweep instances dominate)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    objs = []
+    for src, obj, r in results:
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError(f"nvcc failed for {src}")

@@ -332,6 +332,9 @@ PG_API int pg_set_option(pg_grid *g, const char *key, int64_t value) {
   } else if (k == "rows") {
     REQUIRE(value >= 0 && value <= (1 << 20), "rows must be >= 0");
     g->rows = (int)value;
+  } else if (k == "width") {
+    REQUIRE(value == 0 || value == 32 || value == 64, "width must be 0 (auto), 32 or 64");
+    g->width = (int)value;
   } else if (k == "stages") {
     REQUIRE(value == 0 || (value >= 6 && value <= 17), "stages must be 0 (auto) or 6..17");
     g->stages = (int)value;

@@ -119,10 +119,11 @@ struct pg_grid {
   int timing = 0;                      // per-launch events for the sweep kernel
   int rows = 0;                        // rows per CTA (0: auto)
   int stages = 0;                      // TMA ring stages (0: auto)
+  int width = 0;                       // strip width W in column pairs: 32, 64 (0: auto)
   size_t tma_smem_set = 0;             // dynamic smem attribute currently set
   const void *tma_kernel_set = nullptr;  // ... and for which kernel
   int tma_state = 0;                   // 0 unknown, 1 usable, -1 unavailable
-  CUtensorMap tmap[7];                 // V0, V1, gx, gy, gze, b, invd (encoded once)
+  CUtensorMap tmap[2][7];              // [W = 32 / 64] V0, V1, gx, gy, gze, b, invd (encoded once)
   std::vector<cudaEvent_t> tev;        // timing event pool
   int use_graph = 1;                   // option "graph": replay captured sweep batches
   cudaGraphExec_t batch_exec = nullptr;  // captured batch of `batch` full sweep launches
@@ -150,12 +151,13 @@ cudaError_t launch_scatter_user(pg_grid *g, const double *src_user_order, double
 int sweeps_per_launch(pg_grid *g, int method);
 // temporally blocked red-black sweep (pg_sweep_fused.cu)
 bool tma_available(pg_grid *g);
-int fused_exact_lanes(int F);
+int fused_exact_lanes(int F, int W);
 int fused_default_stages(int L, int F, int D);
-bool fused_variant_exists(int L, int F, int S, int D);
-int fused_ctas_per_sm(int L, int S);
+bool fused_variant_exists(int L, int F, int S, int D, int W);
+int fused_ctas_per_sm(int L, int S, int W);
 cudaError_t launch_rb_sweep_fused(pg_grid *g, double omega, double tol, int j, int nsw, int F,
-                                  int S, int D, int rows_per_cta, int y_begin, int y_end, int ypar);
+                                  int S, int D, int W, int rows_per_cta, int y_begin, int y_end,
+                                  int ypar);
 
 // Multi-grid driver (pg_api.cu): Algorithm 1 over ng grids in lockstep; `ex`
 // (may be null) runs after every sweep launch of all grids.

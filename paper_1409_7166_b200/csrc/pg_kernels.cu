@@ -438,29 +438,37 @@ static inline int grid_for(int64_t work, int block, int num_sms) {
 // Resolved (F, S, D) of the temporally blocked mesh sweep: the requested
 // options if that variant is compiled, else the largest compiled F <= fuse.
 struct FusedCfg {
-  int F, S, D;
+  int F, S, D, W;
 };
 static FusedCfg fused_cfg(const pg_grid *g) {
   const int L = g->md.L;
   for (int F = g->fuse; F >= 1; --F) {
-    const int D = g->lag;
-    if (g->stages > 0 && fused_variant_exists(L, F, g->stages, D)) return {F, g->stages, D};
-    const int S = fused_default_stages(L, F, D);
-    if (fused_variant_exists(L, F, S, D)) return {F, S, D};
-    if (fused_variant_exists(L, F, fused_default_stages(L, F, 3), 3)) return {F, fused_default_stages(L, F, 3), 3};
+    // auto width: 64 column pairs per strip (half the x-halo share) for fused
+    // launches where that variant fits in shared memory, else 32 (measured,
+    // profiles/README.md)
+    const int first = g->width == 64 || (g->width == 0 && F >= 2) ? 64 : 32;
+    const int widths[2] = {first, 32};
+    for (int W : widths) {
+      const int D = g->lag;
+      if (g->stages > 0 && fused_variant_exists(L, F, g->stages, D, W)) return {F, g->stages, D, W};
+      const int S = fused_default_stages(L, F, D);
+      if (fused_variant_exists(L, F, S, D, W)) return {F, S, D, W};
+      const int S3 = fused_default_stages(L, F, 3);
+      if (fused_variant_exists(L, F, S3, 3, W)) return {F, S3, 3, W};
+    }
   }
-  return {1, 6, 3};
+  return {1, 6, 3, 32};
 }
 
 int sweeps_per_launch(pg_grid *g, int method) {
   return (g->kind == 0 && method == PG_METHOD_RBSOR) ? fused_cfg(g).F : 1;
 }
 
-int fused_rows_per_cta(const pg_grid *g, int F, int S, int ny) {
+int fused_rows_per_cta(const pg_grid *g, int F, int S, int W, int ny) {
   if (g->rows > 0) return std::max(1, std::min(g->rows, ny));
-  const int I = fused_exact_lanes(F);
+  const int I = fused_exact_lanes(F, W);
   const int strips = (g->md.HP + I - 1) / I;
-  int chunks = (g->num_sms * fused_ctas_per_sm(g->md.L, S)) / strips;
+  int chunks = (g->num_sms * fused_ctas_per_sm(g->md.L, S, W)) / strips;
   if (chunks < 1) chunks = 1;
   int H = (ny + chunks - 1) / chunks;
   if (H < 1) H = 1;
@@ -517,9 +525,9 @@ cudaError_t launch_sweep(pg_grid *g, int method, double omega, double tol, int j
       if (!tma_available(g)) return cudaErrorNotSupported;
       const FusedCfg c = fused_cfg(g);
       const int y0 = g->slab ? g->y_begin : 0, y1 = g->slab ? g->y_end : g->md.NY;
-      const int H = fused_rows_per_cta(g, c.F, c.S, y1 - y0);
+      const int H = fused_rows_per_cta(g, c.F, c.S, c.W, y1 - y0);
       ++*launches;
-      return launch_rb_sweep_fused(g, omega, tol, j, nsweeps, c.F, c.S, c.D, H, y0, y1,
+      return launch_rb_sweep_fused(g, omega, tol, j, nsweeps, c.F, c.S, c.D, c.W, H, y0, y1,
                                    g->slab ? g->ypar : 0);
     }
     JacobiArgs a;

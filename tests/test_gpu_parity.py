@@ -83,16 +83,17 @@ FUSED_SHAPES = [(2, 6, 5), (1, 1, 1), (4, 9, 70), (2, 33, 31), (8, 5, 3), (4, 40
 
 
 @pytest.mark.parametrize("shape", FUSED_SHAPES)
-@pytest.mark.parametrize("F,lag,rows", [(1, 3, 0), (2, 3, 0), (3, 3, 0), (4, 3, 0), (2, 4, 0), (2, 3, 7),
-                                        (3, 3, 4), (4, 3, 64)])
-def test_fused_sweep_iterates_equal_oracle(pgb, shape, F, lag, rows):
+@pytest.mark.parametrize("F,lag,rows,width", [(1, 3, 0, 32), (2, 3, 0, 32), (3, 3, 0, 32), (4, 3, 0, 32),
+                                              (2, 4, 0, 32), (2, 3, 7, 32), (3, 3, 4, 32), (4, 3, 64, 32),
+                                              (1, 3, 0, 64), (2, 3, 0, 64), (3, 3, 0, 64), (2, 3, 5, 64)])
+def test_fused_sweep_iterates_equal_oracle(pgb, shape, F, lag, rows, width):
     # F red-black SOR sweeps per streaming pass (temporal blocking);
     # k = 5 sweeps per step exercises the partial last launch (nsw < F)
     g = mk(*shape, seed=3 * sum(shape) + F)
     steps, k, omega = 4, 5, 1.6
     ro, _ = oracle_run(g, steps, tol=0.0, omega=omega, max_sweeps=k)
     rg, V = gpu_run(pgb, g, steps, tol=0.0, omega=omega, max_sweeps=k,
-                    options={"fuse": F, "lag": lag, "rows": rows})
+                    options={"fuse": F, "lag": lag, "rows": rows, "width": width})
     assert np.all(rg.sweeps[1:] == k)
     np.testing.assert_allclose(rg.probes, ro.V[:, :g.n], rtol=0, atol=ATOL_ITER)
     np.testing.assert_allclose(V, ro.V[-1, :g.n], rtol=0, atol=ATOL_ITER)
