@@ -416,9 +416,21 @@ __global__ void __launch_bounds__(W * L) k_rb_sweep_fused(const __grid_constant_
       dA = dA > dB ? dA : dB;
       dmax = dA > dmax ? dA : dmax;
       if (out_row) {
-        const double *R = ring + md(u - D * last) * SE;
-        vout_e[(int64_t)ro * P.NXP] = R[pe];
-        vout_o[(int64_t)ro * P.NXP] = R[po];
+        // both colours of row ro are final: black from this step, red from the
+        // previous one (registers on the steady path, else the staged row)
+        double ve, vo;
+        if (steady && last == F - 1) {
+          const double vb = vB[F - 1], vr = redF[F - 1][md3(u - 1)];
+          const bool eb = lpar ^ (ro & 1) ^ 1;
+          ve = eb ? vr : vb;
+          vo = eb ? vb : vr;
+        } else {
+          const double *R = ring + md(u - D * last) * SE;
+          ve = R[pe];
+          vo = R[po];
+        }
+        vout_e[(int64_t)ro * P.NXP] = ve;
+        vout_o[(int64_t)ro * P.NXP] = vo;
       }
       PROF_T(t5);
       PROF_T(t6);
