@@ -93,3 +93,28 @@ def test_slab_errors(pgb):
     with pytest.raises(P.PgError):               # slab grids are driven by their group
         grp.grids[0].transient(g.h, 2, tol=0.0, omega=1.5, max_sweeps=3)
     grp.close()
+
+
+def test_nccl_group_single_rank(pgb):
+    # the NCCL transport end to end on one GPU: dlopen of libnccl, unique id,
+    # communicator, the per-launch norm allreduce (a 1-rank group has no
+    # neighbours, so no send/recv) -- same results as the plain grid
+    import os
+    import torch
+    import torch.distributed as dist
+    P = pgb
+    g = gridgen.mesh_grid(4, 40, 70, seed=4, pad_pitch=5, src_frac=0.4, h=10e-12,
+                          src_start=20e-12, src_width=40e-12)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29531")
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        grp = P.SlabGroup.nccl(g, 0, 1, fuse=2)
+        rn = grp.transient(g.h, 6, tol=1e-10, omega=1.8, max_sweeps=200000)
+        (sp, Vn), = grp.owned_voltages(g)
+        grp.close()
+    finally:
+        dist.destroy_process_group()
+    r1, V1 = single(P, g, 6, 1e-10, 1.8, 200000, 2)
+    np.testing.assert_array_equal(rn.sweeps, r1.sweeps)
+    np.testing.assert_array_equal(Vn, V1)
