@@ -134,48 +134,42 @@ struct FusedParams {
   unsigned long long *prof; // PG_PROF builds: 8 cycle counters (else unused)
 };
 
-// One red-black node update (Eq. (13) + (15)) of the node at offset `me` of
-// row stage Ry (row r-1 in Rn, row r+1 in Rs); `ow`/`oe` are the offsets of
-// its west/east neighbours (other parity half of the same layer row).
-// Returns the new value; the caller stores it (the stores of all levels of a
-// phase are issued after all their loads, so the levels' dependency chains
-// overlap: the compiler cannot reorder a shared store before a later load).
-// Padding columns (x >= NX) and out-of-grid columns (TMA zero fill) have
-// V = b = 1/d = 0 and zero conductances, so the update leaves them at 0 and
-// needs no mask.
-template <int L, int RW>
-__device__ __forceinline__ double node_update(const double *Ry, const double *Rn, const double *Rs,
-                                              int me, int ow, int oe, double w, bool has_down,
-                                              double &Vc) {
+// The constants of one node update: x links (west, east), y links (north,
+// south), vias (up, down), b and 1/d.
+struct NodeC {
+  double gxW, gxE, gyN, gyS, gzU, gzD, b, id;
+};
+
+// Loads a node's constants from its staged row Ry (row r-1 in Rn); the south
+// link is taken from `gyS` when the caller already holds it (gyS_known).
+template <int L, int RW, bool gyS_known = false>
+__device__ __forceinline__ NodeC load_c(const double *Ry, const double *Rn, int me, int ow, bool has_down,
+                                        double gyS = 0.0) {
   constexpr int LAY = L * RW;
   constexpr int GX = 1 * LAY, GY = 2 * LAY, GZ = 3 * LAY, BB = 4 * LAY, ID = 5 * LAY;
-  Vc = Ry[me];
-  double s1 = fma(Ry[GX + ow], Ry[ow], Ry[BB + me]);      // west link g(x-1,x) + K_i (b)
-  s1 = fma(Ry[GX + me], Ry[oe], s1);                      // east link g(x,x+1)
-  s1 = fma(Rn[GY + me], Rn[me], s1);                      // north (row r-1)
-  double s2 = Ry[GY + me] * Rs[me];                       // south (row r+1)
-  s2 = fma(Ry[GZ + me], Ry[me + RW], s2);                 // via up (layer l+1)
-  if (has_down) s2 = fma(Ry[GZ + me - RW], Ry[me - RW], s2);  // via down (layer l-1)
-  return fma(w, (s1 + s2) * Ry[ID + me] - Vc, Vc);
+  NodeC c;
+  c.gxW = Ry[GX + ow];
+  c.gxE = Ry[GX + me];
+  c.gyN = Rn[GY + me];
+  c.gyS = gyS_known ? gyS : Ry[GY + me];
+  c.gzU = Ry[GZ + me];
+  c.gzD = has_down ? Ry[GZ + me - RW] : 0.0;
+  c.b = Ry[BB + me];
+  c.id = Ry[ID + me];
+  return c;
 }
 
-// Same update with the operands a thread may already hold in registers passed
-// in: Vc (the node), VW / VE (x neighbours), VN / VS (rows r-1 / r+1), the
-// north and south link conductances gyN / gyS.  The rest (x links, vias, b,
-// 1/d) comes from the staged row Ry.
-template <int L, int RW>
-__device__ __forceinline__ double node_update_r(const double *Ry, int me, int ow, double w,
-                                                bool has_down, double Vc, double VW, double VE,
-                                                double VN, double VS, double gyN, double gyS) {
-  constexpr int LAY = L * RW;
-  constexpr int GX = 1 * LAY, GZ = 3 * LAY, BB = 4 * LAY, ID = 5 * LAY;
-  double s1 = fma(Ry[GX + ow], VW, Ry[BB + me]);          // west link g(x-1,x) + K_i (b)
-  s1 = fma(Ry[GX + me], VE, s1);                          // east link g(x,x+1)
-  s1 = fma(gyN, VN, s1);                                  // north (row r-1)
-  double s2 = gyS * VS;                                   // south (row r+1)
-  s2 = fma(Ry[GZ + me], Ry[me + RW], s2);                 // via up (layer l+1)
-  if (has_down) s2 = fma(Ry[GZ + me - RW], Ry[me - RW], s2);  // via down (layer l-1)
-  return fma(w, (s1 + s2) * Ry[ID + me] - Vc, Vc);
+// Eq. (13) + (15) from the constants and the neighbour values (VU / VD: via
+// neighbours in layers l+1 / l-1; gzD = 0 in layer 0 cancels VD).
+__device__ __forceinline__ double upd_c(const NodeC &c, double w, double Vc, double VW, double VE,
+                                        double VN, double VS, double VU, double VD) {
+  double s1 = fma(c.gxW, VW, c.b);
+  s1 = fma(c.gxE, VE, s1);
+  s1 = fma(c.gyN, VN, s1);
+  double s2 = c.gyS * VS;
+  s2 = fma(c.gzU, VU, s2);
+  s2 = fma(c.gzD, VD, s2);
+  return fma(w, (s1 + s2) * c.id - Vc, Vc);
 }
 
 template <int L, int F, int S, int D, int W>
@@ -299,6 +293,9 @@ __global__ void __launch_bounds__(W * L) k_rb_sweep_fused(const __grid_constant_
   auto sweep_pass = [&](const int last) {
     const int y_end_loop = r_last + D * last;
     double redF[F][D], blkF[F][D];  // values this thread stored at the last D steps
+    // F == 2: constants level 0 loaded at the last D steps (level 1 reuses them)
+    constexpr bool kReuseC = F == 2;
+    NodeC cRedF[kReuseC ? D : 1], cBlkF[kReuseC ? D : 1];
 #pragma unroll
     for (int f = 0; f < F; ++f)
 #pragma unroll
@@ -318,6 +315,7 @@ __global__ void __launch_bounds__(W * L) k_rb_sweep_fused(const __grid_constant_
       double vA[F], cA[F], nA[F], gA[F];
       {
         double *ad[F];
+        NodeC c0;
 #pragma unroll
         for (int f = 0; f < F; ++f) {
           const int r = y - D * f;
@@ -332,13 +330,17 @@ __global__ void __launch_bounds__(W * L) k_rb_sweep_fused(const __grid_constant_
           if (f > 0 && steady) VN = blkF[f - 1][md3(u - D)]; else VN = Rn[me];
           if (f > 0 && steady) VS = blkF[f - 1][md3(u - D + 2)]; else VS = Rs[me];
           const double Voth = Ry[oth];
-          const double gyN = Rn[GY + me];
+          // constants: level 1 of a 2-sweep launch reuses those level 0 loaded
+          // for the same node D steps ago
+          NodeC c;
+          if (kReuseC && f == 1 && steady) c = cRedF[md3(u - D)];  // (== md3(u): read before the push)
+          else c = load_c<L, RW>(Ry, Rn, me, e ? own : oth, has_down);
+          if (kReuseC && f == 0) c0 = c;
           ad[f] = const_cast<double *>(Ry) + me;
-          vA[f] = node_update_r<L, RW>(Ry, me, e ? own : oth, w, has_down, Vc, e ? Vown : Voth,
-                                       e ? Voth : Vown, VN, VS, gyN, Ry[GY + me]);
+          vA[f] = upd_c(c, w, Vc, e ? Vown : Voth, e ? Voth : Vown, VN, VS, Ry[me + RW], Ry[me - RW]);
           cA[f] = Vc;
           nA[f] = VN;
-          gA[f] = gyN;
+          gA[f] = c.gyN;
         }
 #pragma unroll
         for (int f = 0; f < F; ++f) {
@@ -349,6 +351,7 @@ __global__ void __launch_bounds__(W * L) k_rb_sweep_fused(const __grid_constant_
           dA = f == last ? d : dA;
           vA[f] = in ? vA[f] : cA[f];  // the value the row now holds
         }
+        if (kReuseC) cRedF[md3(u)] = c0;
       }
       {
         const int r = y - D * last;
@@ -375,6 +378,7 @@ __global__ void __launch_bounds__(W * L) k_rb_sweep_fused(const __grid_constant_
       double vB[F];
       {
         double cB[F], *ad[F];
+        NodeC c0;
 #pragma unroll
         for (int f = 0; f < F; ++f) {
           const int r = y - D * f - 1;
@@ -387,9 +391,12 @@ __global__ void __launch_bounds__(W * L) k_rb_sweep_fused(const __grid_constant_
           if (steady) Vown = redF[f][md3(u - 1)]; else Vown = Ry[own];
           if (steady) VN = redF[f][md3(u - 2)]; else VN = Rn[me];
           const double Voth = Ry[oth];
+          NodeC c;
+          if (kReuseC && f == 1 && steady) c = cBlkF[md3(u - D)];
+          else c = load_c<L, RW, true>(Ry, Rn, me, e ? own : oth, has_down, gA[f]);
+          if (kReuseC && f == 0) c0 = c;
           ad[f] = const_cast<double *>(Ry) + me;
-          vB[f] = node_update_r<L, RW>(Ry, me, e ? own : oth, w, has_down, Vc, e ? Vown : Voth,
-                                       e ? Voth : Vown, VN, vA[f], Rn[GY + me], gA[f]);
+          vB[f] = upd_c(c, w, Vc, e ? Vown : Voth, e ? Voth : Vown, VN, vA[f], Ry[me + RW], Ry[me - RW]);
           cB[f] = Vc;
         }
 #pragma unroll
@@ -401,6 +408,7 @@ __global__ void __launch_bounds__(W * L) k_rb_sweep_fused(const __grid_constant_
           dB = f == last ? d : dB;
           vB[f] = in ? vB[f] : cB[f];
         }
+        if (kReuseC) cBlkF[md3(u)] = c0;
       }
       PROF_T(t4);
       // register FIFOs: entry (step index mod D); S % D == 0 keeps it a

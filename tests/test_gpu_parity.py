@@ -179,14 +179,14 @@ def test_csr_grid(pgb):
     o = nodal.NodalOracle(nl)
     order = nodal.red_black_order(2, 20, 18)   # BFS parity of a connected mesh subgraph
     ro = o.transient(g.h, steps, tol=0.0, omega=1.5, order=order, Itab=It, max_sweeps=7)
-    rg, _ = gpu_run(pgb, g, steps, tol=0.0, omega=1.5, max_sweeps=7
+    rg, _ = gpu_run(pgb, g, steps, tol=0.0, omega=1.5, max_sweeps=7)
     np.testing.assert_allclose(rg.probes, ro.V, rtol=0, atol=ATOL_ITER)
     ro = o.transient(g.h, steps, tol=1e-12, omega=1.7, Itab=It)
-    rg, _ = gpu_run(pgb, g, steps, tol=1e-12, omega=1.7
+    rg, _ = gpu_run(pgb, g, steps, tol=1e-12, omega=1.7)
     np.testing.assert_allclose(rg.probes, ro.V, rtol=0, atol=ATOL_CONV)
-    # weighted Jacobi on the CSR / ELL rows
+    # weighted Jacobi on the CSR rows
     ro = o.transient(g.h, steps, tol=0.0, omega=0.9, method="jacobi", Itab=It, max_sweeps=5)
-    rg, _ = gpu_run(pgb, g, steps, tol=0.0, omega=0.9, method="jacobi", max_sweeps=5
+    rg, _ = gpu_run(pgb, g, steps, tol=0.0, omega=0.9, method="jacobi", max_sweeps=5)
     np.testing.assert_allclose(rg.probes, ro.V, rtol=0, atol=ATOL_ITER)
 
 
