@@ -53,6 +53,10 @@ def parse():
     ap.add_argument("--omega", type=float, default=None)
     ap.add_argument("--tol", type=float, default=1e-10)
     ap.add_argument("--method", default="rbsor", choices=["rbsor", "jacobi"])
+    ap.add_argument("--slabs", type=int, default=1,
+                    help="N = 1 only: split the mesh into this many row slabs advanced by the "
+                         "single-process group (pg_group_local): the multi-GPU protocol's "
+                         "exchange cost measured on one GPU")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="N > 1: weak = config rows x N (fixed work per GPU), strong = config split")
     ap.add_argument("--opt", action="append", default=[],
@@ -237,6 +241,10 @@ def run_b200(args):
         G = grp.grids[0]
         sp = grp.specs[0]
         my_nodes = g.layers * (sp.y1 - sp.y0) * g.nx
+    elif args.slabs > 1:
+        grp = P.SlabGroup.local(g, args.slabs, fuse=fuse, stream=stream)
+        G = grp.grids[0]
+        my_nodes = g.n
     else:
         grp = None
         mk = P.Grid.from_mesh_grid if hasattr(g, "gx") else P.Grid.from_edge_grid
@@ -245,7 +253,8 @@ def run_b200(args):
         my_nodes = g.n
     G.set_option("timing", 1)
     for k, v in opts.items():
-        G.set_option(k, int(v))
+        for q in (grp.grids if grp is not None else [G]):
+            q.set_option(k, int(v))
     # relaxation factor: Young's optimum from the library's Jacobi power
     # iteration (§IV-D refers to Young), unless given; not timed
     t_om = time.perf_counter()
@@ -311,7 +320,8 @@ def run_b200(args):
     avg_launch_ms = sweep_ms / max(sweep_launches, 1)
     F = int(r.stats.sweeps_per_launch)
     if hasattr(g, "gx"):
-        launch_nodes = G.info()["layers"] * G.info()["ny"] * G.info()["nx"]
+        grids = grp.grids if grp is not None else [G]   # local group: one launch = all slabs
+        launch_nodes = sum(q.info()["layers"] * q.info()["ny"] * q.info()["nx"] for q in grids)
         bytes_per_launch = BYTES_PER_NODE_PASS * launch_nodes
         kname = "k_rb_sweep_fused"
     else:
@@ -363,7 +373,7 @@ def run_b200(args):
         e2e = {"value": float(ns.item()) / (float(te.item()) * 1e-3) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": float(te.item()) / nrep, "per_rank_bytes": True}
-    elif not args.no_e2e:
+    elif not args.no_e2e and args.slabs <= 1:
         pin = {}
         for name in ("gx", "gy", "gz", "cap", "lz"):
             a = getattr(g, name, None)
@@ -430,7 +440,8 @@ def run_b200(args):
                        "l2": "per-sweep working set ~56 B/node x n > 126 MB L2 (no flush needed)",
                        "parallelism": (f"slab{world}: rows split over {world} GPUs, NCCL ghost-row "
                                        f"exchange + norm allreduce per sweep launch") if world > 1
-                       else "1 GPU"},
+                       else (f"1 GPU, {args.slabs} row slabs exchanged in one process (pg_group_local)"
+                             if args.slabs > 1 else "1 GPU")},
             "clocks": ck, "e2e": e2e, "gpu_launches": launches, "roofline": roof,
             "cpu_baseline": cpu,
         }

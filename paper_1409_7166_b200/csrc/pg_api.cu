@@ -317,7 +317,7 @@ PG_API int pg_set_option(pg_grid *g, const char *key, int64_t value) {
   REQUIRE(g != nullptr && key != nullptr, "grid/key is NULL");
   const std::string k(key);
   if (k == "fuse") {
-    REQUIRE(value >= 1 && value <= 4, "fuse must be in 1..4");
+    REQUIRE(value >= 0 && value <= 4, "fuse must be 0 (auto) or 1..4");
     g->fuse = (int)value;
   } else if (k == "lag") {
     REQUIRE(value == 3 || value == 4, "lag must be 3 or 4");

@@ -113,7 +113,7 @@ struct pg_grid {
   int32_t y_begin = 0, y_end = 0, ypar = 0;
 
   // ---- options
-  int fuse = 2;                        // F: sweeps per launch of the temporally blocked mesh sweep
+  int fuse = 0;                        // F: sweeps per launch of the temporally blocked mesh sweep (0: auto)
   int lag = 3;                         // wavefront lag D between fused levels (3 or 4)
   int batch = 8;
   int timing = 0;                      // per-launch events for the sweep kernel

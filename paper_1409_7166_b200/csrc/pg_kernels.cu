@@ -440,9 +440,23 @@ static inline int grid_for(int64_t work, int block, int num_sms) {
 struct FusedCfg {
   int F, S, D, W;
 };
+int auto_rows_per_cta(const pg_grid *g, int F, int S, int W, int ny);
+static FusedCfg fused_cfg_for(const pg_grid *g, int fuse);
+
+// fuse = 0 (auto): F = 2 sweeps per launch, unless the grid is so small that
+// one wave of CTAs gets fewer than 16 rows each -- then the 4F-1 halo rows and
+// the D(F-1) pipeline steps dominate a launch's latency and F = 1 is faster
 static FusedCfg fused_cfg(const pg_grid *g) {
+  if (g->fuse > 0) return fused_cfg_for(g, g->fuse);
+  const FusedCfg c2 = fused_cfg_for(g, 2);
+  const int ny = g->slab ? g->y_end - g->y_begin : g->md.NY;
+  if (c2.F == 2 && auto_rows_per_cta(g, 2, c2.S, c2.W, ny) >= 16) return c2;
+  return fused_cfg_for(g, 1);
+}
+
+static FusedCfg fused_cfg_for(const pg_grid *g, int fuse) {
   const int L = g->md.L;
-  for (int F = g->fuse; F >= 1; --F) {
+  for (int F = fuse; F >= 1; --F) {
     // auto width: 64 column pairs per strip (half the x-halo share) for fused
     // launches where that variant fits in shared memory, else 32 (measured,
     // profiles/README.md)
@@ -466,6 +480,11 @@ int sweeps_per_launch(pg_grid *g, int method) {
 
 int fused_rows_per_cta(const pg_grid *g, int F, int S, int W, int ny) {
   if (g->rows > 0) return std::max(1, std::min(g->rows, ny));
+  return auto_rows_per_cta(g, F, S, W, ny);
+}
+
+// rows per CTA so that strips x chunks fill one wave of resident CTAs
+int auto_rows_per_cta(const pg_grid *g, int F, int S, int W, int ny) {
   const int I = fused_exact_lanes(F, W);
   const int strips = (g->md.HP + I - 1) / I;
   int chunks = (g->num_sms * fused_ctas_per_sm(g->md.L, S, W)) / strips;

@@ -157,9 +157,10 @@ def test_config0_full_size_converged(pgb):
     assert ro.status == 0 and rg.status == 0
     np.testing.assert_allclose(rg.probes, ro.V, rtol=0, atol=ATOL_CONV)
     # same numbering, same arithmetic up to rounding -> same sweep counts almost
-    # everywhere (the default sweep tests convergence every F = 2 sweeps)
+    # everywhere (the sweep tests convergence every F sweeps; auto F is 1 on
+    # this small grid)
     F = int(rg.stats.sweeps_per_launch)
-    assert F == 2
+    assert F in (1, 2)
     assert np.mean(rg.sweeps[1:] == -(-ro.sweeps[1:] // F) * F) > 0.9
 
 
