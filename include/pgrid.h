@@ -117,8 +117,7 @@ PG_API int pg_set_stream(pg_grid *g, void *stream);
 
 /* Tuning knobs (key, value); unknown keys -> PG_EINVAL.
  *   "fuse"   F, sweeps fused per launch of the temporally blocked mesh sweep,
- *            1..4, or 0 (default, auto: 2, or 1 on grids so small that a wave
- *            of CTAs gets < 16 rows each); Jacobi and CSR sweeps run 1 per launch
+ *            1..4, or 0 (default: 2); Jacobi and CSR sweeps run 1 per launch
  *   "lag"    wavefront lag D (rows) between fused sweep levels: 3 (default) or 4
  *   "batch"  sweep launches enqueued between host convergence polls, >= 1
  *   "graph"  1 (default): replay full batches of sweep launches from a captured

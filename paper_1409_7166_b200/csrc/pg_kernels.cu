@@ -443,16 +443,10 @@ struct FusedCfg {
 int auto_rows_per_cta(const pg_grid *g, int F, int S, int W, int ny);
 static FusedCfg fused_cfg_for(const pg_grid *g, int fuse);
 
-// fuse = 0 (auto): F = 2 sweeps per launch, unless the grid is so small that
-// one wave of CTAs gets fewer than 16 rows each -- then the 4F-1 halo rows and
-// the D(F-1) pipeline steps dominate a launch's latency and F = 1 is faster
-static FusedCfg fused_cfg(const pg_grid *g) {
-  if (g->fuse > 0) return fused_cfg_for(g, g->fuse);
-  const FusedCfg c2 = fused_cfg_for(g, 2);
-  const int ny = g->slab ? g->y_end - g->y_begin : g->md.NY;
-  if (c2.F == 2 && auto_rows_per_cta(g, 2, c2.S, c2.W, ny) >= 16) return c2;
-  return fused_cfg_for(g, 1);
-}
+
+// fuse = 0 (auto): F = 2 sweeps per launch (fastest per sweep on every
+// measured grid, including the 8192-node config 0)
+static FusedCfg fused_cfg(const pg_grid *g) { return fused_cfg_for(g, g->fuse > 0 ? g->fuse : 2); }
 
 static FusedCfg fused_cfg_for(const pg_grid *g, int fuse) {
   const int L = g->md.L;
