@@ -666,6 +666,7 @@ int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, d
     CK(launch_setup(q, h));
     launches += 4;
   }
+  if (ex) CK(ex->begin());
   if (n_probe > 0) {
     CK(launch_probe(g, d_pidx, n_probe, d_pout));
     ++launches;
@@ -719,6 +720,7 @@ int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, d
       pending = slot;
       slot ^= 1;
     }
+    if (ex) CK(ex->end_step(&launches));
     for (int k = 0; k < ng; ++k) {
       CK(launch_step_end(gs[k], s, (int)j, flips, F, max_sweeps, tol));
       ++launches;

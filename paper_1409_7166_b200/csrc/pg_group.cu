@@ -6,8 +6,11 @@
 //      device-side stopping test of the next launch is global (ncclAllReduce on
 //      the 8-byte norm slot; bit pattern of a non-negative double, so the
 //      unsigned max is the double max);
-//   2. copies the G owned rows next to each boundary into the neighbour's
-//      ghost rows (pack kernel -> ncclSend/ncclRecv -> unpack kernel).
+//   2. sends the G owned rows next to each boundary to the neighbour: the
+//      sweep kernel itself writes them to a send buffer as it finishes them,
+//      ncclSend/ncclRecv move them, and the next sweep launch reads its ghost
+//      rows straight from the receive buffer through a TMA tensor map (no pack
+//      or unpack kernel per launch; one unpack into V per time step).
 // A fused launch with F sweeps recomputes the 2F rows next to its owned range
 // from ghost data (pg_sweep_fused.cu), so G >= 2F ghost rows exchanged every
 // launch reproduce the single-grid red-black iterates exactly.
@@ -178,15 +181,9 @@ struct pg_group : public pgb::Exchange {
       unsigned long long *p = &slabs[0]->ctl->dmax[slot];
       if (N.AllReduce(p, p, 1, ncclUint64, ncclMax, comm, st) != ncclSuccess) return cudaErrorUnknown;
     }
-    // 2. pack the G owned rows next to each boundary
-    for (size_t k = 0; k < slabs.size(); ++k) {
-      pg_grid *g = slabs[k];
-      k_halo_pack<<<grid_for(2 * halo, g->num_sms), 256, 0, st>>>(
-          g->md, g->V[0], g->V[1], g->ctl, jr, has_lo((int)k) ? g->y_begin : -1,
-          has_hi((int)k) ? g->y_end - G : -1, G, send_lo[k], send_hi[k]);
-      ++*launches;
-    }
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    // 2. the sweep kernel already wrote the G owned rows next to each
+    //    boundary into the send buffers; the next launch reads its ghost rows
+    //    from the receive buffers (no pack / unpack per launch)
     // 3. transport
     const size_t bytes = sizeof(double) * (size_t)halo;
     if (kind == 0) {
@@ -207,11 +204,29 @@ struct pg_group : public pgb::Exchange {
       }
       if (N.GroupEnd() != ncclSuccess || !ok) return cudaErrorUnknown;
     }
-    // 4. unpack into the ghost rows
+    return cudaGetLastError();
+  }
+
+  // initial state: the ghost rows of V[0] (x(0)) seed the receive buffers
+  cudaError_t begin() override {
+    cudaStream_t st = slabs[0]->stream;
+    for (size_t k = 0; k < slabs.size(); ++k) {
+      pg_grid *g = slabs[k];
+      k_halo_pack<<<grid_for(2 * halo, g->num_sms), 256, 0, st>>>(
+          g->md, g->V[0], g->V[1], g->ctl, -1, has_lo((int)k) ? g->y_begin - G : -1,
+          has_hi((int)k) ? g->y_end : -1, G, recv_lo[k], recv_hi[k]);
+    }
+    return cudaGetLastError();
+  }
+
+  // end of a step: the received ghost rows go into V (the right-hand side and
+  // the inductor update of the next step read them there)
+  cudaError_t end_step(int64_t *launches) override {
+    cudaStream_t st = slabs[0]->stream;
     for (size_t k = 0; k < slabs.size(); ++k) {
       pg_grid *g = slabs[k];
       k_halo_unpack<<<grid_for(2 * halo, g->num_sms), 256, 0, st>>>(
-          g->md, g->V[0], g->V[1], g->ctl, jr, has_lo((int)k) ? g->y_begin - G : -1,
+          g->md, g->V[0], g->V[1], g->ctl, -1, has_lo((int)k) ? g->y_begin - G : -1,
           has_hi((int)k) ? g->y_end : -1, G, recv_lo[k], recv_hi[k]);
       ++*launches;
     }
@@ -219,6 +234,8 @@ struct pg_group : public pgb::Exchange {
   }
 
   void release() {
+    for (pg_grid *g : slabs)
+      if (g) g->hx = SlabHalo{};
     for (auto *v : {&send_lo, &send_hi, &recv_lo, &recv_hi})
       for (double *p : *v)
         if (p) cudaFree(p);
@@ -238,6 +255,28 @@ int check_slab(const pg_grid *g, int G, bool lo, bool hi) {
   REQ(!hi || g->y_end + G <= g->md.NY, "a slab with an upper neighbour needs G ghost rows above its owned rows");
   REQ(lo || g->y_begin == 0, "the first slab owns its lowest row (no ghost rows below the grid)");
   REQ(hi || g->y_end == g->md.NY, "the last slab owns its highest row");
+  return PG_OK;
+}
+
+int alloc_bufs(pg_group *grp);
+
+// hand the exchange buffers to the slab grids' sweeps
+int attach_halo(pg_group *grp) {
+  for (size_t k = 0; k < grp->slabs.size(); ++k) {
+    pg_grid *g = grp->slabs[k];
+    SlabHalo &h = g->hx;
+    h.G = grp->G;
+    h.has_lo = grp->has_lo((int)k);
+    h.has_hi = grp->has_hi((int)k);
+    h.send_lo = grp->send_lo[k];
+    h.send_hi = grp->send_hi[k];
+    h.recv_lo = grp->recv_lo[k];
+    h.recv_hi = grp->recv_hi[k];
+    if (!encode_halo_maps(g)) {
+      set_error("encoding the ghost-row tensor maps failed");
+      return PG_ECUDA;
+    }
+  }
   return PG_OK;
 }
 
@@ -316,7 +355,7 @@ PG_API int pg_group_nccl(pg_grid *slab, const void *id128, int32_t nranks, int32
   grp->rank = rank;
   grp->nranks = nranks;
   grp->G = ghost;
-  if ((rc = alloc_bufs(grp))) {
+  if ((rc = alloc_bufs(grp)) || (rc = attach_halo(grp))) {
     grp->release();
     delete grp;
     return rc;
@@ -348,7 +387,7 @@ PG_API int pg_group_local(int32_t n, pg_grid *const *slabs, int32_t ghost, pg_gr
   grp->slabs.assign(slabs, slabs + n);
   grp->nranks = n;
   grp->G = ghost;
-  if ((rc = alloc_bufs(grp))) {
+  if ((rc = alloc_bufs(grp)) || (rc = attach_halo(grp))) {
     grp->release();
     delete grp;
     return rc;

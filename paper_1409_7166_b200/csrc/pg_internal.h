@@ -57,6 +57,16 @@ __host__ __device__ inline int64_t mesh_col(const MeshDims &d, int64_t i) {
   return o >= d.HP ? 2 * (o - d.HP) + 1 : 2 * o;
 }
 
+// Ghost-row exchange buffers of a slab grid (set by its pg_group): the sweep
+// writes the G owned rows next to each boundary to send_*, and reads the ghost
+// rows from recv_* ([L][G][NXP] parity-split rows; maps per strip width).
+struct SlabHalo {
+  int G = 0;
+  bool has_lo = false, has_hi = false;
+  double *send_lo = nullptr, *send_hi = nullptr, *recv_lo = nullptr, *recv_hi = nullptr;
+  CUtensorMap mlo[2], mhi[2];  // [W = 32 / 64] maps of recv_lo / recv_hi
+};
+
 }  // namespace pgb
 
 struct pg_grid {
@@ -111,6 +121,7 @@ struct pg_grid {
   // owned, the others are ghost rows refreshed by the group exchange
   bool slab = false;
   int32_t y_begin = 0, y_end = 0, ypar = 0;
+  pgb::SlabHalo hx;
 
   // ---- options
   int fuse = 0;                        // F: sweeps per launch of the temporally blocked mesh sweep (0: auto)
@@ -151,9 +162,10 @@ cudaError_t launch_scatter_user(pg_grid *g, const double *src_user_order, double
 int sweeps_per_launch(pg_grid *g, int method);
 // temporally blocked red-black sweep (pg_sweep_fused.cu)
 bool tma_available(pg_grid *g);
+bool encode_halo_maps(pg_grid *g);
 int fused_exact_lanes(int F, int W);
 int fused_default_stages(int L, int F, int D);
-bool fused_variant_exists(int L, int F, int S, int D, int W);
+bool fused_variant_exists(int L, int F, int S, int D, int W, bool slab = false);
 int fused_ctas_per_sm(int L, int S, int W);
 cudaError_t launch_rb_sweep_fused(pg_grid *g, double omega, double tol, int j, int nsw, int F,
                                   int S, int D, int W, int rows_per_cta, int y_begin, int y_end,
@@ -163,6 +175,10 @@ cudaError_t launch_rb_sweep_fused(pg_grid *g, double omega, double tol, int j, i
 // (may be null) runs after every sweep launch of all grids.
 struct Exchange {
   virtual ~Exchange() = default;
+  // before the first step (initial state in V[0]) and after each step's last
+  // sweep launch (before step_end)
+  virtual cudaError_t begin() { return cudaSuccess; }
+  virtual cudaError_t end_step(int64_t *launches) { return cudaSuccess; }
   // launch_idx: index of the launch in the time step; rel: index in its batch
   virtual cudaError_t after_sweep(int launch_idx, int rel, int64_t *launches) = 0;
 };

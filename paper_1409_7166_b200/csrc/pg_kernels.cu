@@ -450,6 +450,7 @@ static FusedCfg fused_cfg(const pg_grid *g) { return fused_cfg_for(g, g->fuse > 
 
 static FusedCfg fused_cfg_for(const pg_grid *g, int fuse) {
   const int L = g->md.L;
+  const bool sl = g->slab && g->hx.G > 0;  // slab of a group: exchange-aware variants
   for (int F = fuse; F >= 1; --F) {
     // auto width: 64 column pairs per strip (half the x-halo share) for fused
     // launches where that variant fits in shared memory, else 32 (measured,
@@ -458,11 +459,11 @@ static FusedCfg fused_cfg_for(const pg_grid *g, int fuse) {
     const int widths[2] = {first, 32};
     for (int W : widths) {
       const int D = g->lag;
-      if (g->stages > 0 && fused_variant_exists(L, F, g->stages, D, W)) return {F, g->stages, D, W};
+      if (g->stages > 0 && fused_variant_exists(L, F, g->stages, D, W, sl)) return {F, g->stages, D, W};
       const int S = fused_default_stages(L, F, D);
-      if (fused_variant_exists(L, F, S, D, W)) return {F, S, D, W};
+      if (fused_variant_exists(L, F, S, D, W, sl)) return {F, S, D, W};
       const int S3 = fused_default_stages(L, F, 3);
-      if (fused_variant_exists(L, F, S3, 3, W)) return {F, S3, 3, W};
+      if (fused_variant_exists(L, F, S3, 3, W, sl)) return {F, S3, 3, W};
     }
   }
   return {1, 6, 3, 32};

@@ -47,7 +47,31 @@ bool encode(CUtensorMap *m, const double *base, const MeshDims &d, int W) {
 }
 
 
+// 4-D view of a slab's ghost-row receive buffer: [L][G][NXP] parity-split rows
+bool encode_rows(CUtensorMap *m, const double *base, const MeshDims &d, int G, int W) {
+  auto fn = get_encoder();
+  if (!fn) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)d.HP, 2, (cuuint64_t)G, (cuuint64_t)d.L};
+  cuuint64_t strides[3] = {(cuuint64_t)d.HP * 8, (cuuint64_t)d.NXP * 8, (cuuint64_t)G * d.NXP * 8};
+  cuuint32_t box[4] = {(cuuint32_t)W, 2, 1, (cuuint32_t)d.L};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double *>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 }  // namespace
+
+bool encode_halo_maps(pg_grid *g) {
+  SlabHalo &h = g->hx;
+  bool ok = true;
+  for (int w = 0; w < 2; ++w) {
+    if (h.has_lo) ok = ok && encode_rows(&h.mlo[w], h.recv_lo, g->md, h.G, w ? 64 : 32);
+    if (h.has_hi) ok = ok && encode_rows(&h.mhi[w], h.recv_hi, g->md, h.G, w ? 64 : 32);
+  }
+  return ok;
+}
 
 // cycle counters of the instrumented build (-DPG_PROF), else null
 unsigned long long *prof_buffer() {
@@ -84,7 +108,17 @@ int fused_default_stages(int L, int F, int D) {
   return D * (F - 1) + 6;
 }
 
-bool fused_variant_exists(int L, int F, int S, int D, int W) {
+bool fused_variant_exists(int L, int F, int S, int D, int W, bool slab) {
+  if (slab) {
+    switch (fused_key(L, F, S, D, W, true)) {
+#define X(l, f, s, d, w) case fused_key(l, f, s, d, w, true):
+      PG_FUSED_SLAB_CASES(X)
+#undef X
+      return true;
+      default:
+        return false;
+    }
+  }
   switch (fused_key(L, F, S, D, W)) {
 #define X(l, f, s, d, w) case fused_key(l, f, s, d, w):
     PG_FUSED_CASES(X)
@@ -131,9 +165,18 @@ cudaError_t launch_rb_sweep_fused(pg_grid *g, double omega, double tol, int j, i
   P.launch_idx = j;
   P.nsw = nsw;
   P.prof = prof_buffer();
+  const SlabHalo &h = g->hx;
+  const bool halo = g->slab && h.G > 0;
+  P.has_rlo = halo && h.has_lo;
+  P.has_rhi = halo && h.has_hi;
+  P.G = h.G;
+  P.send_lo = halo && h.has_lo ? h.send_lo : nullptr;
+  P.send_hi = halo && h.has_hi ? h.send_hi : nullptr;
+  if (P.has_rlo) P.mRlo = h.mlo[W == 64 ? 1 : 0];
+  if (P.has_rhi) P.mRhi = h.mhi[W == 64 ? 1 : 0];
   const int strips = (g->md.HP + fused_exact_lanes(F, W) - 1) / fused_exact_lanes(F, W);
   const dim3 grid(strips, (y_end - y_begin + rows_per_cta - 1) / rows_per_cta);
-  const int key = fused_key(g->md.L, F, S, D, W);
+  const int key = fused_key(g->md.L, F, S, D, W, halo);
   bool found = false;
   cudaError_t e = launch_fused_inst_1(key, g, P, grid, &found);
   if (!found) e = launch_fused_inst_2(key, g, P, grid, &found);

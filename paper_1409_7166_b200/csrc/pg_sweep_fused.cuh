@@ -132,6 +132,13 @@ struct FusedParams {
   int32_t launch_idx;
   int32_t nsw;              // sweeps in this launch, 1..F
   unsigned long long *prof; // PG_PROF builds: 8 cycle counters (else unused)
+  // slab of a partitioned mesh (pg_group): the G ghost rows below y_begin /
+  // from y_end are read from the receive buffers the exchange filled (maps
+  // mRlo / mRhi, rows [0, G) each), and the G owned rows next to each boundary
+  // are also written to the send buffers ([L][G][NXP] rows, parity-split)
+  CUtensorMap mRlo, mRhi;
+  double *send_lo, *send_hi;
+  int32_t has_rlo, has_rhi, G;
 };
 
 // The constants of one node update: x links (west, east), y links (north,
@@ -172,7 +179,7 @@ __device__ __forceinline__ double upd_c(const NodeC &c, double w, double Vc, dou
   return fma(w, (s1 + s2) * c.id - Vc, Vc);
 }
 
-template <int L, int F, int S, int D, int W>
+template <int L, int F, int S, int D, int W, bool SLAB>
 __global__ void __launch_bounds__(W * L) k_rb_sweep_fused(const __grid_constant__ FusedParams P) {
   static_assert(D >= 3, "levels must trail by >= 3 rows");
   static_assert(S >= D * (F - 1) + 5, "ring too small for the wavefront");
@@ -239,10 +246,27 @@ __global__ void __launch_bounds__(W * L) k_rb_sweep_fused(const __grid_constant_
   __syncthreads();
 
   // ring slot of row r is (r - r_first) mod S
+  // V of row r: ghost rows of a slab come from the exchange's receive buffers
+  auto v_src = [&](int r, int &rr) -> const CUtensorMap * {
+    if constexpr (SLAB) {
+      if (P.has_rlo && r < P.y_begin) {
+        rr = r - (P.y_begin - P.G);
+        return &P.mRlo;
+      }
+      if (P.has_rhi && r >= P.y_end) {
+        rr = r - P.y_end;
+        return &P.mRhi;
+      }
+    }
+    rr = r;
+    return mVin;
+  };
   auto issue_slot = [&](int r, int s) {
     double *st = ring + s * SE;
     mbar_expect_tx(&full_bar[s], STAGE_BYTES);
-    tma4(st, mVin, &full_bar[s], ps, r);
+    int rv;
+    const CUtensorMap *mv = v_src(r, rv);
+    tma4(st, mv, &full_bar[s], ps, rv);
     tma4(st + GX, &P.mgx, &full_bar[s], ps, r);
     tma4(st + GY, &P.mgy, &full_bar[s], ps, r);
     tma4(st + GZ, &P.mgz, &full_bar[s], ps, r);
@@ -252,7 +276,9 @@ __global__ void __launch_bounds__(W * L) k_rb_sweep_fused(const __grid_constant_
   // rows R + kL2Ahead are prefetched into L2 when row R is loaded into the ring
   constexpr int kL2Ahead = PG_L2_AHEAD;
   auto prefetch_row = [&](int r) {
-    tma4_prefetch(mVin, ps, r);
+    int rv;
+    const CUtensorMap *mv = v_src(r, rv);
+    tma4_prefetch(mv, ps, rv);
     tma4_prefetch(&P.mgx, ps, r);
     tma4_prefetch(&P.mgy, ps, r);
     tma4_prefetch(&P.mgz, ps, r);
@@ -439,6 +465,19 @@ __global__ void __launch_bounds__(W * L) k_rb_sweep_fused(const __grid_constant_
         }
         vout_e[(int64_t)ro * P.NXP] = ve;
         vout_o[(int64_t)ro * P.NXP] = vo;
+        // slab boundary rows also go to the exchange's send buffers
+        if constexpr (SLAB) {
+          if (P.send_lo && ro < P.y_begin + P.G) {
+            double *sb = P.send_lo + ((int64_t)l * P.G + (ro - P.y_begin)) * P.NXP;
+            sb[gp] = ve;
+            sb[gp + P.HP] = vo;
+          }
+          if (P.send_hi && ro >= P.y_end - P.G) {
+            double *sb = P.send_hi + ((int64_t)l * P.G + (ro - (P.y_end - P.G))) * P.NXP;
+            sb[gp] = ve;
+            sb[gp + P.HP] = vo;
+          }
+        }
       }
       PROF_T(t5);
       PROF_T(t6);
@@ -489,9 +528,9 @@ __global__ void __launch_bounds__(W * L) k_rb_sweep_fused(const __grid_constant_
 
 constexpr size_t fused_smem(int L, int S, int W) { return ((size_t)S * 6 * L * 2 * W + 2 * 2 * W) * 8; }
 
-template <int L, int F, int S, int D, int W>
+template <int L, int F, int S, int D, int W, bool SLAB>
 cudaError_t launch_fused_t(pg_grid *g, const FusedParams &P, dim3 grid) {
-  auto kern = k_rb_sweep_fused<L, F, S, D, W>;
+  auto kern = k_rb_sweep_fused<L, F, S, D, W, SLAB>;
   const size_t smem = fused_smem(L, S, W);
   if (g->tma_kernel_set != (const void *)kern || g->tma_smem_set != smem) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -524,8 +563,16 @@ cudaError_t launch_fused_t(pg_grid *g, const FusedParams &P, dim3 grid) {
   X(2, 1, 6, 3, 64) X(2, 2, 9, 3, 64) X(2, 3, 12, 3, 64)                                    \
   X(3, 1, 6, 3, 64) X(3, 2, 9, 3, 64) X(4, 1, 6, 3, 64) X(4, 2, 9, 3, 64)
 
-constexpr int fused_key(int L, int F, int S, int D, int W) {
-  return (((L * 8 + F) * 32 + S) * 8 + D) * 2 + (W == 64);
+// Variants compiled with slab (ghost-row exchange) support: the defaults
+// F = 2 (W = 64 where it fits, else 32) and F = 1 for every L.
+#define PG_FUSED_SLAB_CASES(X)                                                                   \
+  X(1, 2, 9, 3, 64) X(2, 2, 9, 3, 64) X(3, 2, 9, 3, 64) X(4, 2, 9, 3, 64)                          \
+  X(5, 2, 9, 3, 32) X(6, 2, 9, 3, 32) X(7, 2, 9, 3, 32) X(8, 2, 9, 3, 32)                          \
+  X(1, 1, 6, 3, 32) X(2, 1, 6, 3, 32) X(3, 1, 6, 3, 32) X(4, 1, 6, 3, 32)                          \
+  X(5, 1, 6, 3, 32) X(6, 1, 6, 3, 32) X(7, 1, 6, 3, 32) X(8, 1, 6, 3, 32)
+
+constexpr int fused_key(int L, int F, int S, int D, int W, bool slab = false) {
+  return ((((L * 8 + F) * 32 + S) * 8 + D) * 2 + (W == 64)) * 2 + (slab ? 1 : 0);
 }
 
 

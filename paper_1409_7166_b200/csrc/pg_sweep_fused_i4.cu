@@ -7,9 +7,15 @@ cudaError_t launch_fused_inst_4(int key, pg_grid *g, const FusedParams &P, dim3 
   *found = true;
 #define X(l, f, s, d, w)                                                         \
   if constexpr (l == 4) {                                                        \
-    if (key == fused_key(l, f, s, d, w)) return launch_fused_t<l, f, s, d, w>(g, P, grid); \
+    if (key == fused_key(l, f, s, d, w)) return launch_fused_t<l, f, s, d, w, false>(g, P, grid); \
   }
   PG_FUSED_CASES(X)
+#undef X
+#define X(l, f, s, d, w)                                                         \
+  if constexpr (l == 4) {                                                        \
+    if (key == fused_key(l, f, s, d, w, true)) return launch_fused_t<l, f, s, d, w, true>(g, P, grid); \
+  }
+  PG_FUSED_SLAB_CASES(X)
 #undef X
   *found = false;
   return cudaErrorInvalidValue;

@@ -86,8 +86,8 @@ def test_rlc_slabs(pgb):
 def test_slab_errors(pgb):
     P = pgb
     g = gridgen.mesh_grid(2, 40, 30, seed=1, pad_pitch=5)
-    grp = P.SlabGroup.local(g, 2, fuse=2)
-    grp.grids[0].set_option("fuse", 3)           # 2F = 6 > ghost 4
+    grp = P.SlabGroup.local(g, 2, fuse=1)        # ghost rows G = 2
+    grp.grids[0].set_option("fuse", 2)           # 2F = 4 > G
     with pytest.raises(P.PgError):
         grp.transient(g.h, 2, tol=0.0, omega=1.5, max_sweeps=3)
     with pytest.raises(P.PgError):               # slab grids are driven by their group
