@@ -446,7 +446,10 @@ def run_b200(args):
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
-    G.close()
+    if grp is not None:
+        grp.close()   # the group owns its slab grids (releases the exchange first)
+    else:
+        G.close()
     if world > 1:
         dist.destroy_process_group()
 
