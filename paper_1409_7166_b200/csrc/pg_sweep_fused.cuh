@@ -144,19 +144,24 @@ struct FusedParams {
 // The constants of one node update: x links (west, east), y links (north,
 // south), vias (up, down), b and 1/d.
 struct NodeC {
-  double gxW, gxE, gyN, gyS, gzU, gzD, b, id;
+  double gxOwn, gxOth, gyN, gyS, gzU, gzD, b, id;
 };
 
-// Loads a node's constants from its staged row Ry (row r-1 in Rn); the south
-// link is taken from `gyS` when the caller already holds it (gyS_known).
+// Loads a node's constants from its staged row Ry (row r-1 in Rn).  The x
+// links are taken by neighbour rather than by direction: the link to the
+// other node of my own pair is always the even node's gx (offset pe), the link
+// to the neighbouring lane's node is gx at `oth_link` (the odd node's for an
+// odd node, the previous pair's odd node's for an even node), so the update
+// needs no parity-dependent value selects.  The south link is taken from `gyS`
+// when the caller already holds it (gyS_known).
 template <int L, int RW, bool gyS_known = false>
-__device__ __forceinline__ NodeC load_c(const double *Ry, const double *Rn, int me, int ow, bool has_down,
-                                        double gyS = 0.0) {
+__device__ __forceinline__ NodeC load_c(const double *Ry, const double *Rn, int me, int pe, int oth_link,
+                                        bool has_down, double gyS = 0.0) {
   constexpr int LAY = L * RW;
   constexpr int GX = 1 * LAY, GY = 2 * LAY, GZ = 3 * LAY, BB = 4 * LAY, ID = 5 * LAY;
   NodeC c;
-  c.gxW = Ry[GX + ow];
-  c.gxE = Ry[GX + me];
+  c.gxOwn = Ry[GX + pe];
+  c.gxOth = Ry[GX + oth_link];
   c.gyN = Rn[GY + me];
   c.gyS = gyS_known ? gyS : Ry[GY + me];
   c.gzU = Ry[GZ + me];
@@ -166,12 +171,13 @@ __device__ __forceinline__ NodeC load_c(const double *Ry, const double *Rn, int 
   return c;
 }
 
-// Eq. (13) + (15) from the constants and the neighbour values (VU / VD: via
-// neighbours in layers l+1 / l-1; gzD = 0 in layer 0 cancels VD).
-__device__ __forceinline__ double upd_c(const NodeC &c, double w, double Vc, double VW, double VE,
+// Eq. (13) + (15) from the constants and the neighbour values: Vown / Voth the
+// x neighbours in my lane / the neighbouring lane, VN / VS rows r-1 / r+1,
+// VU / VD via neighbours in layers l+1 / l-1 (gzD = 0 in layer 0 cancels VD).
+__device__ __forceinline__ double upd_c(const NodeC &c, double w, double Vc, double Vown, double Voth,
                                         double VN, double VS, double VU, double VD) {
-  double s1 = fma(c.gxW, VW, c.b);
-  s1 = fma(c.gxE, VE, s1);
+  double s1 = fma(c.gxOwn, Vown, c.b);
+  s1 = fma(c.gxOth, Voth, s1);
   s1 = fma(c.gyN, VN, s1);
   double s2 = c.gyS * VS;
   s2 = fma(c.gzU, VU, s2);
@@ -360,10 +366,10 @@ __global__ void __launch_bounds__(W * L) k_rb_sweep_fused(const __grid_constant_
           // for the same node D steps ago
           NodeC c;
           if (kReuseC && f == 1 && steady) c = cRedF[md3(u - D)];  // (== md3(u): read before the push)
-          else c = load_c<L, RW>(Ry, Rn, me, e ? own : oth, has_down);
+          else c = load_c<L, RW>(Ry, Rn, me, pe, e ? po : po - 1, has_down);
           if (kReuseC && f == 0) c0 = c;
           ad[f] = const_cast<double *>(Ry) + me;
-          vA[f] = upd_c(c, w, Vc, e ? Vown : Voth, e ? Voth : Vown, VN, VS, Ry[me + RW], Ry[me - RW]);
+          vA[f] = upd_c(c, w, Vc, Vown, Voth, VN, VS, Ry[me + RW], Ry[me - RW]);
           cA[f] = Vc;
           nA[f] = VN;
           gA[f] = c.gyN;
@@ -419,10 +425,10 @@ __global__ void __launch_bounds__(W * L) k_rb_sweep_fused(const __grid_constant_
           const double Voth = Ry[oth];
           NodeC c;
           if (kReuseC && f == 1 && steady) c = cBlkF[md3(u - D)];
-          else c = load_c<L, RW, true>(Ry, Rn, me, e ? own : oth, has_down, gA[f]);
+          else c = load_c<L, RW, true>(Ry, Rn, me, pe, e ? po : po - 1, has_down, gA[f]);
           if (kReuseC && f == 0) c0 = c;
           ad[f] = const_cast<double *>(Ry) + me;
-          vB[f] = upd_c(c, w, Vc, e ? Vown : Voth, e ? Voth : Vown, VN, vA[f], Ry[me + RW], Ry[me - RW]);
+          vB[f] = upd_c(c, w, Vc, Vown, Voth, VN, vA[f], Ry[me + RW], Ry[me - RW]);
           cB[f] = Vc;
         }
 #pragma unroll
