@@ -120,6 +120,13 @@ PG_API int pg_set_stream(pg_grid *g, void *stream);
  *            1..4, or 0 (default: 2); Jacobi and CSR sweeps run 1 per launch
  *   "lag"    wavefront lag D (rows) between fused sweep levels: 3 (default) or 4
  *   "batch"  sweep launches enqueued between host convergence polls, >= 1
+ *   "resident" 1 (default): red-black SOR on a single mesh that fits one
+ *            thread-block cluster (<= 16 CTAs x 512 threads, one thread per
+ *            (layer, row, column pair): L * ceil(NX/2) <= 512 and
+ *            ceil(NY / floor(512 / (L * ceil(NX/2)))) <= 16, e.g. 2 x 64 x 64)
+ *            runs all sweeps of a time step in one cluster launch with V in
+ *            shared memory (convergence tested after every sweep, so
+ *            pg_stats.sweeps_per_launch = 1); 0: the streaming sweep
  *   "graph"  1 (default): replay full batches of sweep launches from a captured
  *            CUDA graph (single grids, option "timing" off); 0: plain launches
  *   "rows"   rows per CTA of the mesh sweep (0: auto)

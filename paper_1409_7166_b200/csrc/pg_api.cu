@@ -325,6 +325,8 @@ PG_API int pg_set_option(pg_grid *g, const char *key, int64_t value) {
   } else if (k == "batch") {
     REQUIRE(value >= 1 && value <= 1024, "batch must be in 1..1024");
     g->batch = (int)value;
+  } else if (k == "resident") {
+    g->resident = value != 0;
   } else if (k == "graph") {
     g->use_graph = value != 0;
   } else if (k == "timing") {
@@ -649,6 +651,7 @@ int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, d
 
   int64_t launches = 0;
   const bool graph_ok = g->use_graph && ng == 1 && ex == nullptr && !g->timing;
+  const bool resident = ng == 1 && ex == nullptr && resident_ok(g, method);
   const int F = sweeps_per_launch(g, method);
   for (int k = 1; k < ng; ++k)
     REQUIRE(sweeps_per_launch(gs[k], method) == F, "grids of a group must use the same fuse option");
@@ -685,6 +688,29 @@ int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, d
     for (int k = 0; k < ng; ++k) {
       CK(launch_rhs(gs[k], h, dc ? t_dc : (double)s * h));
       launches += 1 + (gs[k]->npad > 0) + (gs[k]->nsrc > 0);
+    }
+    if (resident) {
+      // the whole sweep loop of the step in one launch (small meshes)
+      if (g->timing) CK(cudaEventRecord(tev(0), st));
+      CK(launch_rb_resident(g, omega, tol, max_sweeps, s));
+      ++launches;
+      if (g->timing) {
+        CK(cudaEventRecord(tev(1), st));
+        CK(cudaEventSynchronize(tev(1)));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, tev(0), tev(1)));
+        sweep_ms += ms;
+        ++sweep_launches;
+      }
+      if (g->rlc) {
+        CK(launch_inductor_update(g, h));
+        launches += 2;
+      }
+      if (n_probe > 0) {
+        CK(launch_probe(g, d_pidx, n_probe, d_pout + s * n_probe));
+        ++launches;
+      }
+      continue;
     }
     int64_t j = 0;
     int pending = -1;  // poll slot of the previous batch

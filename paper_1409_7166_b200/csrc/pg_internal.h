@@ -137,6 +137,7 @@ struct pg_grid {
   CUtensorMap tmap[2][7];              // [W = 32 / 64] V0, V1, gx, gy, gze, b, invd (encoded once)
   std::vector<cudaEvent_t> tev;        // timing event pool
   int use_graph = 1;                   // option "graph": replay captured sweep batches
+  int resident = 1;                    // option "resident": one-CTA sweep loop for tiny meshes
   cudaGraphExec_t batch_exec = nullptr;  // captured batch of `batch` full sweep launches
   cudaStream_t cap_stream = nullptr;     // private stream the batch graph is captured on
   double graph_key[6] = {0, 0, 0, 0, 0, 0};  // omega, tol, method, F, batch, stream of the capture
@@ -152,6 +153,8 @@ cudaError_t launch_rhs(pg_grid *g, double h, double t);
 cudaError_t launch_sweep(pg_grid *g, int method, double omega, double tol, int launch_idx,
                          int nsweeps, int64_t *launches);
 cudaError_t launch_batch_advance(pg_grid *g, int nb);
+bool resident_ok(const pg_grid *g, int method);
+cudaError_t launch_rb_resident(pg_grid *g, double omega, double tol, int64_t max_sweeps, int64_t s);
 cudaError_t launch_step_end(pg_grid *g, int64_t s, int launched, int flips, int fused,
                             int64_t max_sweeps, double tol);
 cudaError_t launch_inductor_update(pg_grid *g, double h);

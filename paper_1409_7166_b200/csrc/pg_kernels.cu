@@ -14,8 +14,11 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cooperative_groups.h>
 
 #include "pg_internal.h"
+
+namespace cg = cooperative_groups;
 
 namespace pgb {
 
@@ -365,6 +368,237 @@ __global__ void k_step_end(DevCtl *c, int64_t s, int32_t launched, int32_t flips
 
 __global__ void k_batch_advance(DevCtl *c, int32_t nb) { c->jbase += nb; }
 
+// ------------------------------------------------- resident sweep (small grids)
+// All sweeps of one time step in ONE launch of one thread-block cluster: the
+// mesh is cut into y-slabs of R rows (all layers), one per CTA of the cluster
+// (<= 16 CTAs); each CTA keeps its slab of V in shared memory and each thread
+// owns one red and one black node of a (layer, row, column pair), their
+// conductances, b and 1/d in registers.  A red-black SOR sweep (Eq. (13) +
+// (15), same numbering and arithmetic order as the streaming sweep) is: red
+// updates, cluster barrier, black updates, cluster barrier; the rows just
+// across a slab boundary are read from the neighbouring CTA's shared memory
+// (distributed shared memory).  max|dV| is reduced per CTA with a shared
+// atomic and read by every thread from all CTAs after the barrier, so the
+// whole cluster stops after the same sweep (convergence tested after every
+// sweep, R13).  For grids whose state fits a few SMs this replaces a launch
+// (and its latency) per sweep by two cluster barriers.  V is updated in
+// place (no ping-pong flip); the step's bookkeeping is done here.
+struct ClusterArgs {
+  MeshDims d;
+  const double *gx, *gy, *gz, *b, *invd;
+  double *V0, *V1;
+  double omega, tol;
+  int64_t max_sweeps, s;
+  int64_t *rec;
+  DevCtl *ctl;
+  int32_t R;    // rows per CTA (the last CTA may hold fewer)
+  int32_t HPx;  // column pairs per row, ceil(NX / 2)
+};
+
+// one node of a thread: its coefficients and where its neighbours live
+struct CNode {
+  double gE, gW, gN, gS, gU, gD, b, id;
+  const double *pN, *pS;   // generic addresses (own or neighbouring CTA)
+  int li, iE, iW, iU, iD;  // shared-memory indices (self where absent, g = 0)
+  bool on;
+};
+
+__device__ __forceinline__ void cnode_init(CNode &n, const ClusterArgs &a, cg::cluster_group &cl,
+                                           double *sv, int rank, int Rt, int l, int yy, int x) {
+  const MeshDims &d = a.d;
+  const int R = a.R, NX = d.NX;
+  const int y = rank * R + yy;
+  n.on = x < NX;
+  if (!n.on) x = NX - 1;  // keep addresses valid; the node is never updated
+  const int64_t i = mesh_index(d, l, y, x);
+  const int li = (l * R + yy) * NX + x;
+  n.li = li;
+  const bool hE = x + 1 < NX, hW = x > 0, hN = y > 0, hS = y + 1 < d.NY;
+  const bool hU = l > 0, hD = l + 1 < d.L;
+  n.gE = hE ? a.gx[i] : 0.0;
+  n.gW = hW ? a.gx[mesh_index(d, l, y, x - 1)] : 0.0;
+  n.gN = hN ? a.gy[i - d.NXP] : 0.0;
+  n.gS = hS ? a.gy[i] : 0.0;
+  n.gU = hU ? a.gz[i - d.layer_stride] : 0.0;
+  n.gD = hD ? a.gz[i] : 0.0;
+  n.b = a.b[i];
+  n.id = a.invd[i];
+  n.iE = hE ? li + 1 : li;
+  n.iW = hW ? li - 1 : li;
+  n.iU = hU ? li - R * NX : li;
+  n.iD = hD ? li + R * NX : li;
+  n.pN = sv + li;
+  n.pS = sv + li;
+  if (hN) n.pN = yy > 0 ? sv + li - NX : cl.map_shared_rank(sv + (l * R + R - 1) * NX + x, rank - 1);
+  if (hS) n.pS = yy + 1 < Rt ? sv + li + NX : cl.map_shared_rank(sv + (l * R) * NX + x, rank + 1);
+}
+
+// Eq. (13) + (15) for one node, the streaming sweep's order of operations
+// (absent neighbours carry g = 0 and read the node itself: fma(0, v, s) == s)
+__device__ __forceinline__ double cnode_update(const CNode &n, const double *sv, double w, double vc) {
+  double s1 = fma(n.gE, sv[n.iE], n.b);
+  s1 = fma(n.gW, sv[n.iW], s1);
+  double s2 = n.gN * *n.pN;
+  s2 = fma(n.gS, *n.pS, s2);
+  s2 = fma(n.gU, sv[n.iU], s2);
+  s2 = fma(n.gD, sv[n.iD], s2);
+  return fma(w, (s1 + s2) * n.id - vc, vc);
+}
+
+__global__ void __launch_bounds__(512) k_rb_cluster(ClusterArgs a) {
+  extern __shared__ double sv[];
+  __shared__ unsigned long long slot[2];
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int ncta = (int)cl.num_blocks();
+  const MeshDims d = a.d;
+  const int R = a.R, NX = d.NX, L = d.L;
+  const int y0 = rank * R;
+  const int Rt = min(R, d.NY - y0);
+  double *V = a.ctl->base ? a.V1 : a.V0;
+  for (int k = threadIdx.x; k < L * Rt * NX; k += blockDim.x) {
+    const int x = k % NX, r = k / NX;
+    const int yy = r % Rt, l = r / Rt;
+    sv[(l * R + yy) * NX + x] = V[mesh_index(d, l, y0 + yy, x)];
+  }
+  if (threadIdx.x < 2) slot[threadIdx.x] = 0ull;
+  CNode nr, nb;
+  nr.on = nb.on = false;
+  const int t = threadIdx.x;
+  if (t < L * Rt * a.HPx) {
+    const int p = t % a.HPx, r = t / a.HPx;
+    const int yy = r % Rt, l = r / Rt;
+    const int e = (l + y0 + yy) & 1;  // red: (l + y + x) even
+    cnode_init(nr, a, cl, sv, rank, Rt, l, yy, 2 * p + e);
+    cnode_init(nb, a, cl, sv, rank, Rt, l, yy, 2 * p + 1 - e);
+  }
+  cl.sync();  // every slab and slot in place
+  double vr = nr.on ? sv[nr.li] : 0.0, vb = nb.on ? sv[nb.li] : 0.0;
+  const double w = a.omega;
+  const int lane = threadIdx.x & 31;
+  // max|dV| of sweep kk (its CTA maxima are final after sweep kk's last barrier)
+  auto sweep_max = [&](int64_t kk) {
+    double m = 0.0;
+    if (lane < ncta)
+      m = __longlong_as_double((long long)*cl.map_shared_rank(&slot[kk & 1], lane));
+    return warp_max(m);
+  };
+  // The stop test of sweep k is taken one half-sweep late: sweep k + 1's red
+  // half runs first and is undone (each thread restores its own red node) if
+  // sweep k converged, so the convergence read overlaps useful work.
+  int64_t k = 0;
+  double last = 0.0;
+  bool conv = false;
+  while (k < a.max_sweeps) {
+    double vrn = vr, vbn = vb;
+    if (nr.on) {
+      vrn = cnode_update(nr, sv, w, vr);
+      sv[nr.li] = vrn;
+    }
+    // slot (k + 1) & 1 was last read during sweep k (before its last barrier)
+    if (threadIdx.x == 0) slot[(k + 1) & 1] = 0ull;
+    cl.sync();
+    double m = 0.0;
+    if (k > 0) m = sweep_max(k);
+    if (nb.on) vbn = cnode_update(nb, sv, w, vb);
+    if (k > 0) {
+      last = m;
+      if (a.tol > 0.0 && m < a.tol) {
+        if (nr.on) sv[nr.li] = vr;  // sweep k converged: undo sweep k + 1's red half
+        conv = true;
+        break;
+      }
+    }
+    if (nb.on) sv[nb.li] = vbn;
+    double dm = fmax(fabs(vrn - vr), fabs(vbn - vb));
+    vr = vrn;
+    vb = vbn;
+    ++k;
+    dm = warp_max(dm);
+    // |dV| >= 0: its bit pattern orders like the value
+    if (lane == 0 && dm > 0.0) atomicMax(&slot[k & 1], (unsigned long long)__double_as_longlong(dm));
+    cl.sync();
+  }
+  if (!conv && k > 0) last = sweep_max(k);
+  cl.sync();  // no CTA leaves while another may still read its shared memory
+  for (int q = threadIdx.x; q < L * Rt * NX; q += blockDim.x) {
+    const int x = q % NX, r = q / NX;
+    const int yy = r % Rt, l = r / Rt;
+    V[mesh_index(d, l, y0 + yy, x)] = sv[(l * R + yy) * NX + x];
+  }
+  if (rank == 0 && threadIdx.x == 0) {
+    DevCtl *c = a.ctl;
+    a.rec[a.s] = k;
+    c->sweeps_total += k;
+    if (k > c->sweeps_max) c->sweeps_max = k;
+    c->last_delta = last;
+    if (a.tol > 0.0 && !(last < a.tol) && c->failed == 0) c->failed = (int32_t)a.s;
+  }
+}
+
+// cluster shape of the resident sweep: R rows per CTA, ncta CTAs (<= 16),
+// T threads (<= 512, one per column pair of the slab); false if it does not fit
+struct ClusterPlan {
+  int R, ncta, T;
+};
+static bool cluster_plan(const MeshDims &d, ClusterPlan *p) {
+  const int per_row = d.L * ((d.NX + 1) / 2);
+  if (per_row > 512) return false;
+  const int rmax = std::min(512 / per_row, d.NY);
+  const int ncta = (d.NY + rmax - 1) / rmax;
+  if (ncta > 16) return false;
+  p->ncta = ncta;
+  p->R = (d.NY + ncta - 1) / ncta;  // even out the slabs
+  p->T = ((p->R * per_row + 31) / 32) * 32;
+  return true;
+}
+
+bool resident_ok(const pg_grid *g, int method) {
+  ClusterPlan p;
+  return g->kind == 0 && method == PG_METHOD_RBSOR && !g->slab && g->resident &&
+         cluster_plan(g->md, &p);
+}
+
+cudaError_t launch_rb_resident(pg_grid *g, double omega, double tol, int64_t max_sweeps, int64_t s) {
+  ClusterPlan p;
+  if (!cluster_plan(g->md, &p)) return cudaErrorInvalidConfiguration;
+  ClusterArgs a;
+  a.d = g->md;
+  a.gx = g->gx; a.gy = g->gy; a.gz = g->gze; a.b = g->b; a.invd = g->invd;
+  a.V0 = g->V[0];
+  a.V1 = g->V[1];
+  a.omega = omega;
+  a.tol = tol;
+  a.max_sweeps = max_sweeps;
+  a.s = s;
+  a.rec = g->dev_sweeps;
+  a.ctl = g->ctl;
+  a.R = p.R;
+  a.HPx = (g->md.NX + 1) / 2;
+  const size_t smem = sizeof(double) * (size_t)p.R * g->md.L * g->md.NX;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_rb_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k_rb_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.ncta);
+  cfg.blockDim = dim3(p.T);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = g->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = p.ncta;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_rb_cluster, a);
+}
+
 __global__ void k_probe(const double *V0, const double *V1, const DevCtl *c, const int64_t *idx,
                         int64_t n, double *out) {
   const double *V = c->base ? V1 : V0;
@@ -470,6 +704,7 @@ static FusedCfg fused_cfg_for(const pg_grid *g, int fuse) {
 }
 
 int sweeps_per_launch(pg_grid *g, int method) {
+  if (resident_ok(g, method)) return 1;  // convergence tested after every sweep
   return (g->kind == 0 && method == PG_METHOD_RBSOR) ? fused_cfg(g).F : 1;
 }
 

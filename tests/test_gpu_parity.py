@@ -65,15 +65,17 @@ def mk(L, NY, NX, seed, rlc=False):
                              src_start=20e-12, src_width=40e-12, rlc=rlc)
 
 
-@pytest.mark.parametrize("F", [1, 2])
+@pytest.mark.parametrize("F,resident", [(1, 0), (2, 0), (0, 1)])
 @pytest.mark.parametrize("shape", SHAPES)
 @pytest.mark.parametrize("omega", [1.0, 1.7])
-def test_rb_sweep_iterates_equal_oracle(pgb, shape, omega, F):
-    # the mesh sweep with F = 1 (one sweep per launch) and the default F = 2
+def test_rb_sweep_iterates_equal_oracle(pgb, shape, omega, F, resident):
+    # the streaming mesh sweep with F = 1 (one sweep per launch) and F = 2, and
+    # the one-CTA resident sweep loop that small meshes use by default
     g = mk(*shape, seed=sum(shape))
     steps, k = 6, 5
     ro, _ = oracle_run(g, steps, tol=0.0, omega=omega, max_sweeps=k)
-    rg, V = gpu_run(pgb, g, steps, tol=0.0, omega=omega, max_sweeps=k, options={"fuse": F})
+    rg, V = gpu_run(pgb, g, steps, tol=0.0, omega=omega, max_sweeps=k,
+                    options={"fuse": F, "resident": resident})
     assert np.all(rg.sweeps[1:] == k)
     np.testing.assert_allclose(rg.probes, ro.V[:, :g.n], rtol=0, atol=ATOL_ITER)
     np.testing.assert_allclose(V, ro.V[-1, :g.n], rtol=0, atol=ATOL_ITER)
@@ -93,7 +95,7 @@ def test_fused_sweep_iterates_equal_oracle(pgb, shape, F, lag, rows, width):
     steps, k, omega = 4, 5, 1.6
     ro, _ = oracle_run(g, steps, tol=0.0, omega=omega, max_sweeps=k)
     rg, V = gpu_run(pgb, g, steps, tol=0.0, omega=omega, max_sweeps=k,
-                    options={"fuse": F, "lag": lag, "rows": rows, "width": width})
+                    options={"fuse": F, "lag": lag, "rows": rows, "width": width, "resident": 0})
     assert np.all(rg.sweeps[1:] == k)
     np.testing.assert_allclose(rg.probes, ro.V[:, :g.n], rtol=0, atol=ATOL_ITER)
     np.testing.assert_allclose(V, ro.V[-1, :g.n], rtol=0, atol=ATOL_ITER)
@@ -105,7 +107,7 @@ def test_fused_converged_sweep_counts(pgb, F):
     # at the first multiple of F at or after the oracle's stopping sweep
     g = gridgen.config_grid(0, dims=(2, 40, 48), steps=15)
     ro, _ = oracle_run(g, 15, tol=1e-10, omega=1.9)
-    rg, _ = gpu_run(pgb, g, 15, tol=1e-10, omega=1.9, options={"fuse": F})
+    rg, _ = gpu_run(pgb, g, 15, tol=1e-10, omega=1.9, options={"fuse": F, "resident": 0})
     np.testing.assert_allclose(rg.probes, ro.V, rtol=0, atol=ATOL_CONV)
     expect = -(-ro.sweeps[1:] // F) * F
     assert np.mean(rg.sweeps[1:] == expect) > 0.9
@@ -143,24 +145,26 @@ def test_rlc_iterates_equal_oracle_series_element(pgb, shape, F):
     g = mk(*shape, seed=60 + sum(shape), rlc=True)
     steps, k = 8, 5
     ro, _ = oracle_run(g, steps, tol=0.0, omega=1.6, max_sweeps=k, series_rl="element")
-    rg, V = gpu_run(pgb, g, steps, tol=0.0, omega=1.6, max_sweeps=k, options={"fuse": F})
+    rg, V = gpu_run(pgb, g, steps, tol=0.0, omega=1.6, max_sweeps=k, options={"fuse": F, "resident": 0})
     assert np.abs(ro.V - 1.0).max() > 1e-6
     np.testing.assert_allclose(rg.probes, ro.V, rtol=0, atol=ATOL_ITER)
 
 
-def test_config0_full_size_converged(pgb):
+@pytest.mark.parametrize("resident", [1, 0])
+def test_config0_full_size_converged(pgb, resident):
     # BASELINE config 0 at full size: 2 x 64 x 64, h = 10 ps, 100 steps, tol 1e-10
+    # (resident one-CTA sweep loop by default; the streaming sweep with F = 2)
     g = gridgen.config_grid(0)
     steps, omega = g.steps, 1.9
     ro, _ = oracle_run(g, steps, tol=1e-10, omega=omega)
-    rg, _ = gpu_run(pgb, g, steps, tol=1e-10, omega=omega)
+    rg, _ = gpu_run(pgb, g, steps, tol=1e-10, omega=omega, options={"resident": resident})
     assert ro.status == 0 and rg.status == 0
     np.testing.assert_allclose(rg.probes, ro.V, rtol=0, atol=ATOL_CONV)
     # same numbering, same arithmetic up to rounding -> same sweep counts almost
     # everywhere (the sweep tests convergence every F sweeps; auto F is 1 on
     # this small grid)
     F = int(rg.stats.sweeps_per_launch)
-    assert F in (1, 2)
+    assert F == (1 if resident else 2)
     assert np.mean(rg.sweeps[1:] == -(-ro.sweeps[1:] // F) * F) > 0.9
 
 
@@ -195,7 +199,7 @@ def test_zero_current_settles_to_vdd(pgb):
     g = mk(3, 17, 40, seed=1)
     g.sources = gridgen.Sources(node=np.zeros(0, np.int64), ptr=np.zeros(1, np.int64), t=np.zeros(0), i=np.zeros(0))
     for F in (1, 2, 3):
-        rg, V = gpu_run(pgb, g, 10, tol=1e-12, omega=1.5, options={"fuse": F})
+        rg, V = gpu_run(pgb, g, 10, tol=1e-12, omega=1.5, options={"fuse": F, "resident": 0})
         assert np.abs(rg.probes - 1.0).max() <= 1e-13
         # one launch (F sweeps) per step: the first sweep already meets tol
         assert np.all(rg.sweeps[1:] == F)

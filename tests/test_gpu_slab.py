@@ -27,6 +27,7 @@ def pgb():
 def single(P, g, steps, tol, omega, k, F):
     G = P.Grid.from_mesh_grid(g, device=True)
     G.set_option("fuse", F)
+    G.set_option("resident", 0)   # the slabs run the streaming sweep
     r = G.transient(g.h, steps, tol=tol, omega=omega, max_sweeps=k, raise_on_noconv=False)
     V = G.voltages().reshape(g.layers, g.ny, g.nx)
     G.close()
