@@ -127,6 +127,9 @@ PG_API int pg_set_stream(pg_grid *g, void *stream);
  *            runs all sweeps of a time step in one cluster launch with V in
  *            shared memory (convergence tested after every sweep, so
  *            pg_stats.sweeps_per_launch = 1); 0: the streaming sweep
+ *   "pipe"   1 (default): full launches of F = 2 mesh sweeps run the
+ *            warp-specialised two-level pipeline kernel (k_rb_sweep2); 0: the
+ *            generic temporally blocked kernel for every F (same results)
  *   "graph"  1 (default): replay full batches of sweep launches from a captured
  *            CUDA graph (single grids, option "timing" off); 0: plain launches
  *   "rows"   rows per CTA of the mesh sweep (0: auto)

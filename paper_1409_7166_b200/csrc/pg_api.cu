@@ -327,6 +327,8 @@ PG_API int pg_set_option(pg_grid *g, const char *key, int64_t value) {
     g->batch = (int)value;
   } else if (k == "resident") {
     g->resident = value != 0;
+  } else if (k == "pipe") {
+    g->pipe = value != 0;
   } else if (k == "graph") {
     g->use_graph = value != 0;
   } else if (k == "timing") {
@@ -343,6 +345,11 @@ PG_API int pg_set_option(pg_grid *g, const char *key, int64_t value) {
   } else {
     set_error("unknown option: " + k);
     return PG_EINVAL;
+  }
+  // a captured sweep batch bakes in the launch configuration: recapture
+  if (g->batch_exec) {
+    cudaGraphExecDestroy(g->batch_exec);
+    g->batch_exec = nullptr;
   }
   return PG_OK;
 }

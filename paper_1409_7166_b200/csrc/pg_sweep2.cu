@@ -1,0 +1,109 @@
+// Host side and template instances of the two-level red-black SOR pipeline
+// (kernel: pg_sweep2.cuh).  Used for full F = 2 launches of the mesh sweep when
+// option "pipe" is on (default); partial launches (fewer than 2 sweeps left)
+// and other F run k_rb_sweep_fused.
+#include "pg_sweep2.cuh"
+
+namespace pgb {
+
+namespace {
+
+template <int L, int W, bool SLAB>
+cudaError_t launch2_t(pg_grid *g, const FusedParams &P, dim3 grid) {
+  auto kern = k_rb_sweep2<L, W, SLAB>;
+  const size_t smem = Sweep2Geo<L, W>::SMEM;
+  if (g->tma_kernel_set != (const void *)kern || g->tma_smem_set != smem) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return e;
+    }
+    g->tma_kernel_set = (const void *)kern;
+    g->tma_smem_set = smem;
+  }
+  kern<<<grid, dim3(Sweep2Geo<L, W>::NT), smem, g->stream>>>(P);
+  return cudaGetLastError();
+}
+
+template <int L, int W, bool SLAB>
+int occupancy_t() {
+  auto kern = k_rb_sweep2<L, W, SLAB>;
+  const size_t smem = Sweep2Geo<L, W>::SMEM;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    cudaGetLastError();
+    return 1;
+  }
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, Sweep2Geo<L, W>::NT, smem) != cudaSuccess) {
+    cudaGetLastError();
+    return 1;
+  }
+  return n < 1 ? 1 : n;
+}
+
+}  // namespace
+
+int sweep2_width(int L) {
+  switch (L) {
+#define X(l, w) \
+  case l:       \
+    return w;
+    PG_SWEEP2_CASES(X)
+#undef X
+    default:
+      return 0;
+  }
+}
+
+int sweep2_ctas_per_sm(int L, bool slab) {
+  static int cache[2][kMaxLayers + 1] = {};
+  if (L < 1 || L > kMaxLayers) return 1;
+  int &c = cache[slab ? 1 : 0][L];
+  if (c == 0) {
+    switch (L) {
+#define X(l, w) \
+  case l:       \
+    c = slab ? occupancy_t<l, w, true>() : occupancy_t<l, w, false>(); \
+    break;
+      PG_SWEEP2_CASES(X)
+#undef X
+      default:
+        c = 1;
+    }
+  }
+  return c;
+}
+
+int sweep2_rows_per_cta(const pg_grid *g, int ny) {
+  const int W = sweep2_width(g->md.L);
+  const int I = W - 4;
+  const int strips = (g->md.HP + I - 1) / I;
+  int chunks = (g->num_sms * sweep2_ctas_per_sm(g->md.L, g->slab && g->hx.G > 0)) / strips;
+  if (chunks < 1) chunks = 1;
+  int H = (ny + chunks - 1) / chunks;
+  return H < 1 ? 1 : H;
+}
+
+cudaError_t launch_rb_sweep2(pg_grid *g, double omega, double tol, int j, int rows_per_cta, int y_begin,
+                             int y_end, int ypar) {
+  const int L = g->md.L;
+  const int W = sweep2_width(L);
+  if (W == 0) return cudaErrorInvalidValue;
+  FusedParams P;
+  if (!fill_fused_params(g, P, omega, tol, j, 2, W, rows_per_cta, y_begin, y_end, ypar))
+    return cudaErrorNotSupported;
+  const bool halo = g->slab && g->hx.G > 0;
+  const int I = W - 4;
+  const dim3 grid((g->md.HP + I - 1) / I, (y_end - y_begin + rows_per_cta - 1) / rows_per_cta);
+  switch (L) {
+#define X(l, w) \
+  case l:       \
+    return halo ? launch2_t<l, w, true>(g, P, grid) : launch2_t<l, w, false>(g, P, grid);
+    PG_SWEEP2_CASES(X)
+#undef X
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace pgb

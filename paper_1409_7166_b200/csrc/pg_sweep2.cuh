@@ -1,0 +1,391 @@
+// Two-level red-black SOR pipeline (sm_100a): the default mesh relaxation
+// kernel for full launches of F = 2 sweeps (option "pipe", default on).
+#pragma once
+//
+// Same arithmetic and halo scheme as k_rb_sweep_fused<L, 2, ...> (header of
+// pg_sweep_fused.cuh; Eq. (13) with the SOR blend of Eq. (15), §IV, in
+// the red-black numbering of DESIGN.md R12): two sweeps per streaming pass,
+// rows [ys - 4, ye + 4) staged, lanes [2, W - 2) and rows [ys, ye) exact.  What
+// differs is the instruction stream of a streaming step:
+//
+// * Spread TMA issue.  W * L threads (lane = column pair, one layer per W
+//   lanes); after the one CTA barrier per step the refill of the slots that
+//   barrier proved dead is issued by lane 0 of several warps, one copy each
+//   (the mbarrier's tx-count may go transiently negative, its single arrival
+//   is the expect_tx), so no warp carries the whole issue sequence.  (A
+//   separate producer warp would make 9 warps: 3 on one SM sub-partition,
+//   which caps the registers at 168 per thread.)
+// * Split rings.  V rows go through a 12-stage ring (4 KB per stage), the five
+//   node-constant arrays (gx, gy, gz_eff, b, 1/d) through a 6-stage ring: the
+//   second sweep level takes its constants from registers (loaded by the first
+//   level 3 rows earlier), so constant rows are live for 2 steps only.  A
+//   12-step unrolled body then makes every ring slot, mbarrier phase, register
+//   FIFO index (depth 3) and red/black column parity a compile-time constant;
+//   the only runtime parity is per warp (q below), folded into 7 per-thread
+//   shared-memory offsets computed once.
+// * Guard-free steady state.  Steps whose four updates, norm rows and output
+//   row are all inside the CTA's range run without predicates; the 7 warm-up
+//   steps and the <= 12 tail steps run the guarded form of the same body.
+// * Registers first.  Every V operand this thread produced or loaded earlier
+//   comes from a register FIFO; shared memory is read only for values of other
+//   threads (x neighbour in the next/previous lane, z neighbours in other
+//   warps) and for new rows.  The second level's black values feed no later
+//   update, so they are never stored to shared memory, only written out.
+// * A zero "layer -1" block before the gz_eff array of each constant stage
+//   makes the layer-0 lower via conductance 0 without a branch.
+//
+// Streaming step y (u = y - r_first - 1, compile-time modulo 12):
+//   phase A: red_0(y), red_1(y - 3)          | fence.proxy.async; bar 1
+//   phase B: black_0(y - 1), black_1(y - 4)  | write row y - 4 (both colours)
+// red_1(r) needs black_0(r - 1 .. r + 1) (steps <= y - 1), black_0(r) needs
+// red_0(r - 1 .. r + 1) (phase A of this step or before), black_1(r) needs
+// red_1(r - 1 .. r + 1).  Cross-warp operands (z neighbours, lanes 31/32 of a
+// layer row) are read only in the phase after the barrier that follows their
+// write, as in pg_sweep_fused.cuh.
+// Barrier of step y: phase B(y - 1) is complete, so the constant row y - 2
+// and the V row y - 6 (and older) are dead; they are refilled with
+// constant row y + 4 and V row y + 5 (one mbarrier "group" per row pair).
+#include "pg_sweep_fused.cuh"
+
+#include <utility>
+
+namespace pgb {
+
+namespace {
+
+template <int A, int B, class Fn>
+__device__ __forceinline__ void static_for(Fn &&fn) {
+  if constexpr (A < B) {
+    fn(std::integral_constant<int, A>{});
+    static_for<A + 1, B>(fn);
+  }
+}
+
+
+}  // namespace
+
+template <int L, int W>
+struct Sweep2Geo {
+  static constexpr int RW = 2 * W;                    // doubles per layer row of a strip
+  static constexpr int LAY = L * RW;                  // doubles per array row (all layers)
+  static constexpr int NC = W * L;                    // compute threads
+  static constexpr int NT = NC;                       // threads per CTA
+  static constexpr int NWARP = NC / 32;
+  static constexpr int SV = 12, SC = 6;               // ring stages (V, constants)
+  static constexpr int VST = LAY;                     // doubles per V stage
+  static constexpr int CGX = 0, CGY = LAY, CZ0 = 2 * LAY, CGZ = 2 * LAY + RW, CB = 3 * LAY + RW,
+                       CID = 4 * LAY + RW;            // constant stage: gx, gy, [zero layer], gz, b, 1/d
+  static constexpr int CST = 5 * LAY + RW;            // doubles per constant stage
+  static constexpr int GUARD = RW;                    // zero band before and after the V ring
+  static constexpr int VOFF = GUARD;                  // V ring offset (doubles)
+  static constexpr int COFF = GUARD + SV * VST + GUARD;
+  static constexpr size_t SMEM = (size_t)(COFF + SC * CST) * 8;
+  static constexpr uint32_t VBYTES = VST * 8u, CBYTES = 5u * LAY * 8u;
+  static constexpr int FH = 2, I = W - 2 * FH;        // x halo (F = 2), exact pairs per strip
+};
+
+template <int L, int W, bool SLAB>
+__global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ FusedParams P) {
+  using Gm = Sweep2Geo<L, W>;
+  constexpr int RW = Gm::RW, NT = Gm::NT, SV = Gm::SV, SC = Gm::SC;
+  constexpr int VST = Gm::VST, CST = Gm::CST;
+  constexpr int CGX = Gm::CGX, CGY = Gm::CGY, CGZ = Gm::CGZ, CB = Gm::CB, CID = Gm::CID;
+  constexpr int FH = Gm::FH, I = Gm::I;
+  extern __shared__ __align__(128) double sm2[];
+  __shared__ uint64_t gbar[SC];
+  double *vring = sm2 + Gm::VOFF;
+  double *cring = sm2 + Gm::COFF;
+
+  const int tid = threadIdx.x;
+  DevCtl *ctl = P.ctl;
+  const int j = *(volatile int32_t *)&ctl->jbase + P.launch_idx;
+  // device-side convergence control, as in k_rb_sweep_fused (uniform)
+  if (*(volatile int32_t *)&ctl->done) return;
+  if (j > 0) {
+    const double prev = __longlong_as_double(
+        (long long)(*(volatile unsigned long long *)&ctl->dmax[(j - 1) & (kRing - 1)]));
+    if (prev < P.tol) {
+      if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) {
+        ctl->done = 1;
+        ctl->launches_done = j;
+      }
+      return;
+    }
+  }
+  if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) ctl->dmax[(j + 1) & (kRing - 1)] = 0ull;
+
+  const int par = (*(volatile int32_t *)&ctl->base + j) & 1;
+  const int ps = blockIdx.x * I - FH;  // first pair of the strip (even)
+  const int ys = P.y_begin + blockIdx.y * P.rows_per_cta;
+  const int ye = min(ys + P.rows_per_cta, P.y_end);
+  const int r_first = ys - 4, r_last = ye + 3;
+
+  // zero bands: before / after the V ring, the "layer -1" block of every constant stage
+  for (int k = tid; k < RW; k += NT) {
+    sm2[k] = 0.0;
+    vring[SV * VST + k] = 0.0;
+  }
+  for (int k = tid; k < SC * RW; k += NT) cring[(k / RW) * CST + Gm::CZ0 + (k % RW)] = 0.0;
+  if (tid == 0) {
+    for (int s = 0; s < SC; ++s) mbar_init(&gbar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  // ---------------------------------------------------------------- TMA issue
+  const CUtensorMap *mVin = par ? &P.mV1 : &P.mV0;
+  auto v_src = [&](int r, int &rr) -> const CUtensorMap * {
+    if constexpr (SLAB) {
+      if (P.has_rlo && r < P.y_begin) {
+        rr = r - (P.y_begin - P.G);
+        return &P.mRlo;
+      }
+      if (P.has_rhi && r >= P.y_end) {
+        rr = r - P.y_end;
+        return &P.mRhi;
+      }
+    }
+    rr = r;
+    return mVin;
+  };
+  // group r: constant row r + V row r + 1 (+ V row r for the first group).
+  // The five constant maps are consecutive in FusedParams (mgx, mgy, mgz, mb,
+  // mid) and their stage offsets are a * LAY (+ RW from gz_eff on), so every
+  // copy is the same instruction sequence (small code: it is replicated in
+  // each of the 12 unrolled steps).
+  constexpr int kL2Ahead = PG_L2_AHEAD;
+  const CUtensorMap *mC = &P.mgx;
+  auto c_dst = [&](int r, int a) { return cring + ((r - r_first) % SC) * CST + a * Gm::LAY + (a >= 2 ? RW : 0); };
+  auto c_bar = [&](int r) { return &gbar[(r - r_first) % SC]; };
+  auto v_copy = [&](int rv_row, int r) {  // V row rv_row into its slot, completing group r
+    int rv;
+    const CUtensorMap *m = v_src(rv_row, rv);
+    tma4(vring + ((rv_row - r_first) % SV) * VST, m, c_bar(r), ps, rv);
+  };
+  auto v_prefetch = [&](int rv_row) {
+    int rv;
+    const CUtensorMap *m = v_src(rv_row, rv);
+    tma4_prefetch(m, ps, rv);
+  };
+  if (tid == 0) {
+    for (int r = r_first; r < r_first + SC && r <= r_last; ++r) {
+      const bool v1 = r + 1 <= r_last, v0 = r == r_first;
+      mbar_expect_tx(c_bar(r), Gm::CBYTES + (v1 ? Gm::VBYTES : 0u) + (v0 ? Gm::VBYTES : 0u));
+      for (int a = 0; a < 5; ++a) tma4(c_dst(r, a), mC + a, c_bar(r), ps, r);
+      if (v1) v_copy(r + 1, r);
+      if (v0) v_copy(r, r);
+    }
+    if (kL2Ahead > 0)
+      for (int r = r_first + SC; r < r_first + SC + kL2Ahead && r <= r_last; ++r) {
+        for (int a = 0; a < 5; ++a) tma4_prefetch(mC + a, ps, r);
+        if (r + 1 <= r_last) v_prefetch(r + 1);
+      }
+  }
+  const int warp = tid >> 5;
+  // refill after the barrier of step y: group R = y + 4 (slots of constant row
+  // y - 2 and V row y - 7).  Lane 0 of warp w issues op w (w + NWARP, ...):
+  // ops 0..4 constant array a = op (op 0 also posts expect_tx), 5: V row R + 1,
+  // 6: L2 prefetch of group R + PG_L2_AHEAD.
+  // cs / vs: ring slots of constant row R and V row R + 1 (compile-time in the
+  // unrolled steps: (u + 5) mod SC and (u + 6) mod SV)
+  auto refill = [&](const int y, const int cs, const int vs) {
+    const int R = y + 4;
+    if ((tid & 31) == 0 && R >= r_first + SC && R <= r_last) {
+      uint64_t *bar = &gbar[cs];
+      double *cdst = cring + cs * CST;
+#pragma unroll 1
+      for (int op = warp; op < 7; op += Gm::NWARP) {
+        if (op < 5) {
+          if (op == 0) mbar_expect_tx(bar, Gm::CBYTES + (R + 1 <= r_last ? Gm::VBYTES : 0u));
+          tma4(cdst + op * Gm::LAY + (op >= 2 ? RW : 0), mC + op, bar, ps, R);
+        } else if (op == 5) {
+          if (R + 1 <= r_last) {
+            int rv;
+            const CUtensorMap *m = v_src(R + 1, rv);
+            tma4(vring + vs * VST, m, bar, ps, rv);
+          }
+        } else if (kL2Ahead > 0 && R + kL2Ahead <= r_last) {
+#pragma unroll 1
+          for (int a = 0; a < 5; ++a) tma4_prefetch(mC + a, ps, R + kL2Ahead);
+          if (R + kL2Ahead + 1 <= r_last) v_prefetch(R + kL2Ahead + 1);
+        }
+      }
+    }
+  };
+
+  // -------------------------------------------------------------- compute warps
+  const int l = tid / W, lane = tid % W;
+  const int pe = l * RW + lane, po = pe + W;
+  // red node of row r sits in the odd column of the pair iff q ^ ((r - r_first - 1) & 1)
+  const int q = (l + P.ypar + r_first + 1) & 1;
+  // per parity class k (column parity q ^ k): node, x neighbour in the next /
+  // previous lane, gx index of the link to that neighbour
+  const int ME0 = q ? po : pe, ME1 = q ? pe : po;
+  const int OT0 = q ? pe + 1 : po - 1, OT1 = q ? po - 1 : pe + 1;
+  const int GX0 = q ? po : po - 1, GX1 = q ? po - 1 : po;
+  const int gp = ps + lane;
+  const bool exact_lane = lane >= FH && lane < FH + I && gp < P.HP;
+  double *Vout = par ? P.V0 : P.V1;
+  double *vout_e = Vout + (int64_t)l * P.layer_stride + gp;
+  double *vout_o = vout_e + P.HP;
+  double *OUT0 = q ? vout_o : vout_e, *OUT1 = q ? vout_e : vout_o;  // red's column for class 0 / 1
+  const double w = P.omega;
+  double dmax = 0.0;
+
+  // register FIFOs (entry = step index mod 3): values this thread produced,
+  // old black values it loaded, constants level 0 loaded for level 1
+  double fR0[3], fB0[3], fR1[3], fWn[3];
+  NodeC cR[3], cB[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    fR0[k] = fB0[k] = fR1[k] = fWn[k] = 0.0;
+    cR[k] = NodeC{0, 0, 0, 0, 0, 0, 0, 0};
+    cB[k] = NodeC{0, 0, 0, 0, 0, 0, 0, 0};
+  }
+
+  auto step = [&](auto U_, auto G_, const int y) {
+    constexpr int u = decltype(U_)::value;
+    constexpr bool G = decltype(G_)::value;  // guarded (warm-up / tail)
+    constexpr int k = u & 1;
+    constexpr int f0 = u % 3, f1 = (u + 2) % 3, f2 = (u + 1) % 3;  // FIFO: now / 1 / 2 (3 = f0) steps ago
+    // ring slots: V row y + d -> (u + 1 + d) mod SV, constant row y + d -> (u + 1 + d) mod SC
+    constexpr int vY = ((u + 1) % SV) * VST, vY1 = ((u + 2) % SV) * VST, vYm = (u % SV) * VST;
+    constexpr int vY2 = ((u + SV - 1) % SV) * VST, vY3 = ((u + SV - 2) % SV) * VST;
+    constexpr int vY4 = ((u + SV - 3) % SV) * VST, vY5 = ((u + SV - 4) % SV) * VST;
+    constexpr int cY = ((u + 1) % SC) * CST, cYm = (u % SC) * CST;
+    const int me = k ? ME1 : ME0, mo = k ? ME0 : ME1;
+    const int ot = k ? OT1 : OT0, ot3 = k ? OT0 : OT1;
+    const int gxo = k ? GX1 : GX0;
+
+    if constexpr (u == 0) mbar_wait(&gbar[0], 0u);  // group r_first: V row r_first, constant row r_first
+    mbar_wait(&gbar[(u + 1) % SC], (uint32_t)(((u + 1) / SC) & 1));
+
+    // ---------------------------------------------------------- phase A
+    // red_0(y): column class k
+    const double Vc = vring[vY + me];
+    const double Vown = vring[vY + mo];
+    const double Voth = vring[vY + ot];
+    const double VN = G ? vring[vYm + me] : fWn[f1];
+    NodeC c0;
+    c0.gxOwn = cring[cY + CGX + pe];
+    c0.gxOth = cring[cY + CGX + gxo];
+    c0.gyN = cring[cYm + CGY + me];
+    c0.gyS = cring[cY + CGY + me];
+    c0.gzU = cring[cY + CGZ + me];
+    c0.gzD = cring[cY + CGZ + me - RW];
+    c0.b = cring[cY + CB + me];
+    c0.id = cring[cY + CID + me];
+    double r0 = upd_c(c0, w, Vc, Vown, Voth, VN, vring[vY1 + me], vring[vY + me + RW], vring[vY + me - RW]);
+    // red_1(y - 3): column class k ^ 1 (= mo)
+    const double Vc1 = G ? vring[vY3 + mo] : fR0[f0];
+    const double Vown1 = G ? vring[vY3 + me] : fB0[f2];
+    const double VN1 = G ? vring[vY4 + mo] : fB0[f0];
+    const double VS1 = G ? vring[vY2 + mo] : fB0[f1];
+    double r1 = upd_c(cR[f0], w, Vc1, Vown1, vring[vY3 + ot3], VN1, VS1, vring[vY3 + mo + RW],
+                      vring[vY3 + mo - RW]);
+    double dA;
+    if (G) {
+      const bool in0 = y > r_first && y < r_last, in1 = y - 3 > r_first && y - 3 < r_last;
+      if (in0) vring[vY + me] = r0; else r0 = Vc;
+      if (in1) vring[vY3 + mo] = r1; else r1 = Vc1;
+      dA = (y - 3 >= ys && y - 3 < ye) ? fabs(r1 - Vc1) : 0.0;
+    } else {
+      vring[vY + me] = r0;
+      vring[vY3 + mo] = r1;
+      dA = fabs(r1 - Vc1);
+    }
+    fence_proxy_async();
+    __syncthreads();
+    refill(y, (u + 5) % SC, (u + 6) % SV);
+
+    // ---------------------------------------------------------- phase B
+    // black_0(y - 1): column class k (its old value is red_0(y)'s north operand)
+    NodeC cb;
+    cb.gxOwn = cring[cYm + CGX + pe];
+    cb.gxOth = cring[cYm + CGX + gxo];
+    cb.gyN = cR[f2].gyS;  // gy of row y - 2 in this column: red_0(y - 2)'s own south link
+    cb.gyS = c0.gyN;
+    cb.gzU = cring[cYm + CGZ + me];
+    cb.gzD = cring[cYm + CGZ + me - RW];
+    cb.b = cring[cYm + CB + me];
+    cb.id = cring[cYm + CID + me];
+    const double Vownb = G ? vring[vYm + mo] : fR0[f1];
+    const double VNb = G ? vring[vY2 + me] : fR0[f2];
+    double b0 = upd_c(cb, w, VN, Vownb, vring[vYm + ot], VNb, r0, vring[vYm + me + RW], vring[vYm + me - RW]);
+    // black_1(y - 4): column class k ^ 1
+    const double Vcb1 = G ? vring[vY4 + mo] : fB0[f0];
+    const double Vownb1 = G ? vring[vY4 + me] : fR1[f1];  // red_1(y - 4): this row's other colour
+    const double VNb1 = G ? vring[vY5 + mo] : fR1[f2];
+    double b1 = upd_c(cB[f0], w, Vcb1, Vownb1, vring[vY4 + ot3], VNb1, r1, vring[vY4 + mo + RW],
+                      vring[vY4 + mo - RW]);
+    double dB;
+    bool out = true;
+    if (G) {
+      const bool inb0 = y - 1 > r_first && y - 1 < r_last, inb1 = y - 4 > r_first && y - 4 < r_last;
+      if (inb0) vring[vYm + me] = b0; else b0 = VN;
+      if (!inb1) b1 = Vcb1;
+      out = y - 4 >= ys && y - 4 < ye;
+      dB = out ? fabs(b1 - Vcb1) : 0.0;
+    } else {
+      vring[vYm + me] = b0;
+      dB = fabs(b1 - Vcb1);
+    }
+    // row y - 4 is final: red_1 (class k) and black_1 (class k ^ 1)
+    if (out && exact_lane) {
+      const int64_t ro = (int64_t)(y - 4) * P.NXP;
+      (k ? OUT1 : OUT0)[ro] = Vownb1;
+      (k ? OUT0 : OUT1)[ro] = b1;
+      if constexpr (SLAB) {
+        const int rr = y - 4;
+        const bool red_odd = (q ^ k) != 0;
+        const double ve = red_odd ? b1 : Vownb1, vo = red_odd ? Vownb1 : b1;
+        if (P.send_lo && rr < P.y_begin + P.G) {
+          double *sb = P.send_lo + ((int64_t)l * P.G + (rr - P.y_begin)) * P.NXP;
+          sb[gp] = ve;
+          sb[gp + P.HP] = vo;
+        }
+        if (P.send_hi && rr >= P.y_end - P.G) {
+          double *sb = P.send_hi + ((int64_t)l * P.G + (rr - (P.y_end - P.G))) * P.NXP;
+          sb[gp] = ve;
+          sb[gp + P.HP] = vo;
+        }
+      }
+    }
+    dA = dA > dB ? dA : dB;
+    dmax = dA > dmax ? dA : dmax;
+    fR0[f0] = r0;
+    fB0[f0] = b0;
+    fR1[f0] = r1;
+    fWn[f0] = Vown;
+    cR[f0] = c0;
+    cB[f0] = cb;
+  };
+
+  // warm-up: y = r_first + 1 .. r_first + 7 (r_last - r_first = H + 7 >= 8)
+  int y = r_first + 1;
+  static_for<0, 7>([&](auto U) {
+    step(U, std::true_type{}, y);
+    ++y;
+  });
+  // steady state: y in [r_first + 8, r_last - 1], blocks of 12 steps
+  for (; y + 11 <= r_last - 1; y += 12) {
+    static_for<7, 19>([&](auto U) { step(U, std::false_type{}, y + (decltype(U)::value - 7)); });
+  }
+  // tail: up to 12 guarded steps until y = r_last
+  static_for<7, 19>([&](auto U) {
+    if (y <= r_last) step(U, std::true_type{}, y);
+    ++y;
+  });
+
+  if (!exact_lane) dmax = 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+  if ((tid & 31) == 0)
+    atomicMax(&ctl->dmax[j & (kRing - 1)], static_cast<unsigned long long>(__double_as_longlong(dmax)));
+}
+
+// Compiled (L, W): W = 64 for L <= 4, W = 32 for L = 5..8 (the fused sweep's default widths)
+#define PG_SWEEP2_CASES(X) \
+  X(1, 64) X(2, 64) X(3, 64) X(4, 64) X(5, 32) X(6, 32) X(7, 32) X(8, 32)
+
+}  // namespace pgb

@@ -135,11 +135,9 @@ int fused_ctas_per_sm(int L, int S, int W) {
   return c < 1 ? 1 : c;
 }
 
-cudaError_t launch_rb_sweep_fused(pg_grid *g, double omega, double tol, int j, int nsw, int F,
-                                  int S, int D, int W, int rows_per_cta, int y_begin, int y_end,
-                                  int ypar) {
-  if (!tma_available(g)) return cudaErrorNotSupported;
-  FusedParams P;
+bool fill_fused_params(pg_grid *g, FusedParams &P, double omega, double tol, int j, int nsw, int W,
+                       int rows_per_cta, int y_begin, int y_end, int ypar) {
+  if (!tma_available(g)) return false;
   const CUtensorMap *tm = g->tmap[W == 64 ? 1 : 0];
   P.mV0 = tm[0];
   P.mV1 = tm[1];
@@ -174,6 +172,16 @@ cudaError_t launch_rb_sweep_fused(pg_grid *g, double omega, double tol, int j, i
   P.send_hi = halo && h.has_hi ? h.send_hi : nullptr;
   if (P.has_rlo) P.mRlo = h.mlo[W == 64 ? 1 : 0];
   if (P.has_rhi) P.mRhi = h.mhi[W == 64 ? 1 : 0];
+  return true;
+}
+
+cudaError_t launch_rb_sweep_fused(pg_grid *g, double omega, double tol, int j, int nsw, int F,
+                                  int S, int D, int W, int rows_per_cta, int y_begin, int y_end,
+                                  int ypar) {
+  FusedParams P;
+  if (!fill_fused_params(g, P, omega, tol, j, nsw, W, rows_per_cta, y_begin, y_end, ypar))
+    return cudaErrorNotSupported;
+  const bool halo = g->slab && g->hx.G > 0;
   const int strips = (g->md.HP + fused_exact_lanes(F, W) - 1) / fused_exact_lanes(F, W);
   const dim3 grid(strips, (y_end - y_begin + rows_per_cta - 1) / rows_per_cta);
   const int key = fused_key(g->md.L, F, S, D, W, halo);

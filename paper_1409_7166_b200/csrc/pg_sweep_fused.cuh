@@ -577,6 +577,10 @@ cudaError_t launch_fused_t(pg_grid *g, const FusedParams &P, dim3 grid) {
   X(1, 1, 6, 3, 32) X(2, 1, 6, 3, 32) X(3, 1, 6, 3, 32) X(4, 1, 6, 3, 32)                          \
   X(5, 1, 6, 3, 32) X(6, 1, 6, 3, 32) X(7, 1, 6, 3, 32) X(8, 1, 6, 3, 32)
 
+// FusedParams of a launch over rows [y_begin, y_end) (false: no TMA maps)
+bool fill_fused_params(pg_grid *g, FusedParams &P, double omega, double tol, int j, int nsw, int W,
+                       int rows_per_cta, int y_begin, int y_end, int ypar);
+
 constexpr int fused_key(int L, int F, int S, int D, int W, bool slab = false) {
   return ((((L * 8 + F) * 32 + S) * 8 + D) * 2 + (W == 64)) * 2 + (slab ? 1 : 0);
 }
