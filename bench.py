@@ -149,14 +149,14 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(F: int):
-    """dram bytes per launch of the sweep kernel (F sweeps per launch) from the
-    committed ncu capture of the same configuration, if any."""
+def ncu_traffic(kernel: str):
+    """dram bytes per launch of the sweep kernel from the committed ncu
+    capture of the same configuration (profiles/rb_sweep_traffic.json), if any."""
     p = os.path.join(ROOT, "profiles", "rb_sweep_traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        e = d.get(f"F{F}") if isinstance(d.get(f"F{F}"), dict) else None
+        e = d.get(kernel) if isinstance(d.get(kernel), dict) else None
         return None if e is None else e.get("dram_bytes_per_launch")
     except Exception:
         return None
@@ -251,7 +251,6 @@ def run_b200(args):
         G = mk(g, device=True)
         G.set_stream(stream)
         my_nodes = g.n
-    G.set_option("timing", 1)
     for k, v in opts.items():
         for q in (grp.grids if grp is not None else [G]):
             q.set_option(k, int(v))
@@ -281,6 +280,13 @@ def run_b200(args):
         if world > 1:
             dist.barrier()
 
+    def set_timing(on):
+        for q in (grp.grids if grp is not None else [G]):
+            q.set_option("timing", 1 if on else 0)
+
+    # headline: the production configuration (CUDA-graph batches, programmatic
+    # dependent launch of consecutive sweeps), timed with events on `stream`
+    set_timing(False)
     for _ in range(args.warmup):
         solve()
     clocks = ClockSampler(local)
@@ -290,15 +296,11 @@ def run_b200(args):
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     sweeps = launches = 0
-    sweep_ms = 0.0
-    sweep_launches = 0
     sweeps_per_tstep = []
     for _ in range(args.steps):
         r = solve()
         sweeps += int(r.stats.sweeps_total)
         launches += int(r.stats.kernel_launches)
-        sweep_ms += float(r.stats.sweep_ms)
-        sweep_launches += int(r.stats.sweep_launches)
         sweeps_per_tstep.append(r.sweeps[1:])
     ev1.record(stream)
     barrier()
@@ -308,6 +310,25 @@ def run_b200(args):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
+
+    # sweep-kernel duration for the roofline: the same K steps again with a
+    # CUDA event after every sweep launch (plain launches, no graph)
+    set_timing(True)
+    sweep_ms = 0.0
+    sweep_launches = 0
+    t1 = 0.0
+    barrier()
+    e_a = torch.cuda.Event(enable_timing=True)
+    e_b = torch.cuda.Event(enable_timing=True)
+    e_a.record(stream)
+    for _ in range(args.steps):
+        rt = solve()
+        sweep_ms += float(rt.stats.sweep_ms)
+        sweep_launches += int(rt.stats.sweep_launches)
+    e_b.record(stream)
+    barrier()
+    t1 = e_a.elapsed_time(e_b)
+    set_timing(False)
     node_sweeps = float(my_nodes) * sweeps
     tot = torch.tensor([node_sweeps], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -323,7 +344,7 @@ def run_b200(args):
         grids = grp.grids if grp is not None else [G]   # local group: one launch = all slabs
         launch_nodes = sum(q.info()["layers"] * q.info()["ny"] * q.info()["nx"] for q in grids)
         bytes_per_launch = BYTES_PER_NODE_PASS * launch_nodes
-        kname = "k_rb_sweep_fused"
+        kname = "k_rb_sweep2" if F == 2 and int(opts.get("pipe", 1)) else "k_rb_sweep_fused"
     else:
         # CSR sweep (one launch per colour per sweep): rowptr 8 + b 8 + 1/d 8 +
         # V read + write 16 per row, column index 4 + value 8 per entry
@@ -334,12 +355,16 @@ def run_b200(args):
         kname = "k_csr_sweep"
     achieved = bytes_per_launch / (avg_launch_ms * 1e-3) / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": ncu_traffic(F) if hasattr(g, "gx") and cfg == 1 else None,
+            "frac": achieved / peak, "traffic": ncu_traffic(kname) if hasattr(g, "gx") and cfg == 1 else None,
             "kernel": kname, "bytes_per_launch": bytes_per_launch,
             "bytes_per_node_per_launch": bytes_per_launch / launch_nodes, "sweeps_per_launch": F,
             "bytes_per_node_sweep": bytes_per_launch / launch_nodes / F, "avg_launch_us": avg_launch_ms * 1e3,
             "kernel_node_sweeps_per_s": launch_nodes * F / (avg_launch_ms * 1e-3) / 1e9,
-            "sweep_share_of_step": sweep_ms / ms if ms > 0 else None, "peak_source": peak_src}
+            "sweep_share_of_step": sweep_ms / t1 if t1 > 0 else None, "peak_source": peak_src,
+            "timing": "avg_launch_us: CUDA events after every sweep launch on the launch stream, "
+                      "in a second pass over the same K bench steps (plain launches); the headline "
+                      "value is the first pass (graph batches + programmatic dependent launch)",
+            "effective_launch_us": ms_max * (sweep_ms / t1 if t1 > 0 else 1.0) / max(sweep_launches, 1) * 1e3}
 
     # e2e: public C-ABI call with host buffers (pinned), copies inside the timed region
     e2e = None

@@ -130,6 +130,9 @@ PG_API int pg_set_stream(pg_grid *g, void *stream);
  *   "pipe"   1 (default): full launches of F = 2 mesh sweeps run the
  *            warp-specialised two-level pipeline kernel (k_rb_sweep2); 0: the
  *            generic temporally blocked kernel for every F (same results)
+ *   "pdl"    1 (default): consecutive sweep launches of a single grid use
+ *            programmatic dependent launch (the next launch's prologue and
+ *            constant-row loads overlap the previous launch's tail); 0: off
  *   "graph"  1 (default): replay full batches of sweep launches from a captured
  *            CUDA graph (single grids, option "timing" off); 0: plain launches
  *   "rows"   rows per CTA of the mesh sweep (0: auto)

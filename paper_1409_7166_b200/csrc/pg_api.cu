@@ -329,6 +329,8 @@ PG_API int pg_set_option(pg_grid *g, const char *key, int64_t value) {
     g->resident = value != 0;
   } else if (k == "pipe") {
     g->pipe = value != 0;
+  } else if (k == "pdl") {
+    g->pdl = value != 0;
   } else if (k == "graph") {
     g->use_graph = value != 0;
   } else if (k == "timing") {
@@ -658,6 +660,10 @@ int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, d
 
   int64_t launches = 0;
   const bool graph_ok = g->use_graph && ng == 1 && ex == nullptr && !g->timing;
+  // consecutive sweep launches of a single grid may overlap (PDL): launch
+  // j > 0 of a batch directly follows launch j - 1 in the stream
+  for (int k = 0; k < ng; ++k) gs[k]->pdl_ok = false;
+  g->pdl_ok = g->pdl != 0 && ng == 1 && ex == nullptr;
   const bool resident = ng == 1 && ex == nullptr && resident_ok(g, method);
   const int F = sweeps_per_launch(g, method);
   for (int k = 1; k < ng; ++k)

@@ -139,6 +139,8 @@ struct pg_grid {
   int use_graph = 1;                   // option "graph": replay captured sweep batches
   int resident = 1;                    // option "resident": one-CTA sweep loop for tiny meshes
   int pipe = 1;                        // option "pipe": two-level pipeline kernel for full F = 2 launches
+  int pdl = 1;                         // option "pdl": programmatic dependent launch of consecutive sweeps
+  bool pdl_ok = false;                 // set by run_transient: single grid, no exchange between launches
   cudaGraphExec_t batch_exec = nullptr;  // captured batch of `batch` full sweep launches
   cudaStream_t cap_stream = nullptr;     // private stream the batch graph is captured on
   double graph_key[6] = {0, 0, 0, 0, 0, 0};  // omega, tol, method, F, batch, stream of the capture
@@ -178,8 +180,9 @@ cudaError_t launch_rb_sweep_fused(pg_grid *g, double omega, double tol, int j, i
 int sweep2_width(int L);  // strip width of the compiled variant, 0: none
 int sweep2_ctas_per_sm(int L, bool slab);
 int sweep2_rows_per_cta(const pg_grid *g, int ny);
+// pdl: launch with programmatic stream serialisation after a sweep launch
 cudaError_t launch_rb_sweep2(pg_grid *g, double omega, double tol, int j, int rows_per_cta, int y_begin,
-                             int y_end, int ypar);
+                             int y_end, int ypar, bool pdl);
 
 // Multi-grid driver (pg_api.cu): Algorithm 1 over ng grids in lockstep; `ex`
 // (may be null) runs after every sweep launch of all grids.

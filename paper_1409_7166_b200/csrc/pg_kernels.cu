@@ -777,7 +777,7 @@ cudaError_t launch_sweep(pg_grid *g, int method, double omega, double tol, int j
       ++*launches;
       if (g->pipe && c.F == 2 && nsweeps == 2 && sweep2_width(g->md.L) == c.W) {
         const int H2 = g->rows > 0 ? std::max(1, std::min(g->rows, y1 - y0)) : sweep2_rows_per_cta(g, y1 - y0);
-        return launch_rb_sweep2(g, omega, tol, j, H2, y0, y1, g->slab ? g->ypar : 0);
+        return launch_rb_sweep2(g, omega, tol, j, H2, y0, y1, g->slab ? g->ypar : 0, g->pdl_ok && j > 0);
       }
       const int H = fused_rows_per_cta(g, c.F, c.S, c.W, y1 - y0);
       return launch_rb_sweep_fused(g, omega, tol, j, nsweeps, c.F, c.S, c.D, c.W, H, y0, y1,

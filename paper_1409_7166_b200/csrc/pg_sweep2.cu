@@ -9,7 +9,7 @@ namespace pgb {
 namespace {
 
 template <int L, int W, bool SLAB>
-cudaError_t launch2_t(pg_grid *g, const FusedParams &P, dim3 grid) {
+cudaError_t launch2_t(pg_grid *g, const FusedParams &P, dim3 grid, bool pdl) {
   auto kern = k_rb_sweep2<L, W, SLAB>;
   const size_t smem = Sweep2Geo<L, W>::SMEM;
   if (g->tma_kernel_set != (const void *)kern || g->tma_smem_set != smem) {
@@ -21,8 +21,19 @@ cudaError_t launch2_t(pg_grid *g, const FusedParams &P, dim3 grid) {
     g->tma_kernel_set = (const void *)kern;
     g->tma_smem_set = smem;
   }
-  kern<<<grid, dim3(Sweep2Geo<L, W>::NT), smem, g->stream>>>(P);
-  return cudaGetLastError();
+  // programmatic dependent launch: this grid may start (prologue, constant
+  // rows) while the previous sweep launch drains; it waits for it in-kernel
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(Sweep2Geo<L, W>::NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = g->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, P);
 }
 
 template <int L, int W, bool SLAB>
@@ -85,20 +96,21 @@ int sweep2_rows_per_cta(const pg_grid *g, int ny) {
 }
 
 cudaError_t launch_rb_sweep2(pg_grid *g, double omega, double tol, int j, int rows_per_cta, int y_begin,
-                             int y_end, int ypar) {
+                             int y_end, int ypar, bool pdl) {
   const int L = g->md.L;
   const int W = sweep2_width(L);
   if (W == 0) return cudaErrorInvalidValue;
   FusedParams P;
   if (!fill_fused_params(g, P, omega, tol, j, 2, W, rows_per_cta, y_begin, y_end, ypar))
     return cudaErrorNotSupported;
+  P.pre = pdl ? 1 : 0;
   const bool halo = g->slab && g->hx.G > 0;
   const int I = W - 4;
   const dim3 grid((g->md.HP + I - 1) / I, (y_end - y_begin + rows_per_cta - 1) / rows_per_cta);
   switch (L) {
 #define X(l, w) \
   case l:       \
-    return halo ? launch2_t<l, w, true>(g, P, grid) : launch2_t<l, w, false>(g, P, grid);
+    return halo ? launch2_t<l, w, true>(g, P, grid, pdl) : launch2_t<l, w, false>(g, P, grid, pdl);
     PG_SWEEP2_CASES(X)
 #undef X
     default:

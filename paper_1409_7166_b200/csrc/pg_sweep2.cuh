@@ -23,9 +23,10 @@
 //   FIFO index (depth 3) and red/black column parity a compile-time constant;
 //   the only runtime parity is per warp (q below), folded into 7 per-thread
 //   shared-memory offsets computed once.
-// * Guard-free steady state.  Steps whose four updates, norm rows and output
-//   row are all inside the CTA's range run without predicates; the 7 warm-up
-//   steps and the <= 12 tail steps run the guarded form of the same body.
+// * One body for every step.  The first and last steps run the same
+//   unguarded body as the steady state (no cold warm-up / tail code: the
+//   kernel's whole streaming loop is one 12-step block); only the norm and the
+//   write-out are masked to the owned rows.
 // * Registers first.  Every V operand this thread produced or loaded earlier
 //   comes from a register FIFO; shared memory is read only for values of other
 //   threads (x neighbour in the next/previous lane, z neighbours in other
@@ -98,27 +99,11 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
 
   const int tid = threadIdx.x;
   DevCtl *ctl = P.ctl;
-  const int j = *(volatile int32_t *)&ctl->jbase + P.launch_idx;
-  // device-side convergence control, as in k_rb_sweep_fused (uniform)
-  if (*(volatile int32_t *)&ctl->done) return;
-  if (j > 0) {
-    const double prev = __longlong_as_double(
-        (long long)(*(volatile unsigned long long *)&ctl->dmax[(j - 1) & (kRing - 1)]));
-    if (prev < P.tol) {
-      if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) {
-        ctl->done = 1;
-        ctl->launches_done = j;
-      }
-      return;
-    }
-  }
-  if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) ctl->dmax[(j + 1) & (kRing - 1)] = 0ull;
-
-  const int par = (*(volatile int32_t *)&ctl->base + j) & 1;
   const int ps = blockIdx.x * I - FH;  // first pair of the strip (even)
   const int ys = P.y_begin + blockIdx.y * P.rows_per_cta;
   const int ye = min(ys + P.rows_per_cta, P.y_end);
   const int r_first = ys - 4, r_last = ye + 3;
+  const int n_init = min(SC, r_last - r_first + 1);  // groups issued before the loop
 
   // zero bands: before / after the V ring, the "layer -1" block of every constant stage
   for (int k = tid; k < RW; k += NT) {
@@ -131,6 +116,49 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+
+  // Programmatic dependent launch: when the previous kernel in the stream is
+  // a sweep launch (P.pre), the node constants are not among its outputs, so
+  // the first constant rows are requested before waiting for it; V and the
+  // control block are read only after griddepcontrol.wait.  (Without the
+  // launch attribute the wait is a no-op.)
+  const CUtensorMap *mC = &P.mgx;
+  auto c_dst = [&](int r, int a) { return cring + ((r - r_first) % SC) * CST + a * Gm::LAY + (a >= 2 ? RW : 0); };
+  auto c_bar = [&](int r) { return &gbar[(r - r_first) % SC]; };
+  if (P.pre && tid == 0) {
+    for (int r = r_first; r < r_first + n_init; ++r) {
+      mbar_expect_tx_only(c_bar(r), Gm::CBYTES);
+      for (int a = 0; a < 5; ++a) tma4(c_dst(r, a), mC + a, c_bar(r), ps, r);
+    }
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+  const int j = *(volatile int32_t *)&ctl->jbase + P.launch_idx;
+  // device-side convergence control, as in k_rb_sweep_fused (uniform)
+  bool skip = *(volatile int32_t *)&ctl->done != 0;
+  if (!skip && j > 0) {
+    const double prev = __longlong_as_double(
+        (long long)(*(volatile unsigned long long *)&ctl->dmax[(j - 1) & (kRing - 1)]));
+    if (prev < P.tol) {
+      if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) {
+        ctl->done = 1;
+        ctl->launches_done = j;
+      }
+      skip = true;
+    }
+  }
+  if (skip) {
+    // drain the constant copies already in flight into this CTA's shared memory
+    if (P.pre && tid == 0)
+      for (int r = r_first; r < r_first + n_init; ++r) {
+        mbar_arrive(c_bar(r));
+        mbar_wait(c_bar(r), 0u);
+      }
+    return;
+  }
+  if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) ctl->dmax[(j + 1) & (kRing - 1)] = 0ull;
+  const int par = (*(volatile int32_t *)&ctl->base + j) & 1;
 
   // ---------------------------------------------------------------- TMA issue
   const CUtensorMap *mVin = par ? &P.mV1 : &P.mV0;
@@ -154,9 +182,6 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
   // copy is the same instruction sequence (small code: it is replicated in
   // each of the 12 unrolled steps).
   constexpr int kL2Ahead = PG_L2_AHEAD;
-  const CUtensorMap *mC = &P.mgx;
-  auto c_dst = [&](int r, int a) { return cring + ((r - r_first) % SC) * CST + a * Gm::LAY + (a >= 2 ? RW : 0); };
-  auto c_bar = [&](int r) { return &gbar[(r - r_first) % SC]; };
   auto v_copy = [&](int rv_row, int r) {  // V row rv_row into its slot, completing group r
     int rv;
     const CUtensorMap *m = v_src(rv_row, rv);
@@ -168,10 +193,12 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
     tma4_prefetch(m, ps, rv);
   };
   if (tid == 0) {
-    for (int r = r_first; r < r_first + SC && r <= r_last; ++r) {
+    for (int r = r_first; r < r_first + n_init; ++r) {
       const bool v1 = r + 1 <= r_last, v0 = r == r_first;
-      mbar_expect_tx(c_bar(r), Gm::CBYTES + (v1 ? Gm::VBYTES : 0u) + (v0 ? Gm::VBYTES : 0u));
-      for (int a = 0; a < 5; ++a) tma4(c_dst(r, a), mC + a, c_bar(r), ps, r);
+      const uint32_t vbytes = (v1 ? Gm::VBYTES : 0u) + (v0 ? Gm::VBYTES : 0u);
+      mbar_expect_tx(c_bar(r), vbytes + (P.pre ? 0u : Gm::CBYTES));
+      if (!P.pre)
+        for (int a = 0; a < 5; ++a) tma4(c_dst(r, a), mC + a, c_bar(r), ps, r);
       if (v1) v_copy(r + 1, r);
       if (v0) v_copy(r, r);
     }
@@ -243,29 +270,35 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
     cB[k] = NodeC{0, 0, 0, 0, 0, 0, 0, 0};
   }
 
-  auto step = [&](auto U_, auto G_, const int y) {
+  // One streaming step (u: position modulo 12).  Every step runs the same
+  // unguarded body, also the first and last ones: the updates of rows outside
+  // (r_first, r_last) and of the stale halo rows only read ring slots that are
+  // loaded or hold finite leftovers (never an exact row's operand: an exact
+  // row's level-1 value depends on old values of rows r - 4 .. r + 4 only, all
+  // in [r_first, r_last], and on intermediate values inside that cone), and
+  // their stores go to slots whose next TMA refill is ordered after them by
+  // the per-step proxy fence.  Only the norm and the write-out are masked.
+  auto step = [&](auto U_, const int y) {
     constexpr int u = decltype(U_)::value;
-    constexpr bool G = decltype(G_)::value;  // guarded (warm-up / tail)
     constexpr int k = u & 1;
     constexpr int f0 = u % 3, f1 = (u + 2) % 3, f2 = (u + 1) % 3;  // FIFO: now / 1 / 2 (3 = f0) steps ago
     // ring slots: V row y + d -> (u + 1 + d) mod SV, constant row y + d -> (u + 1 + d) mod SC
     constexpr int vY = ((u + 1) % SV) * VST, vY1 = ((u + 2) % SV) * VST, vYm = (u % SV) * VST;
-    constexpr int vY2 = ((u + SV - 1) % SV) * VST, vY3 = ((u + SV - 2) % SV) * VST;
-    constexpr int vY4 = ((u + SV - 3) % SV) * VST, vY5 = ((u + SV - 4) % SV) * VST;
+    constexpr int vY3 = ((u + SV - 2) % SV) * VST, vY4 = ((u + SV - 3) % SV) * VST;
     constexpr int cY = ((u + 1) % SC) * CST, cYm = (u % SC) * CST;
     const int me = k ? ME1 : ME0, mo = k ? ME0 : ME1;
     const int ot = k ? OT1 : OT0, ot3 = k ? OT0 : OT1;
     const int gxo = k ? GX1 : GX0;
 
-    if constexpr (u == 0) mbar_wait(&gbar[0], 0u);  // group r_first: V row r_first, constant row r_first
     mbar_wait(&gbar[(u + 1) % SC], (uint32_t)(((u + 1) / SC) & 1));
 
     // ---------------------------------------------------------- phase A
-    // red_0(y): column class k
+    // red_0(y): column class k; its north operand (old black of row y - 1) was
+    // loaded as the previous step's own-pair operand
     const double Vc = vring[vY + me];
     const double Vown = vring[vY + mo];
     const double Voth = vring[vY + ot];
-    const double VN = G ? vring[vYm + me] : fWn[f1];
+    const double VN = fWn[f1];
     NodeC c0;
     c0.gxOwn = cring[cY + CGX + pe];
     c0.gxOth = cring[cY + CGX + gxo];
@@ -275,25 +308,16 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
     c0.gzD = cring[cY + CGZ + me - RW];
     c0.b = cring[cY + CB + me];
     c0.id = cring[cY + CID + me];
-    double r0 = upd_c(c0, w, Vc, Vown, Voth, VN, vring[vY1 + me], vring[vY + me + RW], vring[vY + me - RW]);
-    // red_1(y - 3): column class k ^ 1 (= mo)
-    const double Vc1 = G ? vring[vY3 + mo] : fR0[f0];
-    const double Vown1 = G ? vring[vY3 + me] : fB0[f2];
-    const double VN1 = G ? vring[vY4 + mo] : fB0[f0];
-    const double VS1 = G ? vring[vY2 + mo] : fB0[f1];
-    double r1 = upd_c(cR[f0], w, Vc1, Vown1, vring[vY3 + ot3], VN1, VS1, vring[vY3 + mo + RW],
-                      vring[vY3 + mo - RW]);
-    double dA;
-    if (G) {
-      const bool in0 = y > r_first && y < r_last, in1 = y - 3 > r_first && y - 3 < r_last;
-      if (in0) vring[vY + me] = r0; else r0 = Vc;
-      if (in1) vring[vY3 + mo] = r1; else r1 = Vc1;
-      dA = (y - 3 >= ys && y - 3 < ye) ? fabs(r1 - Vc1) : 0.0;
-    } else {
-      vring[vY + me] = r0;
-      vring[vY3 + mo] = r1;
-      dA = fabs(r1 - Vc1);
-    }
+    const double r0 = upd_c(c0, w, Vc, Vown, Voth, VN, vring[vY1 + me], vring[vY + me + RW], vring[vY + me - RW]);
+    // red_1(y - 3): column class k ^ 1 (= mo); own value red_0(y - 3), x
+    // neighbour black_0(y - 3), north / south black_0(y - 4) / black_0(y - 2)
+    const double Vc1 = fR0[f0];
+    const double r1 = upd_c(cR[f0], w, Vc1, fB0[f2], vring[vY3 + ot3], fB0[f0], fB0[f1], vring[vY3 + mo + RW],
+                            vring[vY3 + mo - RW]);
+    vring[vY + me] = r0;
+    vring[vY3 + mo] = r1;
+    double dA = fabs(r1 - Vc1);
+    if (!(y >= ys + 3 && y < r_last)) dA = 0.0;  // norm over rows [ys, ye) only
     fence_proxy_async();
     __syncthreads();
     refill(y, (u + 5) % SC, (u + 6) % SV);
@@ -309,27 +333,18 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
     cb.gzD = cring[cYm + CGZ + me - RW];
     cb.b = cring[cYm + CB + me];
     cb.id = cring[cYm + CID + me];
-    const double Vownb = G ? vring[vYm + mo] : fR0[f1];
-    const double VNb = G ? vring[vY2 + me] : fR0[f2];
-    double b0 = upd_c(cb, w, VN, Vownb, vring[vYm + ot], VNb, r0, vring[vYm + me + RW], vring[vYm + me - RW]);
-    // black_1(y - 4): column class k ^ 1
-    const double Vcb1 = G ? vring[vY4 + mo] : fB0[f0];
-    const double Vownb1 = G ? vring[vY4 + me] : fR1[f1];  // red_1(y - 4): this row's other colour
-    const double VNb1 = G ? vring[vY5 + mo] : fR1[f2];
-    double b1 = upd_c(cB[f0], w, Vcb1, Vownb1, vring[vY4 + ot3], VNb1, r1, vring[vY4 + mo + RW],
-                      vring[vY4 + mo - RW]);
-    double dB;
-    bool out = true;
-    if (G) {
-      const bool inb0 = y - 1 > r_first && y - 1 < r_last, inb1 = y - 4 > r_first && y - 4 < r_last;
-      if (inb0) vring[vYm + me] = b0; else b0 = VN;
-      if (!inb1) b1 = Vcb1;
-      out = y - 4 >= ys && y - 4 < ye;
-      dB = out ? fabs(b1 - Vcb1) : 0.0;
-    } else {
-      vring[vYm + me] = b0;
-      dB = fabs(b1 - Vcb1);
-    }
+    const double b0 = upd_c(cb, w, VN, fR0[f1], vring[vYm + ot], fR0[f2], r0, vring[vYm + me + RW],
+                            vring[vYm + me - RW]);
+    // black_1(y - 4): column class k ^ 1; own value black_0(y - 4), x neighbour
+    // red_1(y - 4), north / south red_1(y - 5) / red_1(y - 3)
+    const double Vcb1 = fB0[f0];
+    const double Vownb1 = fR1[f1];
+    const double b1 = upd_c(cB[f0], w, Vcb1, Vownb1, vring[vY4 + ot3], fR1[f2], r1, vring[vY4 + mo + RW],
+                            vring[vY4 + mo - RW]);
+    vring[vYm + me] = b0;
+    const bool out = y >= ys + 4;  // row y - 4 owned (y - 4 < ye always)
+    double dB = fabs(b1 - Vcb1);
+    if (!out) dB = 0.0;
     // row y - 4 is final: red_1 (class k) and black_1 (class k ^ 1)
     if (out && exact_lane) {
       const int64_t ro = (int64_t)(y - 4) * P.NXP;
@@ -361,21 +376,22 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
     cB[f0] = cb;
   };
 
-  // warm-up: y = r_first + 1 .. r_first + 7 (r_last - r_first = H + 7 >= 8)
+  // the first step's north operand: old black of row r_first in the column of red(r_first + 1)
+  mbar_wait(&gbar[0], 0u);
+  fWn[2] = vring[ME0];
+  // y = r_first + 1 .. r_last (r_last - r_first = H + 7 >= 8), blocks of 12 steps
+  // (the exits jump straight out of the unrolled block: only dmax is live
+  // after the loop, so the register FIFOs need no fixed registers at them)
   int y = r_first + 1;
-  static_for<0, 7>([&](auto U) {
-    step(U, std::true_type{}, y);
-    ++y;
-  });
-  // steady state: y in [r_first + 8, r_last - 1], blocks of 12 steps
-  for (; y + 11 <= r_last - 1; y += 12) {
-    static_for<7, 19>([&](auto U) { step(U, std::false_type{}, y + (decltype(U)::value - 7)); });
+#define PG_STEP2(U)                               \
+  step(std::integral_constant<int, U>{}, y);      \
+  if (++y > r_last) goto done;
+  while (true) {
+    PG_STEP2(0) PG_STEP2(1) PG_STEP2(2) PG_STEP2(3) PG_STEP2(4) PG_STEP2(5)
+    PG_STEP2(6) PG_STEP2(7) PG_STEP2(8) PG_STEP2(9) PG_STEP2(10) PG_STEP2(11)
   }
-  // tail: up to 12 guarded steps until y = r_last
-  static_for<7, 19>([&](auto U) {
-    if (y <= r_last) step(U, std::true_type{}, y);
-    ++y;
-  });
+#undef PG_STEP2
+done:
 
   if (!exact_lane) dmax = 0.0;
 #pragma unroll

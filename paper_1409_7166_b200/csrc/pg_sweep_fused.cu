@@ -163,6 +163,7 @@ bool fill_fused_params(pg_grid *g, FusedParams &P, double omega, double tol, int
   P.launch_idx = j;
   P.nsw = nsw;
   P.prof = prof_buffer();
+  P.pre = 0;
   const SlabHalo &h = g->hx;
   const bool halo = g->slab && h.G > 0;
   P.has_rlo = halo && h.has_lo;

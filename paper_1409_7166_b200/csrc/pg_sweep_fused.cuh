@@ -83,6 +83,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
   }
 }
+// tx-count only (no arrival): the phase still needs its arrival
+__device__ __forceinline__ void mbar_expect_tx_only(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(bar)) : "memory");
+}
 // box {32 half-columns from c0, both parities, row y, all layers}
 __device__ __forceinline__ void tma4(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int y) {
   asm volatile(
@@ -139,6 +146,7 @@ struct FusedParams {
   CUtensorMap mRlo, mRhi;
   double *send_lo, *send_hi;
   int32_t has_rlo, has_rhi, G;
+  int32_t pre;  // k_rb_sweep2: the previous kernel in the stream is a sweep launch (PDL prologue)
 };
 
 // The constants of one node update: x links (west, east), y links (north,

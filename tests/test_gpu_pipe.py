@@ -97,10 +97,13 @@ def test_pipe_rlc_equals_fused(pgb, L, NY, NX, rows):
     np.testing.assert_allclose(rp.probes, Vo, rtol=0, atol=1e-12)
 
 
-def test_pipe_converged_matches_fused(pgb):
-    # converged transient (tol 1e-10): identical sweep counts and voltages
+@pytest.mark.parametrize("opts", [{"pdl": 1}, {"pdl": 0}, {"pdl": 1, "timing": 1}, {"pdl": 1, "graph": 0},
+                                  {"pdl": 1, "batch": 3}])
+def test_pipe_converged_matches_fused(pgb, opts):
+    # converged transient (tol 1e-10): identical sweep counts and voltages,
+    # with and without programmatic dependent launch, graphs, timing events
     g = mk(4, 48, 96, seed=11)
-    rp = run(pgb, g, 8, 100000, 1.9, {"pipe": 1}, tol=1e-10)
+    rp = run(pgb, g, 8, 100000, 1.9, {"pipe": 1, **opts}, tol=1e-10)
     rf = run(pgb, g, 8, 100000, 1.9, {"pipe": 0}, tol=1e-10)
     assert np.array_equal(rp.sweeps, rf.sweeps)
     assert np.array_equal(rp.probes, rf.probes)
