@@ -133,6 +133,11 @@ PG_API int pg_set_stream(pg_grid *g, void *stream);
  *   "pdl"    1 (default): consecutive sweep launches of a single grid use
  *            programmatic dependent launch (the next launch's prologue and
  *            constant-row loads overlap the previous launch's tail); 0: off
+ *   "l2ahead" rows of L2 prefetch (cp.async.bulk.prefetch) beyond the shared-
+ *            memory ring in the two-level pipeline kernel, 0..16 (default 0:
+ *            measured fastest; the prefetch costs 50 % on the 134M-node mesh)
+ *   "l2promo" L2 promotion of the sweep's TMA loads in bytes: 0, 64, 128,
+ *            256 (default 256)
  *   "graph"  1 (default): replay full batches of sweep launches from a captured
  *            CUDA graph (single grids, option "timing" off); 0: plain launches
  *   "rows"   rows per CTA of the mesh sweep (0: auto)

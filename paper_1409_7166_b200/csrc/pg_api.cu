@@ -331,6 +331,17 @@ PG_API int pg_set_option(pg_grid *g, const char *key, int64_t value) {
     g->pipe = value != 0;
   } else if (k == "pdl") {
     g->pdl = value != 0;
+  } else if (k == "l2ahead") {
+    REQUIRE(value >= 0 && value <= 16, "l2ahead must be in 0..16");
+    g->l2ahead = (int)value;
+  } else if (k == "l2promo") {
+    REQUIRE(value == 0 || value == 64 || value == 128 || value == 256, "l2promo must be 0, 64, 128 or 256");
+    g->l2promo = (int)value;
+    g->tma_state = 0;  // re-encode the tensor maps
+    if (g->slab && g->hx.G > 0 && !encode_halo_maps(g)) {
+      set_error("re-encoding the slab halo tensor maps failed");
+      return PG_ECUDA;
+    }
   } else if (k == "graph") {
     g->use_graph = value != 0;
   } else if (k == "timing") {

@@ -139,6 +139,8 @@ struct pg_grid {
   int use_graph = 1;                   // option "graph": replay captured sweep batches
   int resident = 1;                    // option "resident": one-CTA sweep loop for tiny meshes
   int pipe = 1;                        // option "pipe": two-level pipeline kernel for full F = 2 launches
+  int l2ahead = 0;                     // option "l2ahead": rows of L2 prefetch beyond the ring (k_rb_sweep2; 0: none, measured fastest)
+  int l2promo = 256;                   // option "l2promo": TMA L2 promotion bytes (0, 64, 128, 256)
   int pdl = 1;                         // option "pdl": programmatic dependent launch of consecutive sweeps
   bool pdl_ok = false;                 // set by run_transient: single grid, no exchange between launches
   cudaGraphExec_t batch_exec = nullptr;  // captured batch of `batch` full sweep launches

@@ -104,6 +104,7 @@ cudaError_t launch_rb_sweep2(pg_grid *g, double omega, double tol, int j, int ro
   if (!fill_fused_params(g, P, omega, tol, j, 2, W, rows_per_cta, y_begin, y_end, ypar))
     return cudaErrorNotSupported;
   P.pre = pdl ? 1 : 0;
+  P.l2ahead = g->l2ahead;
   const bool halo = g->slab && g->hx.G > 0;
   const int I = W - 4;
   const dim3 grid((g->md.HP + I - 1) / I, (y_end - y_begin + rows_per_cta - 1) / rows_per_cta);

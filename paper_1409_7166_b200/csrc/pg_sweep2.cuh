@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
   // mid) and their stage offsets are a * LAY (+ RW from gz_eff on), so every
   // copy is the same instruction sequence (small code: it is replicated in
   // each of the 12 unrolled steps).
-  constexpr int kL2Ahead = PG_L2_AHEAD;
+  const int kL2Ahead = P.l2ahead;
   auto v_copy = [&](int rv_row, int r) {  // V row rv_row into its slot, completing group r
     int rv;
     const CUtensorMap *m = v_src(rv_row, rv);

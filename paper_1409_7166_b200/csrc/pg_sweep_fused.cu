@@ -33,7 +33,16 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encoder() {
 
 // 4-D view of a parity-split mesh array: (half-column, parity, row, layer),
 // box {W half-columns, 2 parities, 1 row, L layers}
-bool encode(CUtensorMap *m, const double *base, const MeshDims &d, int W) {
+CUtensorMapL2promotion promo_of(int bytes) {
+  switch (bytes) {
+    case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    case 64: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    case 128: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    default: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }
+}
+
+bool encode(CUtensorMap *m, const double *base, const MeshDims &d, int W, int promo) {
   auto fn = get_encoder();
   if (!fn) return false;
   cuuint64_t dims[4] = {(cuuint64_t)d.HP, 2, (cuuint64_t)d.NY, (cuuint64_t)d.L};
@@ -42,13 +51,13 @@ bool encode(CUtensorMap *m, const double *base, const MeshDims &d, int W) {
   cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double *>(base), dims, strides, box, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  promo_of(promo), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
 
 // 4-D view of a slab's ghost-row receive buffer: [L][G][NXP] parity-split rows
-bool encode_rows(CUtensorMap *m, const double *base, const MeshDims &d, int G, int W) {
+bool encode_rows(CUtensorMap *m, const double *base, const MeshDims &d, int G, int W, int promo) {
   auto fn = get_encoder();
   if (!fn) return false;
   cuuint64_t dims[4] = {(cuuint64_t)d.HP, 2, (cuuint64_t)G, (cuuint64_t)d.L};
@@ -57,7 +66,7 @@ bool encode_rows(CUtensorMap *m, const double *base, const MeshDims &d, int G, i
   cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double *>(base), dims, strides, box, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  promo_of(promo), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
@@ -67,8 +76,8 @@ bool encode_halo_maps(pg_grid *g) {
   SlabHalo &h = g->hx;
   bool ok = true;
   for (int w = 0; w < 2; ++w) {
-    if (h.has_lo) ok = ok && encode_rows(&h.mlo[w], h.recv_lo, g->md, h.G, w ? 64 : 32);
-    if (h.has_hi) ok = ok && encode_rows(&h.mhi[w], h.recv_hi, g->md, h.G, w ? 64 : 32);
+    if (h.has_lo) ok = ok && encode_rows(&h.mlo[w], h.recv_lo, g->md, h.G, w ? 64 : 32, g->l2promo);
+    if (h.has_hi) ok = ok && encode_rows(&h.mhi[w], h.recv_hi, g->md, h.G, w ? 64 : 32, g->l2promo);
   }
   return ok;
 }
@@ -97,7 +106,7 @@ bool tma_available(pg_grid *g) {
     const double *bufs[7] = {g->V[0], g->V[1], g->gx, g->gy, g->gze, g->b, g->invd};
     bool ok = get_encoder() != nullptr;
     for (int w = 0; w < 2; ++w)
-      for (int k = 0; ok && k < 7; ++k) ok = encode(&g->tmap[w][k], bufs[k], g->md, w ? 64 : 32);
+      for (int k = 0; ok && k < 7; ++k) ok = encode(&g->tmap[w][k], bufs[k], g->md, w ? 64 : 32, g->l2promo);
     if (ok) g->tma_state = 1;
   }
   return g->tma_state == 1;

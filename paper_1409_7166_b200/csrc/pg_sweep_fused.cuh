@@ -146,7 +146,8 @@ struct FusedParams {
   CUtensorMap mRlo, mRhi;
   double *send_lo, *send_hi;
   int32_t has_rlo, has_rhi, G;
-  int32_t pre;  // k_rb_sweep2: the previous kernel in the stream is a sweep launch (PDL prologue)
+  int32_t pre;      // k_rb_sweep2: the previous kernel in the stream is a sweep launch (PDL prologue)
+  int32_t l2ahead;  // k_rb_sweep2: rows of L2 prefetch beyond the ring (0: none)
 };
 
 // The constants of one node update: x links (west, east), y links (north,
