@@ -670,7 +670,7 @@ int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, d
   Ev evguard{evs};
 
   int64_t launches = 0;
-  const bool graph_ok = g->use_graph && ng == 1 && ex == nullptr && !g->timing;
+  const bool graph_ok = g->use_graph && ng == 1 && ex == nullptr;
   // consecutive sweep launches of a single grid may overlap (PDL): launch
   // j > 0 of a batch directly follows launch j - 1 in the stream
   for (int k = 0; k < ng; ++k) gs[k]->pdl_ok = false;
@@ -713,19 +713,15 @@ int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, d
       CK(launch_rhs(gs[k], h, dc ? t_dc : (double)s * h));
       launches += 1 + (gs[k]->npad > 0) + (gs[k]->nsrc > 0);
     }
+    // option "timing": an event pair around the step's sweep launches (read
+    // after the run, so timing adds no synchronisation and keeps the graphs)
+    if (g->timing && !tev(2 * (s - 1) + 1)) return cuda_fail(cudaErrorMemoryAllocation, "timing events");
     if (resident) {
       // the whole sweep loop of the step in one launch (small meshes)
-      if (g->timing) CK(cudaEventRecord(tev(0), st));
+      if (g->timing) CK(cudaEventRecord(tev(2 * (s - 1)), st));
       CK(launch_rb_resident(g, omega, tol, max_sweeps, s));
       ++launches;
-      if (g->timing) {
-        CK(cudaEventRecord(tev(1), st));
-        CK(cudaEventSynchronize(tev(1)));
-        float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, tev(0), tev(1)));
-        sweep_ms += ms;
-        ++sweep_launches;
-      }
+      if (g->timing) CK(cudaEventRecord(tev(2 * (s - 1) + 1), st));
       if (g->rlc) {
         CK(launch_inductor_update(g, h));
         launches += 2;
@@ -739,7 +735,7 @@ int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, d
     int64_t j = 0;
     int pending = -1;  // poll slot of the previous batch
     int slot = 0;
-    if (g->timing) CK(cudaEventRecord(tev(0), st));
+    if (g->timing) CK(cudaEventRecord(tev(2 * (s - 1)), st));
     while (j < max_launch) {
       const int64_t nb = std::min<int64_t>(g->batch, max_launch - j);
       // a full batch (batch launches of F sweeps) of a single grid replays the
@@ -754,7 +750,6 @@ int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, d
           const int nsw = (int)std::min<int64_t>(F, max_sweeps - (j + b) * F);
           for (int k = 0; k < ng; ++k) CK(launch_sweep(gs[k], method, omega, tol, (int)b, nsw, &launches));
           if (ex) CK(ex->after_sweep((int)(j + b), (int)b, &launches));
-          if (g->timing) CK(cudaEventRecord(tev(j + b + 1), st));
         }
         for (int k = 0; k < ng; ++k) CK(launch_batch_advance(gs[k], (int)nb));
         launches += ng;
@@ -770,22 +765,11 @@ int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, d
       pending = slot;
       slot ^= 1;
     }
+    if (g->timing) CK(cudaEventRecord(tev(2 * (s - 1) + 1), st));
     if (ex) CK(ex->end_step(&launches));
     for (int k = 0; k < ng; ++k) {
       CK(launch_step_end(gs[k], s, (int)j, flips, F, max_sweeps, tol));
       ++launches;
-    }
-    if (g->timing) {
-      CK(cudaMemcpyAsync(g->ctl_host, g->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      // launches that did work: all queued ones unless convergence was detected earlier
-      const int64_t ran = g->ctl_host->done ? g->ctl_host->launches_done : j;
-      if (ran > 0) {
-        float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, tev(0), tev(ran)));
-        sweep_ms += ms;
-        sweep_launches += ran;
-      }
     }
     for (int k = 0; k < ng; ++k) {
       if (gs[k]->rlc) {
@@ -806,9 +790,25 @@ int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, d
     CK(cudaMemcpyAsync(probe_out, d_pout, sizeof(double) * (steps + 1) * n_probe, cudaMemcpyDeviceToHost, st));
   if (sweeps_out)
     CK(cudaMemcpyAsync(sweeps_out, g->dev_sweeps, sizeof(int64_t) * (steps + 1), cudaMemcpyDeviceToHost, st));
+  std::vector<int64_t> step_sweeps;
+  if (g->timing) {
+    step_sweeps.resize(steps + 1);
+    CK(cudaMemcpyAsync(step_sweeps.data(), g->dev_sweeps, sizeof(int64_t) * (steps + 1), cudaMemcpyDeviceToHost,
+                       st));
+  }
   CK(cudaStreamSynchronize(st));
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, ev0, ev1));
+  if (g->timing) {
+    // sweep-phase time of every step; launches that did work = ceil(sweeps / F)
+    // (the resident sweep: one launch per step)
+    for (int64_t s = 1; s <= steps; ++s) {
+      float m = 0.f;
+      CK(cudaEventElapsedTime(&m, tev(2 * (s - 1)), tev(2 * (s - 1) + 1)));
+      sweep_ms += m;
+      sweep_launches += resident ? 1 : (step_sweeps[s] + F - 1) / F;
+    }
+  }
   const DevCtl &c = *g->ctl_host;
   if (stats) {
     stats->steps_done = steps;

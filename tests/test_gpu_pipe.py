@@ -107,3 +107,19 @@ def test_pipe_converged_matches_fused(pgb, opts):
     rf = run(pgb, g, 8, 100000, 1.9, {"pipe": 0}, tol=1e-10)
     assert np.array_equal(rp.sweeps, rf.sweeps)
     assert np.array_equal(rp.probes, rf.probes)
+
+
+def test_timing_option_accounts_sweep_launches(pgb):
+    # option "timing": per-step event pairs around the sweep launches; the
+    # launches that did work are ceil(sweeps / F) per step, the sweep time is
+    # part of the device time
+    g = mk(4, 48, 96, seed=5)
+    G = pgb.Grid.from_mesh_grid(g, device=True)
+    G.set_option("resident", 0)
+    G.set_option("timing", 1)
+    r = G.transient(g.h, 6, tol=1e-10, omega=1.9, max_sweeps=100000)
+    G.close()
+    F = int(r.stats.sweeps_per_launch)
+    assert F == 2
+    assert int(r.stats.sweep_launches) == int(sum((s + F - 1) // F for s in r.sweeps[1:]))
+    assert 0.0 < float(r.stats.sweep_ms) <= float(r.stats.device_ms)
