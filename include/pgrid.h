@@ -136,6 +136,14 @@ PG_API int pg_set_stream(pg_grid *g, void *stream);
  *   "l2ahead" rows of L2 prefetch (cp.async.bulk.prefetch) beyond the shared-
  *            memory ring in the two-level pipeline kernel, 0..16 (default 0:
  *            measured fastest; the prefetch costs 50 % on the 134M-node mesh)
+ *   "l2keep" / "l2first" L2 eviction policy of the pipeline kernel, 6-bit
+ *            masks over (gx, gy, gz_eff, b, 1/d, V): l2keep bits 0-4 read that
+ *            constant array with evict_last, bit 5 writes V with evict_last;
+ *            l2first reads the arrays (bit 5: V) with evict_first; others
+ *            evict_normal.  -1 (default, auto): meshes with a per-launch
+ *            footprint (56 B per element) below twice the L2 use l2keep = 32,
+ *            l2first = 63 (stream the reads, keep the freshly written V for
+ *            the next launch), larger meshes 0 / 0
  *   "l2promo" L2 promotion of the sweep's TMA loads in bytes: 0, 64, 128,
  *            256 (default 256)
  *   "graph"  1 (default): replay full batches of sweep launches from a captured

@@ -334,6 +334,19 @@ PG_API int pg_set_option(pg_grid *g, const char *key, int64_t value) {
   } else if (k == "l2ahead") {
     REQUIRE(value >= 0 && value <= 16, "l2ahead must be in 0..16");
     g->l2ahead = (int)value;
+  } else if (k == "l2keep") {
+    REQUIRE(value >= -1 && value < 64, "l2keep is a 6-bit mask (gx, gy, gz, b, 1/d, V) or -1 (auto)");
+    g->l2keep = (int)value;
+    if (value > 0 && (value & 31)) {
+      // evict_last lines may only occupy the persisting L2 set-aside
+      cudaDeviceProp prop;
+      if (cudaGetDeviceProperties(&prop, g->dev) == cudaSuccess && prop.persistingL2CacheMaxSize > 0)
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)prop.persistingL2CacheMaxSize);
+      cudaGetLastError();
+    }
+  } else if (k == "l2first") {
+    REQUIRE(value >= -1 && value < 64, "l2first is a 6-bit mask (gx, gy, gz, b, 1/d, V) or -1 (auto)");
+    g->l2first = (int)value;
   } else if (k == "l2promo") {
     REQUIRE(value == 0 || value == 64 || value == 128 || value == 256, "l2promo must be 0, 64, 128 or 256");
     g->l2promo = (int)value;

@@ -123,12 +123,25 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
   // control block are read only after griddepcontrol.wait.  (Without the
   // launch attribute the wait is a no-op.)
   const CUtensorMap *mC = &P.mgx;
+  // L2 eviction policy per array (options "l2keep" / "l2first", auto by
+  // footprint, pg_sweep2.cu): evict_last / evict_first hints on the TMA
+  // copies; policy 0 = plain copy without a cache hint (measured faster than
+  // an explicit evict_normal hint on config 4)
+  const uint64_t pol_last = policy_evict_last(), pol_first = policy_evict_first();
+  auto pol = [&](int a) -> uint64_t {
+    return (a < 5 && ((P.l2keep >> a) & 1)) ? pol_last : (((P.l2first >> a) & 1) ? pol_first : 0ull);
+  };
+  auto tma = [&](void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int y, uint64_t p) {
+    if (p) tma4h(dst, map, bar, c0, y, p);
+    else tma4(dst, map, bar, c0, y);
+  };
+
   auto c_dst = [&](int r, int a) { return cring + ((r - r_first) % SC) * CST + a * Gm::LAY + (a >= 2 ? RW : 0); };
   auto c_bar = [&](int r) { return &gbar[(r - r_first) % SC]; };
   if (P.pre && tid == 0) {
     for (int r = r_first; r < r_first + n_init; ++r) {
       mbar_expect_tx_only(c_bar(r), Gm::CBYTES);
-      for (int a = 0; a < 5; ++a) tma4(c_dst(r, a), mC + a, c_bar(r), ps, r);
+      for (int a = 0; a < 5; ++a) tma(c_dst(r, a), mC + a, c_bar(r), ps, r, pol(a));
     }
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -185,7 +198,7 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
   auto v_copy = [&](int rv_row, int r) {  // V row rv_row into its slot, completing group r
     int rv;
     const CUtensorMap *m = v_src(rv_row, rv);
-    tma4(vring + ((rv_row - r_first) % SV) * VST, m, c_bar(r), ps, rv);
+    tma(vring + ((rv_row - r_first) % SV) * VST, m, c_bar(r), ps, rv, pol(5));
   };
   auto v_prefetch = [&](int rv_row) {
     int rv;
@@ -198,7 +211,7 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
       const uint32_t vbytes = (v1 ? Gm::VBYTES : 0u) + (v0 ? Gm::VBYTES : 0u);
       mbar_expect_tx(c_bar(r), vbytes + (P.pre ? 0u : Gm::CBYTES));
       if (!P.pre)
-        for (int a = 0; a < 5; ++a) tma4(c_dst(r, a), mC + a, c_bar(r), ps, r);
+        for (int a = 0; a < 5; ++a) tma(c_dst(r, a), mC + a, c_bar(r), ps, r, pol(a));
       if (v1) v_copy(r + 1, r);
       if (v0) v_copy(r, r);
     }
@@ -224,12 +237,12 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
       for (int op = warp; op < 7; op += Gm::NWARP) {
         if (op < 5) {
           if (op == 0) mbar_expect_tx(bar, Gm::CBYTES + (R + 1 <= r_last ? Gm::VBYTES : 0u));
-          tma4(cdst + op * Gm::LAY + (op >= 2 ? RW : 0), mC + op, bar, ps, R);
+          tma(cdst + op * Gm::LAY + (op >= 2 ? RW : 0), mC + op, bar, ps, R, pol(op));
         } else if (op == 5) {
           if (R + 1 <= r_last) {
             int rv;
             const CUtensorMap *m = v_src(R + 1, rv);
-            tma4(vring + vs * VST, m, bar, ps, rv);
+            tma(vring + vs * VST, m, bar, ps, rv, pol(5));
           }
         } else if (kL2Ahead > 0 && R + kL2Ahead <= r_last) {
 #pragma unroll 1
@@ -270,29 +283,33 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
     cB[k] = NodeC{0, 0, 0, 0, 0, 0, 0, 0};
   }
 
-  // One streaming step (u: position modulo 12).  Every step runs the same
-  // unguarded body, also the first and last ones: the updates of rows outside
-  // (r_first, r_last) and of the stale halo rows only read ring slots that are
-  // loaded or hold finite leftovers (never an exact row's operand: an exact
-  // row's level-1 value depends on old values of rows r - 4 .. r + 4 only, all
-  // in [r_first, r_last], and on intermediate values inside that cone), and
-  // their stores go to slots whose next TMA refill is ordered after them by
-  // the per-step proxy fence.  Only the norm and the write-out are masked.
-  auto step = [&](auto U_, const int y) {
-    constexpr int u = decltype(U_)::value;
+  // Streaming step y (u: position modulo 12) = phase A(y) | barrier | phase
+  // B(y).  Phase B(y) and phase A(y + 1) touch no value of another warp that
+  // the other writes (header), so the loop body is barrier(y), refill, wait for
+  // row group y + 1, then B(y) and A(y + 1) in one branch-free block: the
+  // compiler interleaves their four independent update chains.  Every step
+  // runs the same unguarded code, also the first and last ones: the updates
+  // of rows outside (r_first, r_last) and of the stale halo rows only read
+  // ring slots that are loaded or hold finite leftovers (never an exact row's
+  // operand: an exact row's level-1 value depends on old values of rows
+  // r - 4 .. r + 4 only, all in [r_first, r_last], and on intermediate values
+  // inside that cone), and their stores go to slots whose next TMA refill is
+  // ordered after them by the per-step proxy fence.  Only the norm and the
+  // write-out are masked.  A(r_last + 1) runs without its (never issued) row
+  // group and its results are discarded.
+  double aR0 = 0.0, aR1 = 0.0, aVN = 0.0, aGyN = 0.0;  // phase A results phase B needs
+  auto phaseA = [&](auto U_, const int y) {
+    constexpr int u = decltype(U_)::value % 12;
     constexpr int k = u & 1;
     constexpr int f0 = u % 3, f1 = (u + 2) % 3, f2 = (u + 1) % 3;  // FIFO: now / 1 / 2 (3 = f0) steps ago
     // ring slots: V row y + d -> (u + 1 + d) mod SV, constant row y + d -> (u + 1 + d) mod SC
-    constexpr int vY = ((u + 1) % SV) * VST, vY1 = ((u + 2) % SV) * VST, vYm = (u % SV) * VST;
-    constexpr int vY3 = ((u + SV - 2) % SV) * VST, vY4 = ((u + SV - 3) % SV) * VST;
+    constexpr int vY = ((u + 1) % SV) * VST, vY1 = ((u + 2) % SV) * VST;
+    constexpr int vY3 = ((u + SV - 2) % SV) * VST;
     constexpr int cY = ((u + 1) % SC) * CST, cYm = (u % SC) * CST;
     const int me = k ? ME1 : ME0, mo = k ? ME0 : ME1;
     const int ot = k ? OT1 : OT0, ot3 = k ? OT0 : OT1;
     const int gxo = k ? GX1 : GX0;
-
-    mbar_wait(&gbar[(u + 1) % SC], (uint32_t)(((u + 1) / SC) & 1));
-
-    // ---------------------------------------------------------- phase A
+    (void)f2;
     // red_0(y): column class k; its north operand (old black of row y - 1) was
     // loaded as the previous step's own-pair operand
     const double Vc = vring[vY + me];
@@ -312,44 +329,65 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
     // red_1(y - 3): column class k ^ 1 (= mo); own value red_0(y - 3), x
     // neighbour black_0(y - 3), north / south black_0(y - 4) / black_0(y - 2)
     const double Vc1 = fR0[f0];
-    const double r1 = upd_c(cR[f0], w, Vc1, fB0[f2], vring[vY3 + ot3], fB0[f0], fB0[f1], vring[vY3 + mo + RW],
-                            vring[vY3 + mo - RW]);
+    const double r1 = upd_c(cR[f0], w, Vc1, fB0[(u + 1) % 3], vring[vY3 + ot3], fB0[f0], fB0[f1],
+                            vring[vY3 + mo + RW], vring[vY3 + mo - RW]);
     vring[vY + me] = r0;
     vring[vY3 + mo] = r1;
     double dA = fabs(r1 - Vc1);
     if (!(y >= ys + 3 && y < r_last)) dA = 0.0;  // norm over rows [ys, ye) only
-    fence_proxy_async();
-    __syncthreads();
-    refill(y, (u + 5) % SC, (u + 6) % SV);
-
-    // ---------------------------------------------------------- phase B
+    dmax = dA > dmax ? dA : dmax;
+    fR0[f0] = r0;
+    fR1[f0] = r1;
+    fWn[f0] = Vown;
+    cR[f0] = c0;
+    aR0 = r0;
+    aR1 = r1;
+    aVN = VN;
+    aGyN = c0.gyN;
+  };
+  auto phaseB = [&](auto U_, const int y) {
+    constexpr int u = decltype(U_)::value % 12;
+    constexpr int k = u & 1;
+    constexpr int f0 = u % 3, f1 = (u + 2) % 3, f2 = (u + 1) % 3;
+    constexpr int vYm = (u % SV) * VST, vY4 = ((u + SV - 3) % SV) * VST;
+    constexpr int cYm = (u % SC) * CST;
+    const int me = k ? ME1 : ME0, mo = k ? ME0 : ME1;
+    const int ot = k ? OT1 : OT0, ot3 = k ? OT0 : OT1;
+    const int gxo = k ? GX1 : GX0;
+    (void)mo;
     // black_0(y - 1): column class k (its old value is red_0(y)'s north operand)
     NodeC cb;
     cb.gxOwn = cring[cYm + CGX + pe];
     cb.gxOth = cring[cYm + CGX + gxo];
     cb.gyN = cR[f2].gyS;  // gy of row y - 2 in this column: red_0(y - 2)'s own south link
-    cb.gyS = c0.gyN;
+    cb.gyS = aGyN;
     cb.gzU = cring[cYm + CGZ + me];
     cb.gzD = cring[cYm + CGZ + me - RW];
     cb.b = cring[cYm + CB + me];
     cb.id = cring[cYm + CID + me];
-    const double b0 = upd_c(cb, w, VN, fR0[f1], vring[vYm + ot], fR0[f2], r0, vring[vYm + me + RW],
+    const double b0 = upd_c(cb, w, aVN, fR0[f1], vring[vYm + ot], fR0[f2], aR0, vring[vYm + me + RW],
                             vring[vYm + me - RW]);
     // black_1(y - 4): column class k ^ 1; own value black_0(y - 4), x neighbour
     // red_1(y - 4), north / south red_1(y - 5) / red_1(y - 3)
     const double Vcb1 = fB0[f0];
     const double Vownb1 = fR1[f1];
-    const double b1 = upd_c(cB[f0], w, Vcb1, Vownb1, vring[vY4 + ot3], fR1[f2], r1, vring[vY4 + mo + RW],
+    const double b1 = upd_c(cB[f0], w, Vcb1, Vownb1, vring[vY4 + ot3], fR1[f2], aR1, vring[vY4 + mo + RW],
                             vring[vY4 + mo - RW]);
     vring[vYm + me] = b0;
     const bool out = y >= ys + 4;  // row y - 4 owned (y - 4 < ye always)
     double dB = fabs(b1 - Vcb1);
     if (!out) dB = 0.0;
+    dmax = dB > dmax ? dB : dmax;
     // row y - 4 is final: red_1 (class k) and black_1 (class k ^ 1)
     if (out && exact_lane) {
       const int64_t ro = (int64_t)(y - 4) * P.NXP;
-      (k ? OUT1 : OUT0)[ro] = Vownb1;
-      (k ? OUT0 : OUT1)[ro] = b1;
+      if (P.l2keep & 32) {  // the next launch reads this V buffer: keep it in L2
+        stg_hint((k ? OUT1 : OUT0) + ro, Vownb1, pol_last);
+        stg_hint((k ? OUT0 : OUT1) + ro, b1, pol_last);
+      } else {
+        (k ? OUT1 : OUT0)[ro] = Vownb1;
+        (k ? OUT0 : OUT1)[ro] = b1;
+      }
       if constexpr (SLAB) {
         const int rr = y - 4;
         const bool red_odd = (q ^ k) != 0;
@@ -366,25 +404,33 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
         }
       }
     }
-    dA = dA > dB ? dA : dB;
-    dmax = dA > dmax ? dA : dmax;
-    fR0[f0] = r0;
     fB0[f0] = b0;
-    fR1[f0] = r1;
-    fWn[f0] = Vown;
-    cR[f0] = c0;
     cB[f0] = cb;
   };
+  // loop body of step y: barrier, refill, wait for row group y + 1, B(y) + A(y + 1)
+  auto body = [&](auto U_, const int y) {
+    constexpr int u = decltype(U_)::value;
+    __syncthreads();
+    refill(y, (u + 5) % SC, (u + 6) % SV);
+    if (y + 1 <= r_last) mbar_wait(&gbar[(u + 2) % SC], (uint32_t)(((u + 2) / SC) & 1));
+    phaseB(U_, y);
+    phaseA(std::integral_constant<int, u + 1>{}, y + 1);
+    fence_proxy_async();
+  };
 
-  // the first step's north operand: old black of row r_first in the column of red(r_first + 1)
+  // the first step's north operand: old black of row r_first in the column of
+  // red(r_first + 1), then phase A of the first step
   mbar_wait(&gbar[0], 0u);
   fWn[2] = vring[ME0];
-  // y = r_first + 1 .. r_last (r_last - r_first = H + 7 >= 8), blocks of 12 steps
-  // (the exits jump straight out of the unrolled block: only dmax is live
-  // after the loop, so the register FIFOs need no fixed registers at them)
+  mbar_wait(&gbar[1], 0u);
+  phaseA(std::integral_constant<int, 0>{}, r_first + 1);
+  fence_proxy_async();
+  // y = r_first + 1 .. r_last (r_last - r_first = H + 7 >= 8), blocks of 12
+  // steps (the exits jump straight out of the unrolled block: only dmax is
+  // live after the loop, so the register FIFOs need no fixed registers there)
   int y = r_first + 1;
-#define PG_STEP2(U)                               \
-  step(std::integral_constant<int, U>{}, y);      \
+#define PG_STEP2(U)                                  \
+  body(std::integral_constant<int, U>{}, y);         \
   if (++y > r_last) goto done;
   while (true) {
     PG_STEP2(0) PG_STEP2(1) PG_STEP2(2) PG_STEP2(3) PG_STEP2(4) PG_STEP2(5)
@@ -392,7 +438,6 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
   }
 #undef PG_STEP2
 done:
-
   if (!exact_lane) dmax = 0.0;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));

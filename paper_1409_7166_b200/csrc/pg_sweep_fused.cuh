@@ -98,6 +98,33 @@ __device__ __forceinline__ void tma4(void *dst, const CUtensorMap *map, uint64_t
       "l"(reinterpret_cast<uint64_t>(map)), "r"(su32(bar)), "r"(c0), "r"(0), "r"(y), "r"(0)
       : "memory");
 }
+// the same box with an L2 cache-eviction policy (createpolicy)
+__device__ __forceinline__ void tma4h(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int y,
+                                      uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(su32(bar)), "r"(c0), "r"(0), "r"(y), "r"(0), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void stg_hint(double *p, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
 // L2 prefetch of the same box (no shared memory, no completion): rows beyond
 // the ring are pulled into L2 early so the ring's TMA loads see L2 latency
 __device__ __forceinline__ void tma4_prefetch(const CUtensorMap *map, int c0, int y) {
@@ -148,6 +175,9 @@ struct FusedParams {
   int32_t has_rlo, has_rhi, G;
   int32_t pre;      // k_rb_sweep2: the previous kernel in the stream is a sweep launch (PDL prologue)
   int32_t l2ahead;  // k_rb_sweep2: rows of L2 prefetch beyond the ring (0: none)
+  int32_t l2keep;   // k_rb_sweep2: bit a < 5: constant array a (gx, gy, gz_eff, b, 1/d) read with L2 evict_last;
+                    // bit 5: V written with evict_last (the next launch reads it)
+  int32_t l2first;  // k_rb_sweep2: arrays read with evict_first (bits as above, bit 5: V reads); others evict_normal
 };
 
 // The constants of one node update: x links (west, east), y links (north,
