@@ -200,15 +200,25 @@ PG_API int pg_create_mesh(int32_t layers, int32_t ny, int32_t nx, const double *
   REQUIRE(std::isfinite(vdd), "vdd must be finite");
   const int64_t n = (int64_t)layers * ny * nx;
   if (mem == PG_MEM_HOST) {  // value checks (device inputs are trusted)
-    for (int64_t k = 0; k < n; ++k) {
-      const int64_t x = k % nx, y = (k / nx) % ny, l = k / ((int64_t)nx * ny);
-      REQUIRE(gx[k] >= 0 && gy[k] >= 0 && gz[k] >= 0 && cap[k] >= 0 && std::isfinite(cap[k]),
-              "conductances and capacitances must be >= 0");
-      REQUIRE(x < nx - 1 || gx[k] == 0.0, "gx must be 0 in the last column");
-      REQUIRE(y < ny - 1 || gy[k] == 0.0, "gy must be 0 in the last row");
-      REQUIRE(l < layers - 1 || gz[k] == 0.0, "gz must be 0 in the top layer");
-      if (lz) REQUIRE(lz[k] >= 0.0 && std::isfinite(lz[k]), "lz must be finite and >= 0");
-    }
+    bool ok_val = true, ok_x = true, ok_y = true, ok_z = true, ok_l = true;
+    int64_t k = 0;
+    for (int32_t l = 0; l < layers; ++l)
+      for (int32_t y = 0; y < ny; ++y) {
+        for (int32_t x = 0; x < nx; ++x, ++k)
+          ok_val &= gx[k] >= 0 && gy[k] >= 0 && gz[k] >= 0 && cap[k] >= 0 && std::isfinite(cap[k]);
+        ok_x &= gx[k - 1] == 0.0;
+        if (y == ny - 1)
+          for (int32_t x = 0; x < nx; ++x) ok_y &= gy[k - nx + x] == 0.0;
+        if (l == layers - 1)
+          for (int32_t x = 0; x < nx; ++x) ok_z &= gz[k - nx + x] == 0.0;
+      }
+    if (lz)
+      for (int64_t q = 0; q < n; ++q) ok_l &= lz[q] >= 0.0 && std::isfinite(lz[q]);
+    REQUIRE(ok_val, "conductances and capacitances must be >= 0");
+    REQUIRE(ok_x, "gx must be 0 in the last column");
+    REQUIRE(ok_y, "gy must be 0 in the last row");
+    REQUIRE(ok_z, "gz must be 0 in the top layer");
+    REQUIRE(ok_l, "lz must be finite and >= 0");
   }
   pg_grid *g = new pg_grid();
   GridGuard guard{g};
@@ -426,9 +436,15 @@ PG_API int pg_set_sources(pg_grid *g, int64_t n_src, const int64_t *node, const 
   }
   std::vector<int64_t> sidx((size_t)n_src);
   for (int64_t k = 0; k < n_src; ++k) sidx[k] = storage_index(g, nd[k], &iperm_h);
+  // sources in storage order (ties: input order, so per-node sums are
+  // deterministic); (key, position) pairs sort faster than an indirect stable sort
   std::vector<int64_t> order((size_t)n_src);
-  std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return sidx[a] < sidx[b]; });
+  {
+    std::vector<std::pair<int64_t, int64_t>> kp((size_t)n_src);
+    for (int64_t k = 0; k < n_src; ++k) kp[k] = {sidx[k], k};
+    if (!std::is_sorted(kp.begin(), kp.end())) std::sort(kp.begin(), kp.end());
+    for (int64_t k = 0; k < n_src; ++k) order[k] = kp[k].second;
+  }
   std::vector<int64_t> s2(n_src), p2(n_src + 1);
   std::vector<double> t2((size_t)npts), i2((size_t)npts);
   int64_t off = 0;
