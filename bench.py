@@ -333,6 +333,11 @@ def run_b200(args):
         launch_nodes = sum(q.info()["layers"] * q.info()["ny"] * q.info()["nx"] for q in grids)
         bytes_per_launch = BYTES_PER_NODE_PASS * launch_nodes
         kname = "k_rb_sweep2" if F == 2 and int(opts.get("pipe", 1)) else "k_rb_sweep_fused"
+        if grp is None and sweep_launches == args.steps * T and sweeps > sweep_launches:
+            # cluster-resident sweep (small meshes): one launch runs all sweeps of a
+            # time step with V and the constants in shared memory, HBM once per step
+            kname = "k_rb_cluster"
+            F = sweeps / max(sweep_launches, 1)
     else:
         # CSR sweep (one launch per colour per sweep): rowptr 8 + b 8 + 1/d 8 +
         # V read + write 16 per row, column index 4 + value 8 per entry
@@ -353,6 +358,10 @@ def run_b200(args):
                       "sweep launches (graph batches, programmatic dependent launch; includes the batch "
                       "bookkeeping kernel and queued launches that exit after convergence) / launches "
                       "that did work, inside the timed region"}
+    if kname == "k_rb_cluster":
+        roof["note"] = ("cluster-resident kernel: all sweeps of a time step in one launch with V and the "
+                        "node constants in distributed shared memory; HBM is read once per time step, the "
+                        "sweep rate is bound by cluster-barrier latency, not by HBM (DESIGN.md section 7)")
 
     # e2e: public C-ABI call with host buffers (pinned), copies inside the timed region
     e2e = None
