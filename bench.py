@@ -57,6 +57,9 @@ def parse():
                     help="N = 1 only: split the mesh into this many row slabs advanced by the "
                          "single-process group (pg_group_local): the multi-GPU protocol's "
                          "exchange cost measured on one GPU")
+    ap.add_argument("--transport", default=None, choices=["nccl", "copy", "p2p"],
+                    help="slab exchange: nccl (N > 1 default), copy (--slabs default), or p2p: "
+                         "fused into the sweep kernel over peer memory (CUDA IPC for N > 1)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="N > 1: weak = config rows x N (fixed work per GPU), strong = config split")
     ap.add_argument("--opt", action="append", default=[],
@@ -234,15 +237,25 @@ def run_b200(args):
     stream = torch.cuda.current_stream()
     opts = dict(kv.split("=", 1) for kv in args.opt)
     fuse = int(opts.get("fuse", 2))
+    p2p = args.transport == "p2p"
+    iopts = {k: int(v) for k, v in opts.items()}
+
+    def make_group(device=True):
+        # slab partition over the ranks, exchange after every sweep launch
+        # inside the library (pg_group_transient): NCCL halo send/recv + norm
+        # allreduce, or the peer-memory exchange fused into the sweep kernel
+        if p2p:
+            return P.SlabGroup.p2p(g, rank, world, fuse=fuse, stream=stream, device=device, options=iopts)
+        return P.SlabGroup.nccl(g, rank, world, fuse=fuse, stream=stream, device=device)
+
     if world > 1:
-        # slab partition over the ranks: NCCL halo exchange + norm allreduce
-        # after every sweep launch inside the library (pg_group_transient)
-        grp = P.SlabGroup.nccl(g, rank, world, fuse=fuse, stream=stream)
+        grp = make_group()
         G = grp.grids[0]
         sp = grp.specs[0]
         my_nodes = g.layers * (sp.y1 - sp.y0) * g.nx
     elif args.slabs > 1:
-        grp = P.SlabGroup.local(g, args.slabs, fuse=fuse, stream=stream)
+        grp = P.SlabGroup.local(g, args.slabs, fuse=fuse, stream=stream, transport="p2p" if p2p else "copy",
+                                options=iopts if p2p else None)
         G = grp.grids[0]
         my_nodes = g.n
     else:
@@ -376,9 +389,10 @@ def run_b200(args):
         nrep = max(1, min(args.steps, 2))
         h2d = d2h = 0
         for _ in range(nrep):
-            H = P.SlabGroup.nccl(g, rank, world, fuse=fuse, stream=stream, device=False)
-            for k, v in opts.items():
-                H.grids[0].set_option(k, int(v))
+            H = make_group(device=False)
+            if not p2p:
+                for k, v in opts.items():
+                    H.grids[0].set_option(k, int(v))
             rr = H.transient(g.h, T, tol=tol, omega=omega, max_sweeps=200000)
             Vo = H.owned_voltages(g)
             sm = H.specs[0]
@@ -460,9 +474,14 @@ def run_b200(args):
                        "sweeps_per_time_step_mean": float(spt.mean()),
                        "sweeps_per_time_step_max": int(spt.max()),
                        "l2": "per-sweep working set ~56 B/node x n > 126 MB L2 (no flush needed)",
-                       "parallelism": (f"slab{world}: rows split over {world} GPUs, NCCL ghost-row "
-                                       f"exchange + norm allreduce per sweep launch") if world > 1
-                       else (f"1 GPU, {args.slabs} row slabs exchanged in one process (pg_group_local)"
+                       "parallelism": (f"slab{world}: rows split over {world} GPUs, "
+                                       + ("ghost rows and norm exchanged by the sweep kernel over peer "
+                                          "memory (CUDA IPC)" if p2p else
+                                          "NCCL ghost-row exchange + norm allreduce per sweep launch"))
+                       if world > 1
+                       else (f"1 GPU, {args.slabs} row slabs exchanged in one process ("
+                             + ("pg_group_local_p2p: peer-memory exchange in the sweep kernel"
+                                if p2p else "pg_group_local: copies") + ")"
                              if args.slabs > 1 else "1 GPU")},
             "clocks": ck, "e2e": e2e, "gpu_launches": launches, "roofline": roof,
             "cpu_baseline": cpu,

@@ -235,6 +235,27 @@ PG_API int pg_group_local(int32_t n, pg_grid *const *slabs, int32_t ghost, pg_gr
  * equal the single-grid iterates.  Arguments as pg_transient (no probes;
  * voltages via pg_get_voltages on each slab, owned rows); sweeps_out / stats
  * describe this process's first slab (identical on all ranks).  Collective.  */
+/* Peer-memory slab exchange: the sweep kernel of every slab
+ * stores its boundary rows straight into the neighbours' receive buffers
+ * (double-buffered by launch epoch), max-reduces its convergence norm into
+ * every slab's norm ring with remote atomics and bumps every slab's arrival
+ * counter; the next launch waits on its local counter -- no separate
+ * collective per launch.  Needs the two-sweep pipeline kernel for every launch
+ * (options fuse = 0 / 2, pipe = 1; max_sweeps even) and ghost >= 4; at most
+ * 8 slabs.  All slabs must run the same transients.  A wait that exceeds ~4 s
+ * (a missing peer) makes pg_group_transient return PG_ECUDA.
+ *
+ * pg_group_local_p2p: n slabs on the current device in one process (their
+ *   "peers" are each other's buffers; the launches are ordered on one stream).
+ * pg_group_p2p_create / _export / _connect: one slab per process and GPU;
+ *   export this rank's record (CUDA IPC handles of its receive buffers and
+ *   control block; *len bytes, blob may be NULL to query the size), gather the
+ *   records of all ranks ordered by rank (e.g. torch.distributed), connect. */
+PG_API int pg_group_local_p2p(int32_t n, pg_grid *const *slabs, int32_t ghost, pg_group **out);
+PG_API int pg_group_p2p_create(pg_grid *slab, int32_t nranks, int32_t rank, int32_t ghost, pg_group **out);
+PG_API int pg_group_p2p_export(pg_group *grp, void *blob, int64_t cap, int64_t *len);
+PG_API int pg_group_p2p_connect(pg_group *grp, const void *blobs, int64_t blob_len);
+
 PG_API int pg_group_transient(pg_group *grp, double h, int64_t steps, double tol, double omega,
                               int64_t max_sweeps, int64_t *sweeps_out, pg_stats *stats);
 

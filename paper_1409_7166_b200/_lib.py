@@ -53,6 +53,10 @@ SIGNATURES = {
     "pg_nccl_unique_id": (_c_int, [_vp]),
     "pg_group_nccl": (_c_int, [_vp, _vp, _i32, _i32, _i32, ctypes.POINTER(_vp)]),
     "pg_group_local": (_c_int, [_i32, ctypes.POINTER(_vp), _i32, ctypes.POINTER(_vp)]),
+    "pg_group_local_p2p": (_c_int, [_i32, ctypes.POINTER(_vp), _i32, ctypes.POINTER(_vp)]),
+    "pg_group_p2p_create": (_c_int, [_vp, _i32, _i32, _i32, ctypes.POINTER(_vp)]),
+    "pg_group_p2p_export": (_c_int, [_vp, _vp, _i64, ctypes.POINTER(_i64)]),
+    "pg_group_p2p_connect": (_c_int, [_vp, _vp, _i64]),
     "pg_group_transient": (_c_int, [_vp, _dbl, _i64, _dbl, _dbl, _i64, _vp, ctypes.POINTER(PgStats)]),
     "pg_group_destroy": (None, [_vp]),
     "pg_last_error": (ctypes.c_char_p, []),

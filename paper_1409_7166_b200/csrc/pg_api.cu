@@ -699,11 +699,14 @@ int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, d
   Ev evguard{evs};
 
   int64_t launches = 0;
-  const bool graph_ok = g->use_graph && ng == 1 && ex == nullptr;
-  // consecutive sweep launches of a single grid may overlap (PDL): launch
-  // j > 0 of a batch directly follows launch j - 1 in the stream
+  // a single grid, or one slab per process whose exchange is fused into the
+  // sweep kernels (peer memory), has nothing to do between sweep launches
+  const bool quiet = ng == 1 && (ex == nullptr || ex->fused());
+  const bool graph_ok = g->use_graph && quiet;
+  // consecutive sweep launches may overlap (PDL): launch j > 0 of a batch
+  // directly follows launch j - 1 in the stream
   for (int k = 0; k < ng; ++k) gs[k]->pdl_ok = false;
-  g->pdl_ok = g->pdl != 0 && ng == 1 && ex == nullptr;
+  g->pdl_ok = g->pdl != 0 && quiet;
   const bool resident = ng == 1 && ex == nullptr && resident_ok(g, method);
   const int F = sweeps_per_launch(g, method);
   for (int k = 1; k < ng; ++k)

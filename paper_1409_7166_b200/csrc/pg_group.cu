@@ -26,6 +26,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstddef>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -139,6 +140,69 @@ __global__ void k_halo_unpack(MeshDims d, double *V0, double *V1, const DevCtl *
   }
 }
 
+// ------------------------------------------------ peer-memory exchange kernels
+// wait (thread 0 of each block) until `sig` reaches `target`, with a watchdog
+__device__ __forceinline__ void wait_sig(DevCtl *c, unsigned long long target) {
+  if (threadIdx.x == 0) {
+    const long long t0 = clock64();
+    while (*(volatile unsigned long long *)&c->sig < target && !*(volatile int32_t *)&c->p2p_timeout) {
+      if (clock64() - t0 > (1ll << 33)) {
+        c->p2p_timeout = 1;
+        break;
+      }
+      __nanosleep(64);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// transient start: this slab's ghost rows of x(0) (V[base]) seed the receive
+// buffers of parity epoch & 1, which the first sweep launch reads
+__global__ void k_halo_seed_p2p(MeshDims d, const double *V0, const double *V1, const DevCtl *c, int lo_row,
+                                int hi_row, int G, double *lo_a, double *lo_b, double *hi_a, double *hi_b) {
+  const double *V = c->base ? V1 : V0;
+  const int par = (int)(c->epoch & 1);
+  double *lo_buf = par ? lo_b : lo_a, *hi_buf = par ? hi_b : hi_a;
+  const int64_t per = (int64_t)d.L * G * d.NXP;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < 2 * per;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int side = k >= per;
+    const int64_t q = side ? k - per : k;
+    const int row0 = side ? hi_row : lo_row;
+    double *buf = side ? hi_buf : lo_buf;
+    if (row0 < 0 || buf == nullptr) continue;
+    const int64_t x = q % d.NXP, lr = q / d.NXP;
+    const int64_t l = lr / G, r = lr % G;
+    buf[q] = V[l * d.layer_stride + (row0 + r) * d.NXP + x];
+  }
+}
+
+// end of a step: once every slab finished the step's last working launch, the
+// ghost rows it stored into this slab's receive buffers go into V
+__global__ void k_halo_unpack_p2p(MeshDims d, double *V0, double *V1, DevCtl *c, int lo_row, int hi_row, int G,
+                                  const double *lo_a, const double *lo_b, const double *hi_a, const double *hi_b,
+                                  int64_t total_ctas) {
+  const int64_t ran = c->done ? c->launches_done : c->jbase;
+  const int64_t en = c->epoch + ran;
+  wait_sig(c, (unsigned long long)en * (unsigned long long)total_ctas);
+  double *V = ((c->base + ran) & 1) ? V1 : V0;
+  const int par = (int)(en & 1);
+  const double *lo_buf = par ? lo_b : lo_a, *hi_buf = par ? hi_b : hi_a;
+  const int64_t per = (int64_t)d.L * G * d.NXP;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < 2 * per;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int side = k >= per;
+    const int64_t q = side ? k - per : k;
+    const int row0 = side ? hi_row : lo_row;
+    const double *buf = side ? hi_buf : lo_buf;
+    if (row0 < 0 || buf == nullptr) continue;
+    const int64_t x = q % d.NXP, lr = q / d.NXP;
+    const int64_t l = lr / G, r = lr % G;
+    V[l * d.layer_stride + (row0 + r) * d.NXP + x] = buf[q];
+  }
+}
+
 // local transport: max of the launch's norm slot over all slabs, written back
 __global__ void k_group_max(DevCtl **ctls, int n, int slot) {
   unsigned long long m = 0ull;
@@ -155,19 +219,28 @@ int grid_for(int64_t work, int num_sms) {
 }  // namespace
 
 struct pg_group : public pgb::Exchange {
-  int kind = 0;  // 0 local, 1 nccl
+  int kind = 0;  // 0 local (copies), 1 nccl, 2 local peer-memory, 3 ipc peer-memory
   std::vector<pg_grid *> slabs;
   int rank = 0, nranks = 1, G = 0;
   int64_t halo = 0;  // doubles per side per slab
-  std::vector<double *> send_lo, send_hi, recv_lo, recv_hi;
+  std::vector<double *> send_lo, send_hi, recv_lo, recv_hi, recv_lo_b, recv_hi_b;
+  std::vector<void *> opened;  // peers' buffers mapped with cudaIpcOpenMemHandle
+  int64_t my_ctas = 0;         // ipc: this slab's CTAs per launch (exported)
+  bool p2p() const { return kind >= 2; }
   DevCtl **d_ctls = nullptr;
   ncclComm_t comm = nullptr;
   std::string err;
 
-  bool has_lo(int k) const { return (kind == 0 ? k : rank) > 0; }
-  bool has_hi(int k) const { return (kind == 0 ? k : rank) < nranks - 1; }
+  bool local() const { return kind == 0 || kind == 2; }
+  bool has_lo(int k) const { return (local() ? k : rank) > 0; }
+  bool has_hi(int k) const { return (local() ? k : rank) < nranks - 1; }
+
+  bool fused() const override { return p2p(); }
 
   cudaError_t after_sweep(int j, int jr, int64_t *launches) override {
+    // peer-memory exchange: the sweep kernel itself stored the boundary rows
+    // into the neighbours' buffers and max-reduced the norm into every slab
+    if (p2p()) return cudaSuccess;
     cudaStream_t st = slabs[0]->stream;
     const int slot = j & (kRing - 1);
     cudaError_t e;
@@ -210,6 +283,15 @@ struct pg_group : public pgb::Exchange {
   // initial state: the ghost rows of V[0] (x(0)) seed the receive buffers
   cudaError_t begin() override {
     cudaStream_t st = slabs[0]->stream;
+    if (p2p()) {
+      for (size_t k = 0; k < slabs.size(); ++k) {
+        pg_grid *g = slabs[k];
+        k_halo_seed_p2p<<<grid_for(2 * halo, g->num_sms), 256, 0, st>>>(
+            g->md, g->V[0], g->V[1], g->ctl, has_lo((int)k) ? g->y_begin - G : -1,
+            has_hi((int)k) ? g->y_end : -1, G, recv_lo[k], recv_lo_b[k], recv_hi[k], recv_hi_b[k]);
+      }
+      return cudaGetLastError();
+    }
     for (size_t k = 0; k < slabs.size(); ++k) {
       pg_grid *g = slabs[k];
       k_halo_pack<<<grid_for(2 * halo, g->num_sms), 256, 0, st>>>(
@@ -223,6 +305,17 @@ struct pg_group : public pgb::Exchange {
   // the inductor update of the next step read them there)
   cudaError_t end_step(int64_t *launches) override {
     cudaStream_t st = slabs[0]->stream;
+    if (p2p()) {
+      for (size_t k = 0; k < slabs.size(); ++k) {
+        pg_grid *g = slabs[k];
+        k_halo_unpack_p2p<<<grid_for(2 * halo, g->num_sms), 256, 0, st>>>(
+            g->md, g->V[0], g->V[1], g->ctl, has_lo((int)k) ? g->y_begin - G : -1,
+            has_hi((int)k) ? g->y_end : -1, G, recv_lo[k], recv_lo_b[k], recv_hi[k], recv_hi_b[k],
+            g->hx.total_ctas);
+        ++*launches;
+      }
+      return cudaGetLastError();
+    }
     for (size_t k = 0; k < slabs.size(); ++k) {
       pg_grid *g = slabs[k];
       k_halo_unpack<<<grid_for(2 * halo, g->num_sms), 256, 0, st>>>(
@@ -236,7 +329,9 @@ struct pg_group : public pgb::Exchange {
   void release() {
     for (pg_grid *g : slabs)
       if (g) g->hx = SlabHalo{};
-    for (auto *v : {&send_lo, &send_hi, &recv_lo, &recv_hi})
+    for (void *p : opened) cudaIpcCloseMemHandle(p);
+    opened.clear();
+    for (auto *v : {&send_lo, &send_hi, &recv_lo, &recv_hi, &recv_lo_b, &recv_hi_b})
       for (double *p : *v)
         if (p) cudaFree(p);
     if (d_ctls) cudaFree(d_ctls);
@@ -272,6 +367,9 @@ int attach_halo(pg_group *grp) {
     h.send_hi = grp->send_hi[k];
     h.recv_lo = grp->recv_lo[k];
     h.recv_hi = grp->recv_hi[k];
+    h.p2p = grp->p2p();
+    h.recv_lo_b = grp->recv_lo_b[k];
+    h.recv_hi_b = grp->recv_hi_b[k];
     if (!encode_halo_maps(g)) {
       set_error("encoding the ghost-row tensor maps failed");
       return PG_ECUDA;
@@ -287,9 +385,18 @@ int alloc_bufs(pg_group *grp) {
         "slabs must share layers and columns");
   grp->halo = (int64_t)g0->md.L * grp->G * g0->md.NXP;
   const size_t n = grp->slabs.size();
-  for (auto *v : {&grp->send_lo, &grp->send_hi, &grp->recv_lo, &grp->recv_hi}) v->assign(n, nullptr);
+  for (auto *v : {&grp->send_lo, &grp->send_hi, &grp->recv_lo, &grp->recv_hi, &grp->recv_lo_b, &grp->recv_hi_b})
+    v->assign(n, nullptr);
+  std::vector<std::vector<double *> *> bufs = {&grp->recv_lo, &grp->recv_hi};
+  if (grp->p2p()) {
+    bufs.push_back(&grp->recv_lo_b);
+    bufs.push_back(&grp->recv_hi_b);
+  } else {
+    bufs.push_back(&grp->send_lo);
+    bufs.push_back(&grp->send_hi);
+  }
   for (size_t k = 0; k < n; ++k) {
-    for (auto *v : {&grp->send_lo, &grp->send_hi, &grp->recv_lo, &grp->recv_hi}) {
+    for (auto *v : bufs) {
       cudaError_t e = cudaMalloc((void **)&(*v)[k], sizeof(double) * (size_t)grp->halo);
       if (e != cudaSuccess) {
         set_error(std::string("halo buffer allocation failed: ") + cudaGetErrorString(e));
@@ -300,6 +407,30 @@ int alloc_bufs(pg_group *grp) {
   }
   return PG_OK;
 }
+
+// peer-memory exchange: every launch must be a full two-sweep launch of the
+// pipeline kernel (its CTA count is part of the arrival target)
+int check_p2p(const pg_grid *g) {
+  REQ(g->pipe && sweep2_width(g->md.L) != 0 && sweeps_per_launch(const_cast<pg_grid *>(g), PG_METHOD_RBSOR) == 2,
+      "the peer-memory exchange needs the two-sweep pipeline kernel (options fuse = 0 or 2, pipe = 1)");
+  return PG_OK;
+}
+
+// fresh exchange state: epochs, arrival counter, norm ring, watchdog flag
+int reset_p2p_state(pg_grid *g) {
+  const size_t off = offsetof(DevCtl, epoch);
+  CKR(cudaMemset(reinterpret_cast<char *>(g->ctl) + off, 0, sizeof(DevCtl) - off));
+  return PG_OK;
+}
+
+// Serialised per-slab description exchanged between ranks (ipc transport)
+struct P2pBlob {
+  uint32_t magic, version;
+  int32_t rank, nranks;
+  int64_t ctas;
+  cudaIpcMemHandle_t recv_lo, recv_lo_b, recv_hi, recv_hi_b, ctl;
+};
+constexpr uint32_t kBlobMagic = 0x50473250u;  // "PG2P"
 
 }  // namespace
 
@@ -406,14 +537,179 @@ PG_API int pg_group_local(int32_t n, pg_grid *const *slabs, int32_t ghost, pg_gr
   return PG_OK;
 }
 
+PG_API int pg_group_local_p2p(int32_t n, pg_grid *const *slabs, int32_t ghost, pg_group **out) {
+  if (out) *out = nullptr;
+  REQ(out != nullptr && slabs != nullptr, "out/slabs is NULL");
+  REQ(n >= 1 && n <= kMaxPeers, "peer-memory groups have 1..8 slabs");
+  REQ(ghost >= 4 && ghost <= 64, "ghost rows must be in 4..64 (2 F, F = 2)");
+  int rc;
+  for (int k = 0; k < n; ++k) {
+    if ((rc = check_slab(slabs[k], ghost, k > 0, k < n - 1))) return rc;
+    if ((rc = check_p2p(slabs[k]))) return rc;
+  }
+  pg_group *grp = new pg_group();
+  grp->kind = 2;
+  grp->slabs.assign(slabs, slabs + n);
+  grp->nranks = n;
+  grp->G = ghost;
+  if ((rc = alloc_bufs(grp))) {
+    grp->release();
+    delete grp;
+    return rc;
+  }
+  // "peers" are the other slabs on this device: the kernels see exactly the
+  // pointers a multi-GPU group maps from its neighbours
+  for (int k = 0; k < n; ++k) {
+    SlabHalo &h = slabs[k]->hx;
+    h = SlabHalo{};
+    h.nranks = n;
+    for (int r = 0; r < n; ++r) {
+      h.sig_all[r] = &slabs[r]->ctl->sig;
+      h.pnorm_all[r] = slabs[r]->ctl->pnorm;
+    }
+    if (k > 0) {
+      h.peer_lo[0] = grp->recv_hi[k - 1];
+      h.peer_lo[1] = grp->recv_hi_b[k - 1];
+    }
+    if (k < n - 1) {
+      h.peer_hi[0] = grp->recv_lo[k + 1];
+      h.peer_hi[1] = grp->recv_lo_b[k + 1];
+    }
+    if ((rc = reset_p2p_state(slabs[k]))) {
+      grp->release();
+      delete grp;
+      return rc;
+    }
+  }
+  if ((rc = attach_halo(grp))) {
+    grp->release();
+    delete grp;
+    return rc;
+  }
+  // arrival target: CTAs of one launch of every slab (the slab variant's grid)
+  int64_t total = 0;
+  for (int k = 0; k < n; ++k) total += sweep2_grid_ctas(slabs[k]);
+  for (int k = 0; k < n; ++k) slabs[k]->hx.total_ctas = total;
+  *out = grp;
+  return PG_OK;
+}
+
+PG_API int pg_group_p2p_create(pg_grid *slab, int32_t nranks, int32_t rank, int32_t ghost, pg_group **out) {
+  if (out) *out = nullptr;
+  REQ(out != nullptr, "out is NULL");
+  REQ(nranks >= 1 && nranks <= kMaxPeers && rank >= 0 && rank < nranks, "bad rank / nranks (1..8 ranks)");
+  REQ(ghost >= 4 && ghost <= 64, "ghost rows must be in 4..64 (2 F, F = 2)");
+  int rc;
+  if ((rc = check_slab(slab, ghost, rank > 0, rank < nranks - 1)) || (rc = check_p2p(slab))) return rc;
+  pg_group *grp = new pg_group();
+  grp->kind = 3;
+  grp->slabs = {slab};
+  grp->rank = rank;
+  grp->nranks = nranks;
+  grp->G = ghost;
+  slab->hx.G = ghost;  // the slab variant's grid (occupancy) decides the CTA count
+  grp->my_ctas = sweep2_grid_ctas(slab);
+  if ((rc = alloc_bufs(grp)) || (rc = reset_p2p_state(slab))) {
+    grp->release();
+    delete grp;
+    return rc;
+  }
+  cudaDeviceSynchronize();
+  *out = grp;
+  return PG_OK;
+}
+
+PG_API int pg_group_p2p_export(pg_group *grp, void *blob, int64_t cap, int64_t *len) {
+  REQ(grp != nullptr && grp->kind == 3, "not an ipc peer-memory group");
+  REQ(len != nullptr, "len is NULL");
+  *len = (int64_t)sizeof(P2pBlob);
+  if (blob == nullptr) return PG_OK;
+  REQ(cap >= (int64_t)sizeof(P2pBlob), "blob buffer too small");
+  P2pBlob b;
+  std::memset(&b, 0, sizeof(b));
+  b.magic = kBlobMagic;
+  b.version = 1;
+  b.rank = grp->rank;
+  b.nranks = grp->nranks;
+  b.ctas = grp->my_ctas;
+  CKR(cudaIpcGetMemHandle(&b.recv_lo, grp->recv_lo[0]));
+  CKR(cudaIpcGetMemHandle(&b.recv_lo_b, grp->recv_lo_b[0]));
+  CKR(cudaIpcGetMemHandle(&b.recv_hi, grp->recv_hi[0]));
+  CKR(cudaIpcGetMemHandle(&b.recv_hi_b, grp->recv_hi_b[0]));
+  CKR(cudaIpcGetMemHandle(&b.ctl, grp->slabs[0]->ctl));
+  std::memcpy(blob, &b, sizeof(b));
+  return PG_OK;
+}
+
+PG_API int pg_group_p2p_connect(pg_group *grp, const void *blobs, int64_t blob_len) {
+  REQ(grp != nullptr && grp->kind == 3, "not an ipc peer-memory group");
+  REQ(blobs != nullptr && blob_len == (int64_t)sizeof(P2pBlob), "blobs: nranks records from pg_group_p2p_export");
+  std::vector<P2pBlob> all((size_t)grp->nranks);
+  std::memcpy(all.data(), blobs, sizeof(P2pBlob) * all.size());
+  int64_t total = 0;
+  for (int r = 0; r < grp->nranks; ++r) {
+    REQ(all[r].magic == kBlobMagic && all[r].version == 1 && all[r].rank == r && all[r].nranks == grp->nranks,
+        "inconsistent peer records (order them by rank)");
+    total += all[r].ctas;
+  }
+  pg_grid *g = grp->slabs[0];
+  SlabHalo h;
+  h.nranks = grp->nranks;
+  h.total_ctas = total;
+  auto open = [&](const cudaIpcMemHandle_t &hd, void **p) -> int {
+    CKR(cudaIpcOpenMemHandle(p, hd, cudaIpcMemLazyEnablePeerAccess));
+    grp->opened.push_back(*p);
+    return PG_OK;
+  };
+  int rc;
+  for (int r = 0; r < grp->nranks; ++r) {
+    DevCtl *c = g->ctl;
+    if (r != grp->rank) {
+      void *p = nullptr;
+      if ((rc = open(all[r].ctl, &p))) return rc;
+      c = reinterpret_cast<DevCtl *>(p);
+    }
+    h.sig_all[r] = &c->sig;
+    h.pnorm_all[r] = c->pnorm;
+  }
+  void *p[2];
+  if (grp->rank > 0) {
+    if ((rc = open(all[grp->rank - 1].recv_hi, &p[0])) || (rc = open(all[grp->rank - 1].recv_hi_b, &p[1])))
+      return rc;
+    h.peer_lo[0] = reinterpret_cast<double *>(p[0]);
+    h.peer_lo[1] = reinterpret_cast<double *>(p[1]);
+  }
+  if (grp->rank < grp->nranks - 1) {
+    if ((rc = open(all[grp->rank + 1].recv_lo, &p[0])) || (rc = open(all[grp->rank + 1].recv_lo_b, &p[1])))
+      return rc;
+    h.peer_hi[0] = reinterpret_cast<double *>(p[0]);
+    h.peer_hi[1] = reinterpret_cast<double *>(p[1]);
+  }
+  g->hx = h;
+  return attach_halo(grp);
+}
+
 PG_API int pg_group_transient(pg_group *grp, double h, int64_t steps, double tol, double omega,
                               int64_t max_sweeps, int64_t *sweeps_out, pg_stats *stats) {
   REQ(grp != nullptr, "group is NULL");
   for (pg_grid *g : grp->slabs)
     REQ(2 * sweeps_per_launch(g, PG_METHOD_RBSOR) <= grp->G,
         "ghost rows must cover 2 F rows (F = fuse option): lower fuse or rebuild the slabs");
-  return run_transient(grp->slabs.data(), (int)grp->slabs.size(), grp, h, steps, tol, omega,
-                       PG_METHOD_RBSOR, max_sweeps, 0, nullptr, nullptr, PG_MEM_HOST, sweeps_out, stats);
+  if (grp->p2p()) {
+    REQ(max_sweeps % 2 == 0, "the peer-memory exchange runs full two-sweep launches: max_sweeps must be even");
+    int rc;
+    for (pg_grid *g : grp->slabs)
+      if ((rc = check_p2p(g))) return rc;
+  }
+  const int rc = run_transient(grp->slabs.data(), (int)grp->slabs.size(), grp, h, steps, tol, omega,
+                               PG_METHOD_RBSOR, max_sweeps, 0, nullptr, nullptr, PG_MEM_HOST, sweeps_out, stats);
+  if (grp->p2p())
+    for (pg_grid *g : grp->slabs)
+      if (g->ctl_host->p2p_timeout) {
+        set_error("peer-memory exchange: a wait for the other slabs timed out (results invalid)");
+        return PG_ECUDA;
+      }
+  return rc;
 }
 
 PG_API void pg_group_destroy(pg_group *grp) {

@@ -27,6 +27,16 @@ struct DevCtl {
   int32_t jbase;           // launch index of the first launch of the current batch:
                            // a sweep kernel's launch index is jbase + its argument,
                            // so one captured batch (CUDA graph) serves every batch
+  // peer-memory slab exchange (pg_group kinds "p2p"): sweep launches that did
+  // work since the group was formed (epoch of the next launch = epoch + its
+  // index in the step), the arrival counter every CTA of every slab bumps
+  // (remotely) when its launch is complete, and the norm ring indexed by epoch
+  // that every CTA max-reduces into (remotely) -- none is reset per step or
+  // per transient, so early remote contributions are never lost
+  int64_t epoch;
+  unsigned long long sig;
+  unsigned long long pnorm[4];
+  int32_t p2p_timeout;     // a peer wait gave up (watchdog), results invalid
 };
 
 constexpr int kRing = 4;
@@ -65,7 +75,20 @@ struct SlabHalo {
   bool has_lo = false, has_hi = false;
   double *send_lo = nullptr, *send_hi = nullptr, *recv_lo = nullptr, *recv_hi = nullptr;
   CUtensorMap mlo[2], mhi[2];  // [W = 32 / 64] maps of recv_lo / recv_hi
+  // peer-memory exchange: receive buffers double-buffered by launch epoch
+  // (recv_* = parity 0, recv_*_b = parity 1); the sweep of epoch e reads its
+  // ghost rows from parity e & 1 and stores its boundary rows straight into the
+  // neighbours' parity (e + 1) & 1 buffers (peer_lo: the lower neighbour's
+  // recv_hi pair, peer_hi: the upper neighbour's recv_lo pair)
+  bool p2p = false;
+  double *recv_lo_b = nullptr, *recv_hi_b = nullptr;
+  CUtensorMap mlo_b[2], mhi_b[2];
+  double *peer_lo[2] = {nullptr, nullptr}, *peer_hi[2] = {nullptr, nullptr};
+  unsigned long long *sig_all[8] = {}, *pnorm_all[8] = {};  // every slab's DevCtl::sig / pnorm
+  int nranks = 1;
+  int64_t total_ctas = 0;  // CTAs of one sweep launch, summed over all slabs
 };
+constexpr int kMaxPeers = 8;
 
 }  // namespace pgb
 
@@ -184,6 +207,7 @@ cudaError_t launch_rb_sweep_fused(pg_grid *g, double omega, double tol, int j, i
 int sweep2_width(int L);  // strip width of the compiled variant, 0: none
 int sweep2_ctas_per_sm(int L, bool slab);
 int sweep2_rows_per_cta(const pg_grid *g, int ny);
+int64_t sweep2_grid_ctas(const pg_grid *g);
 // pdl: launch with programmatic stream serialisation after a sweep launch
 cudaError_t launch_rb_sweep2(pg_grid *g, double omega, double tol, int j, int rows_per_cta, int y_begin,
                              int y_end, int ypar, bool pdl);
@@ -198,6 +222,9 @@ struct Exchange {
   virtual cudaError_t end_step(int64_t *launches) { return cudaSuccess; }
   // launch_idx: index of the launch in the time step; rel: index in its batch
   virtual cudaError_t after_sweep(int launch_idx, int rel, int64_t *launches) = 0;
+  // the exchange happens inside the sweep kernels (nothing between launches):
+  // a single slab per process may then use graph batches and PDL
+  virtual bool fused() const { return false; }
 };
 int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, double tol,
                   double omega, int method, int64_t max_sweeps, int64_t n_probe,

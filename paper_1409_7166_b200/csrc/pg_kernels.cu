@@ -354,6 +354,7 @@ __global__ void k_ind_update_pads(int64_t npad, const int64_t *idx, const double
 __global__ void k_step_end(DevCtl *c, int64_t s, int32_t launched, int32_t flips, int32_t fused,
                            int64_t max_sweeps, double tol, int64_t *rec) {
   const int64_t ran = c->done ? c->launches_done : launched;
+  c->epoch += ran;  // sweep launches that did work (peer-exchange epochs)
   int64_t sw = ran * fused;
   if (sw > max_sweeps) sw = max_sweeps;
   if (flips) c->base ^= (int32_t)(ran & 1);

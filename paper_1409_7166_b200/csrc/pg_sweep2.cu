@@ -4,6 +4,8 @@
 // and other F run k_rb_sweep_fused.
 #include "pg_sweep2.cuh"
 
+#include <algorithm>
+
 namespace pgb {
 
 namespace {
@@ -85,6 +87,16 @@ int sweep2_ctas_per_sm(int L, bool slab) {
   return c;
 }
 
+// CTAs of one k_rb_sweep2 launch over the grid's (owned) rows
+int64_t sweep2_grid_ctas(const pg_grid *g) {
+  const int W = sweep2_width(g->md.L);
+  if (W == 0) return 0;
+  const int y0 = g->slab ? g->y_begin : 0, y1 = g->slab ? g->y_end : g->md.NY;
+  const int H = g->rows > 0 ? std::max(1, std::min(g->rows, y1 - y0)) : sweep2_rows_per_cta(g, y1 - y0);
+  const int I = W - 4;
+  return (int64_t)((g->md.HP + I - 1) / I) * ((y1 - y0 + H - 1) / H);
+}
+
 int sweep2_rows_per_cta(const pg_grid *g, int ny) {
   const int W = sweep2_width(g->md.L);
   const int I = W - 4;
@@ -104,6 +116,23 @@ cudaError_t launch_rb_sweep2(pg_grid *g, double omega, double tol, int j, int ro
   if (!fill_fused_params(g, P, omega, tol, j, 2, W, rows_per_cta, y_begin, y_end, ypar))
     return cudaErrorNotSupported;
   P.pre = pdl ? 1 : 0;
+  {
+    const SlabHalo &h = g->hx;
+    P.p2p = (g->slab && h.G > 0 && h.p2p) ? 1 : 0;
+    P.nranks = h.nranks;
+    P.total_ctas = h.total_ctas;
+    for (int k = 0; k < 2; ++k) {
+      P.peer_lo[k] = h.peer_lo[k];
+      P.peer_hi[k] = h.peer_hi[k];
+    }
+    for (int k = 0; k < kMaxPeers; ++k) {
+      P.sig_all[k] = h.sig_all[k];
+      P.pnorm_all[k] = h.pnorm_all[k];
+    }
+    const int wi = W == 64 ? 1 : 0;
+    if (P.p2p && h.has_lo) P.mRlo_b = h.mlo_b[wi];
+    if (P.p2p && h.has_hi) P.mRhi_b = h.mhi_b[wi];
+  }
   P.l2ahead = g->l2ahead;
   // L2 policy (auto): a mesh whose per-launch footprint (56 B per storage
   // element) is below twice the L2 streams its reads evict_first and writes V

@@ -150,9 +150,34 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
   const int j = *(volatile int32_t *)&ctl->jbase + P.launch_idx;
   // device-side convergence control, as in k_rb_sweep_fused (uniform)
   bool skip = *(volatile int32_t *)&ctl->done != 0;
+  // peer-memory slab exchange: launch epoch e waits until every CTA of every
+  // slab finished epoch e - 1 (their boundary rows are in this slab's parity
+  // e & 1 receive buffers and their norms in pnorm[(e - 1) & 3]); the norm
+  // test below then reads the global max
+  int64_t e = 0;
+  const bool p2p = SLAB && P.p2p;
+  if (p2p && !skip) {
+    e = *(volatile int64_t *)&ctl->epoch + j;
+    if (e > 0 && tid == 0) {
+      const unsigned long long target = (unsigned long long)e * (unsigned long long)P.total_ctas;
+      const long long t0 = clock64();
+      while (*(volatile unsigned long long *)&ctl->sig < target && !*(volatile int32_t *)&ctl->p2p_timeout) {
+        if (clock64() - t0 > (1ll << 33)) {  // watchdog (~4 s): report, do not hang
+          ctl->p2p_timeout = 1;
+          break;
+        }
+        __nanosleep(64);
+      }
+      __threadfence();
+    }
+    __syncthreads();
+    if (j > 0 && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0)  // the global norm, for k_step_end
+      ctl->dmax[(j - 1) & (kRing - 1)] = *(volatile unsigned long long *)&ctl->pnorm[(e - 1) & 3];
+  }
   if (!skip && j > 0) {
-    const double prev = __longlong_as_double(
-        (long long)(*(volatile unsigned long long *)&ctl->dmax[(j - 1) & (kRing - 1)]));
+    const double prev = __longlong_as_double((long long)(
+        p2p ? *(volatile unsigned long long *)&ctl->pnorm[(e - 1) & 3]
+            : *(volatile unsigned long long *)&ctl->dmax[(j - 1) & (kRing - 1)]));
     if (prev < P.tol) {
       if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) {
         ctl->done = 1;
@@ -170,20 +195,26 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
       }
     return;
   }
-  if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) ctl->dmax[(j + 1) & (kRing - 1)] = 0ull;
+  if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) {
+    ctl->dmax[(j + 1) & (kRing - 1)] = 0ull;
+    // pnorm[(e + 1) & 3] receives epoch e + 1's remote maxima, which start
+    // only after every slab finished this epoch, i.e. after this store
+    if (p2p) ctl->pnorm[(e + 1) & 3] = 0ull;
+  }
   const int par = (*(volatile int32_t *)&ctl->base + j) & 1;
 
   // ---------------------------------------------------------------- TMA issue
   const CUtensorMap *mVin = par ? &P.mV1 : &P.mV0;
   auto v_src = [&](int r, int &rr) -> const CUtensorMap * {
     if constexpr (SLAB) {
+      const bool b = p2p && (e & 1);  // peer exchange: parity-e receive buffers
       if (P.has_rlo && r < P.y_begin) {
         rr = r - (P.y_begin - P.G);
-        return &P.mRlo;
+        return b ? &P.mRlo_b : &P.mRlo;
       }
       if (P.has_rhi && r >= P.y_end) {
         rr = r - P.y_end;
-        return &P.mRhi;
+        return b ? &P.mRhi_b : &P.mRhi;
       }
     }
     rr = r;
@@ -392,13 +423,15 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
         const int rr = y - 4;
         const bool red_odd = (q ^ k) != 0;
         const double ve = red_odd ? b1 : Vownb1, vo = red_odd ? Vownb1 : b1;
-        if (P.send_lo && rr < P.y_begin + P.G) {
-          double *sb = P.send_lo + ((int64_t)l * P.G + (rr - P.y_begin)) * P.NXP;
+        double *slo = p2p ? P.peer_lo[(e + 1) & 1] : P.send_lo;
+        double *shi = p2p ? P.peer_hi[(e + 1) & 1] : P.send_hi;
+        if (slo && rr < P.y_begin + P.G) {
+          double *sb = slo + ((int64_t)l * P.G + (rr - P.y_begin)) * P.NXP;
           sb[gp] = ve;
           sb[gp + P.HP] = vo;
         }
-        if (P.send_hi && rr >= P.y_end - P.G) {
-          double *sb = P.send_hi + ((int64_t)l * P.G + (rr - (P.y_end - P.G))) * P.NXP;
+        if (shi && rr >= P.y_end - P.G) {
+          double *sb = shi + ((int64_t)l * P.G + (rr - (P.y_end - P.G))) * P.NXP;
           sb[gp] = ve;
           sb[gp + P.HP] = vo;
         }
@@ -443,6 +476,23 @@ done:
   for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
   if ((tid & 31) == 0)
     atomicMax(&ctl->dmax[j & (kRing - 1)], static_cast<unsigned long long>(__double_as_longlong(dmax)));
+  if constexpr (SLAB) {
+    if (p2p) {
+      // this CTA's boundary rows (plain stores into peer memory) and its norm
+      // reach every slab before its arrival count does
+      __shared__ unsigned long long cta_max;
+      if (tid == 0) cta_max = 0ull;
+      __syncthreads();
+      if ((tid & 31) == 0) atomicMax(&cta_max, static_cast<unsigned long long>(__double_as_longlong(dmax)));
+      __threadfence_system();
+      __syncthreads();
+      if (tid == 0) {
+        for (int r = 0; r < P.nranks; ++r) atomicMax_system(P.pnorm_all[r] + (e & 3), cta_max);
+        __threadfence_system();
+        for (int r = 0; r < P.nranks; ++r) atomicAdd_system(P.sig_all[r], 1ull);
+      }
+    }
+  }
 }
 
 // Compiled (L, W): W = 64 for L <= 4, W = 32 for L = 5..8 (the fused sweep's default widths)

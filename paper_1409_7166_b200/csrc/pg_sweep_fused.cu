@@ -78,6 +78,8 @@ bool encode_halo_maps(pg_grid *g) {
   for (int w = 0; w < 2; ++w) {
     if (h.has_lo) ok = ok && encode_rows(&h.mlo[w], h.recv_lo, g->md, h.G, w ? 64 : 32, g->l2promo);
     if (h.has_hi) ok = ok && encode_rows(&h.mhi[w], h.recv_hi, g->md, h.G, w ? 64 : 32, g->l2promo);
+    if (h.p2p && h.has_lo) ok = ok && encode_rows(&h.mlo_b[w], h.recv_lo_b, g->md, h.G, w ? 64 : 32, g->l2promo);
+    if (h.p2p && h.has_hi) ok = ok && encode_rows(&h.mhi_b[w], h.recv_hi_b, g->md, h.G, w ? 64 : 32, g->l2promo);
   }
   return ok;
 }
@@ -173,6 +175,9 @@ bool fill_fused_params(pg_grid *g, FusedParams &P, double omega, double tol, int
   P.nsw = nsw;
   P.prof = prof_buffer();
   P.pre = 0;
+  P.p2p = 0;
+  P.nranks = 1;
+  P.total_ctas = 0;
   const SlabHalo &h = g->hx;
   const bool halo = g->slab && h.G > 0;
   P.has_rlo = halo && h.has_lo;

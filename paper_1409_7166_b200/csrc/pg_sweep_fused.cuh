@@ -178,6 +178,12 @@ struct FusedParams {
   int32_t l2keep;   // k_rb_sweep2: bit a < 5: constant array a (gx, gy, gz_eff, b, 1/d) read with L2 evict_last;
                     // bit 5: V written with evict_last (the next launch reads it)
   int32_t l2first;  // k_rb_sweep2: arrays read with evict_first (bits as above, bit 5: V reads); others evict_normal
+  // k_rb_sweep2 slab with the peer-memory exchange (SlabHalo::p2p)
+  CUtensorMap mRlo_b, mRhi_b;  // parity-1 receive buffers
+  int32_t p2p, nranks;
+  int64_t total_ctas;
+  double *peer_lo[2], *peer_hi[2];
+  unsigned long long *sig_all[8], *pnorm_all[8];
 };
 
 // The constants of one node update: x links (west, east), y links (north,

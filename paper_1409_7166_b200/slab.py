@@ -134,19 +134,57 @@ class SlabGroup:
     # ----------------------------------------------------------------- create
     @classmethod
     def local(cls, m, nslabs: int, fuse: int = 2, ghost: Optional[int] = None,
-              device: bool = True, stream=None) -> "SlabGroup":
+              device: bool = True, stream=None, transport: str = "copy",
+              options: Optional[dict] = None) -> "SlabGroup":
         """nslabs slabs of mesh m on the current device (the n-rank protocol
-        emulated in one process)."""
+        emulated in one process).  transport "copy": per-launch norm max and
+        ghost-row copies (the NCCL protocol); "p2p": the peer-memory exchange
+        inside the sweep kernel (pg_group_local_p2p).  `options` are set on
+        every slab grid before the group is formed."""
         G = ghost if ghost is not None else 2 * fuse
         specs = [slab_spec(m.ny, r, nslabs, G) for r in range(nslabs)]
         grids = [make_slab_grid(m, sp, device, fuse) for sp in specs]
-        if stream is not None:
-            for g in grids:
+        for g in grids:
+            if stream is not None:
                 g.set_stream(stream)
+            for k, v in (options or {}).items():
+                g.set_option(k, int(v))
         arr = (ctypes.c_void_p * nslabs)(*[g._h.value for g in grids])
         out = ctypes.c_void_p()
-        L.check(L.load().pg_group_local(nslabs, arr, G, ctypes.byref(out)))
+        fn = L.load().pg_group_local_p2p if transport == "p2p" else L.load().pg_group_local
+        if transport not in ("copy", "p2p"):
+            raise ValueError("transport must be 'copy' or 'p2p'")
+        L.check(fn(nslabs, arr, G, ctypes.byref(out)))
         return cls(out.value, grids, specs)
+
+    @classmethod
+    def p2p(cls, m, rank: int, nranks: int, fuse: int = 2, ghost: Optional[int] = None,
+            stream=None, group=None, device: bool = True, options: Optional[dict] = None) -> "SlabGroup":
+        """This process's slab (one GPU per rank) with the peer-memory exchange:
+        CUDA IPC records of all ranks are gathered over torch.distributed (the
+        default process group or `group`), then every rank maps its
+        neighbours' receive buffers and all control blocks."""
+        import torch.distributed as dist
+        G = ghost if ghost is not None else 2 * fuse
+        sp = slab_spec(m.ny, rank, nranks, G)
+        g = make_slab_grid(m, sp, device, fuse)
+        if stream is not None:
+            g.set_stream(stream)
+        for k, v in (options or {}).items():
+            g.set_option(k, int(v))
+        lib = L.load()
+        out = ctypes.c_void_p()
+        L.check(lib.pg_group_p2p_create(g._h, nranks, rank, G, ctypes.byref(out)))
+        n = ctypes.c_int64()
+        L.check(lib.pg_group_p2p_export(out, None, 0, ctypes.byref(n)))
+        buf = (ctypes.c_uint8 * n.value)()
+        L.check(lib.pg_group_p2p_export(out, buf, n.value, ctypes.byref(n)))
+        recs = [None] * nranks
+        dist.all_gather_object(recs, bytes(buf), group=group)
+        blob = b"".join(recs)
+        L.check(lib.pg_group_p2p_connect(out, blob, n.value))
+        dist.barrier(group=group)
+        return cls(out.value, [g], [sp])
 
     @classmethod
     def nccl(cls, m, rank: int, nranks: int, fuse: int = 2, ghost: Optional[int] = None,
