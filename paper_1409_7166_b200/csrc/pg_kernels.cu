@@ -137,6 +137,28 @@ struct CsrArgs {
   DevCtl *ctl;
 };
 
+// streamed loads with an L2 eviction policy (createpolicy)
+__device__ __forceinline__ uint64_t pol_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double ldf(const double *p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int32_t ldi(const int32_t *p, uint64_t pol) {
+  int32_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int64_t ldl(const int64_t *p, uint64_t pol) {
+  int64_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.s64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
 __global__ void __launch_bounds__(256) k_csr_sweep(CsrArgs a) {
   __shared__ double wmax[8];
   a.launch_idx += *(volatile int32_t *)&a.ctl->jbase;
@@ -144,13 +166,16 @@ __global__ void __launch_bounds__(256) k_csr_sweep(CsrArgs a) {
   zero_next_slot(a.ctl, a.launch_idx, a.first != 0);
   double *V = (*(volatile int32_t *)&a.ctl->base) ? a.V1 : a.V0;
   double dmax = 0.0;
+  // the row data (structure, values, b, 1/d) streams through L2 evict_first so
+  // that the gathered neighbour voltages stay resident
+  const uint64_t pf = pol_first();
   for (int64_t i = a.r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.r1;
        i += (int64_t)gridDim.x * blockDim.x) {
-    double s = a.b[i];
-    const int64_t k1 = a.rowptr[i + 1];
-    for (int64_t k = a.rowptr[i]; k < k1; ++k) s = fma(__ldg(a.val + k), V[__ldg(a.col + k)], s);
+    double s = ldf(a.b + i, pf);
+    const int64_t k1 = ldl(a.rowptr + i + 1, pf);
+    for (int64_t k = ldl(a.rowptr + i, pf); k < k1; ++k) s = fma(ldf(a.val + k, pf), V[ldi(a.col + k, pf)], s);
     const double vc = V[i];
-    const double vn = fma(a.omega, s * a.invd[i] - vc, vc);
+    const double vn = fma(a.omega, s * ldf(a.invd + i, pf) - vc, vc);
     V[i] = vn;
     dmax = fmax(dmax, fabs(vn - vc));
   }
