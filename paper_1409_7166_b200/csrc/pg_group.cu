@@ -182,10 +182,10 @@ __global__ void k_halo_seed_p2p(MeshDims d, const double *V0, const double *V1, 
 // ghost rows it stored into this slab's receive buffers go into V
 __global__ void k_halo_unpack_p2p(MeshDims d, double *V0, double *V1, DevCtl *c, int lo_row, int hi_row, int G,
                                   const double *lo_a, const double *lo_b, const double *hi_a, const double *hi_b,
-                                  int64_t total_ctas) {
+                                  int32_t nranks) {
   const int64_t ran = c->done ? c->launches_done : c->jbase;
   const int64_t en = c->epoch + ran;
-  wait_sig(c, (unsigned long long)en * (unsigned long long)total_ctas);
+  wait_sig(c, (unsigned long long)en * (unsigned long long)nranks);
   double *V = ((c->base + ran) & 1) ? V1 : V0;
   const int par = (int)(en & 1);
   const double *lo_buf = par ? lo_b : lo_a, *hi_buf = par ? hi_b : hi_a;
@@ -311,7 +311,7 @@ struct pg_group : public pgb::Exchange {
         k_halo_unpack_p2p<<<grid_for(2 * halo, g->num_sms), 256, 0, st>>>(
             g->md, g->V[0], g->V[1], g->ctl, has_lo((int)k) ? g->y_begin - G : -1,
             has_hi((int)k) ? g->y_end : -1, G, recv_lo[k], recv_lo_b[k], recv_hi[k], recv_hi_b[k],
-            g->hx.total_ctas);
+            g->hx.nranks);
         ++*launches;
       }
       return cudaGetLastError();
@@ -427,7 +427,7 @@ int reset_p2p_state(pg_grid *g) {
 struct P2pBlob {
   uint32_t magic, version;
   int32_t rank, nranks;
-  int64_t ctas;
+  int64_t ctas;  // informational: CTAs of one sweep launch of this slab
   cudaIpcMemHandle_t recv_lo, recv_lo_b, recv_hi, recv_hi_b, ctl;
 };
 constexpr uint32_t kBlobMagic = 0x50473250u;  // "PG2P"
@@ -586,10 +586,6 @@ PG_API int pg_group_local_p2p(int32_t n, pg_grid *const *slabs, int32_t ghost, p
     delete grp;
     return rc;
   }
-  // arrival target: CTAs of one launch of every slab (the slab variant's grid)
-  int64_t total = 0;
-  for (int k = 0; k < n; ++k) total += sweep2_grid_ctas(slabs[k]);
-  for (int k = 0; k < n; ++k) slabs[k]->hx.total_ctas = total;
   *out = grp;
   return PG_OK;
 }
@@ -646,16 +642,12 @@ PG_API int pg_group_p2p_connect(pg_group *grp, const void *blobs, int64_t blob_l
   REQ(blobs != nullptr && blob_len == (int64_t)sizeof(P2pBlob), "blobs: nranks records from pg_group_p2p_export");
   std::vector<P2pBlob> all((size_t)grp->nranks);
   std::memcpy(all.data(), blobs, sizeof(P2pBlob) * all.size());
-  int64_t total = 0;
-  for (int r = 0; r < grp->nranks; ++r) {
+  for (int r = 0; r < grp->nranks; ++r)
     REQ(all[r].magic == kBlobMagic && all[r].version == 1 && all[r].rank == r && all[r].nranks == grp->nranks,
         "inconsistent peer records (order them by rank)");
-    total += all[r].ctas;
-  }
   pg_grid *g = grp->slabs[0];
   SlabHalo h;
   h.nranks = grp->nranks;
-  h.total_ctas = total;
   auto open = [&](const cudaIpcMemHandle_t &hd, void **p) -> int {
     CKR(cudaIpcOpenMemHandle(p, hd, cudaIpcMemLazyEnablePeerAccess));
     grp->opened.push_back(*p);

@@ -29,11 +29,13 @@ struct DevCtl {
                            // so one captured batch (CUDA graph) serves every batch
   // peer-memory slab exchange (pg_group kinds "p2p"): sweep launches that did
   // work since the group was formed (epoch of the next launch = epoch + its
-  // index in the step), the arrival counter every CTA of every slab bumps
-  // (remotely) when its launch is complete, and the norm ring indexed by epoch
-  // that every CTA max-reduces into (remotely) -- none is reset per step or
-  // per transient, so early remote contributions are never lost
+  // index in the step), the count of this slab's finished CTAs, the arrival
+  // counter every slab bumps (remotely) when its launch is complete, and the
+  // norm ring indexed by epoch that every slab max-reduces into (remotely) --
+  // none is reset per step or per transient, so early remote contributions are
+  // never lost
   int64_t epoch;
+  unsigned int ccount[4];  // CTAs of this slab that finished launch e, slot e & 3 (the last one publishes)
   unsigned long long sig;
   unsigned long long pnorm[4];
   int32_t p2p_timeout;     // a peer wait gave up (watchdog), results invalid
@@ -86,7 +88,6 @@ struct SlabHalo {
   double *peer_lo[2] = {nullptr, nullptr}, *peer_hi[2] = {nullptr, nullptr};
   unsigned long long *sig_all[8] = {}, *pnorm_all[8] = {};  // every slab's DevCtl::sig / pnorm
   int nranks = 1;
-  int64_t total_ctas = 0;  // CTAs of one sweep launch, summed over all slabs
 };
 constexpr int kMaxPeers = 8;
 

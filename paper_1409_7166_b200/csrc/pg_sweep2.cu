@@ -120,7 +120,6 @@ cudaError_t launch_rb_sweep2(pg_grid *g, double omega, double tol, int j, int ro
     const SlabHalo &h = g->hx;
     P.p2p = (g->slab && h.G > 0 && h.p2p) ? 1 : 0;
     P.nranks = h.nranks;
-    P.total_ctas = h.total_ctas;
     for (int k = 0; k < 2; ++k) {
       P.peer_lo[k] = h.peer_lo[k];
       P.peer_hi[k] = h.peer_hi[k];

@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
   if (p2p && !skip) {
     e = *(volatile int64_t *)&ctl->epoch + j;
     if (e > 0 && tid == 0) {
-      const unsigned long long target = (unsigned long long)e * (unsigned long long)P.total_ctas;
+      const unsigned long long target = (unsigned long long)e * (unsigned long long)P.nranks;
       const long long t0 = clock64();
       while (*(volatile unsigned long long *)&ctl->sig < target && !*(volatile int32_t *)&ctl->p2p_timeout) {
         if (clock64() - t0 > (1ll << 33)) {  // watchdog (~4 s): report, do not hang
@@ -302,6 +302,10 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
   double *OUT0 = q ? vout_o : vout_e, *OUT1 = q ? vout_e : vout_o;  // red's column for class 0 / 1
   const double w = P.omega;
   double dmax = 0.0;
+  bool wrote_peer = false;  // this thread stored boundary rows into a neighbour's buffer
+  // only the first / last chunk of a slab writes rows for a neighbour
+  const bool send_cta = SLAB && ((ys < P.y_begin + P.G && (P.send_lo || (p2p && P.peer_lo[0]))) ||
+                                 (ye > P.y_end - P.G && (P.send_hi || (p2p && P.peer_hi[0]))));
 
   // register FIFOs (entry = step index mod 3): values this thread produced,
   // old black values it loaded, constants level 0 loaded for level 1
@@ -419,7 +423,7 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
         (k ? OUT1 : OUT0)[ro] = Vownb1;
         (k ? OUT0 : OUT1)[ro] = b1;
       }
-      if constexpr (SLAB) {
+      if (SLAB && send_cta) {
         const int rr = y - 4;
         const bool red_odd = (q ^ k) != 0;
         const double ve = red_odd ? b1 : Vownb1, vo = red_odd ? Vownb1 : b1;
@@ -429,11 +433,13 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
           double *sb = slo + ((int64_t)l * P.G + (rr - P.y_begin)) * P.NXP;
           sb[gp] = ve;
           sb[gp + P.HP] = vo;
+          wrote_peer = true;
         }
         if (shi && rr >= P.y_end - P.G) {
           double *sb = shi + ((int64_t)l * P.G + (rr - (P.y_end - P.G))) * P.NXP;
           sb[gp] = ve;
           sb[gp + P.HP] = vo;
+          wrote_peer = true;
         }
       }
     }
@@ -474,22 +480,38 @@ done:
   if (!exact_lane) dmax = 0.0;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
-  if ((tid & 31) == 0)
-    atomicMax(&ctl->dmax[j & (kRing - 1)], static_cast<unsigned long long>(__double_as_longlong(dmax)));
+  // one atomic per CTA (warp maxima combined in shared memory first)
+  __shared__ unsigned long long cta_max;
+  if (tid == 0) cta_max = 0ull;
+  __syncthreads();
+  if ((tid & 31) == 0) atomicMax(&cta_max, static_cast<unsigned long long>(__double_as_longlong(dmax)));
+  // Peer exchange: boundary rows (plain stores into peer memory) are made
+  // visible system wide by the threads that stored them before the CTA counts
+  // itself done
+  if (SLAB && p2p && wrote_peer) __threadfence_system();
+  __syncthreads();
+  if (tid == 0) atomicMax(&ctl->dmax[j & (kRing - 1)], cta_max);
   if constexpr (SLAB) {
     if (p2p) {
-      // this CTA's boundary rows (plain stores into peer memory) and its norm
-      // reach every slab before its arrival count does
-      __shared__ unsigned long long cta_max;
-      if (tid == 0) cta_max = 0ull;
-      __syncthreads();
-      if ((tid & 31) == 0) atomicMax(&cta_max, static_cast<unsigned long long>(__double_as_longlong(dmax)));
-      __threadfence_system();
-      __syncthreads();
+      // every CTA adds its norm to this slab's slot and counts itself done;
+      // the last CTA of the launch then max-reduces the slab's norm into every
+      // other slab's slot and bumps every slab's arrival counter (2 N remote
+      // atomics per launch)
       if (tid == 0) {
-        for (int r = 0; r < P.nranks; ++r) atomicMax_system(P.pnorm_all[r] + (e & 3), cta_max);
-        __threadfence_system();
-        for (int r = 0; r < P.nranks; ++r) atomicAdd_system(P.sig_all[r], 1ull);
+        atomicMax(&ctl->pnorm[e & 3], cta_max);
+        __threadfence();
+        const unsigned int done = atomicAdd(&ctl->ccount[e & 3], 1u) + 1u;  // (after this CTA's norm)
+        if (done == gridDim.x * gridDim.y) {  // last CTA of this slab's launch e
+          // slot e + 2 is next counted by launch e + 2, which starts after every
+          // slab finished e + 1; its previous user, launch e - 2, is complete
+          ctl->ccount[(e + 2) & 3] = 0u;
+          __threadfence_system();
+          const unsigned long long m = *(volatile unsigned long long *)&ctl->pnorm[e & 3];
+          for (int r = 0; r < P.nranks; ++r)
+            if (P.pnorm_all[r] != ctl->pnorm) atomicMax_system(P.pnorm_all[r] + (e & 3), m);
+          __threadfence_system();
+          for (int r = 0; r < P.nranks; ++r) atomicAdd_system(P.sig_all[r], 1ull);
+        }
       }
     }
   }

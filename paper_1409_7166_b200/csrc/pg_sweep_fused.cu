@@ -177,7 +177,6 @@ bool fill_fused_params(pg_grid *g, FusedParams &P, double omega, double tol, int
   P.pre = 0;
   P.p2p = 0;
   P.nranks = 1;
-  P.total_ctas = 0;
   const SlabHalo &h = g->hx;
   const bool halo = g->slab && h.G > 0;
   P.has_rlo = halo && h.has_lo;

@@ -181,7 +181,6 @@ struct FusedParams {
   // k_rb_sweep2 slab with the peer-memory exchange (SlabHalo::p2p)
   CUtensorMap mRlo_b, mRhi_b;  // parity-1 receive buffers
   int32_t p2p, nranks;
-  int64_t total_ctas;
   double *peer_lo[2], *peer_hi[2];
   unsigned long long *sig_all[8], *pnorm_all[8];
 };
