@@ -159,3 +159,108 @@ def test_monolithic_model_is_the_oracle_iteration():
                                          order=nodal.red_black_order(m.layers, m.ny, m.nx),
                                          Itab=pwl.node_currents_table(nl, m.h, steps))
     np.testing.assert_allclose(mono.V.reshape(-1), ro.V[-1], rtol=0, atol=1e-12)
+
+
+# ------------------------------------------ peer-memory protocol (gloo model)
+def _worker_p2p(rank, world, port, F, steps, k_max, tol, omega, repeat, out):
+    """The peer-memory exchange of DESIGN.md §10 with real processes: receive
+    buffers double-buffered by launch epoch e (launch e reads parity e & 1,
+    its boundary rows land in the neighbours' parity (e + 1) & 1 buffers),
+    the epoch counts working launches and continues across transients, the
+    receive buffers are seeded from x(0) at a transient's start and unpacked
+    into V after a step's last launch.  Remote stores are modelled by
+    send/recv into the parity buffer, the arrival wait by their completion and
+    the remote norm maxima by an allreduce."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import torch
+    m = mesh()
+    G = 2 * F
+    sp = slab.slab_spec(m.ny, rank, world, G)
+    sm = slab.slab_mesh(m, sp)
+    rows = (1 if rank > 0 else 0, sm.ny - 1 if rank < world - 1 else sm.ny)
+    md = slab_model.Model(sm, row0=sp.lo, rows=rows, owned=(sp.y_begin, sp.y_end))
+    shape = (sm.layers, G, sm.nx)
+    recv = {(side, p): np.zeros(shape) for side in ("lo", "hi") for p in (0, 1)}
+    lo, hi = rank > 0, rank < world - 1
+    epoch = 0
+
+    def ghosts_from(p):
+        if lo:
+            md.V[:, sp.y_begin - G:sp.y_begin] = recv[("lo", p)]
+        if hi:
+            md.V[:, sp.y_end:sp.y_end + G] = recv[("hi", p)]
+
+    def store_to_neighbours(p):
+        ops, bufs = [], {}
+        if lo:
+            ops.append(dist.P2POp(dist.isend, torch.from_numpy(np.ascontiguousarray(
+                md.V[:, sp.y_begin:sp.y_begin + G])), rank - 1))
+            bufs["lo"] = torch.zeros(shape, dtype=torch.float64)
+            ops.append(dist.P2POp(dist.irecv, bufs["lo"], rank - 1))
+        if hi:
+            ops.append(dist.P2POp(dist.isend, torch.from_numpy(np.ascontiguousarray(
+                md.V[:, sp.y_end - G:sp.y_end])), rank + 1))
+            bufs["hi"] = torch.zeros(shape, dtype=torch.float64)
+            ops.append(dist.P2POp(dist.irecv, bufs["hi"], rank + 1))
+        for w in dist.batch_isend_irecv(ops) if ops else []:
+            w.wait()
+        for side, t in bufs.items():
+            recv[(side, p)] = t.numpy().copy()
+
+    def allmax(x):
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    runs = []
+    for _ in range(repeat):
+        md.V[:] = m.vdd                           # x(0)
+        if lo:                                    # seed parity epoch & 1 from x(0)
+            recv[("lo", epoch & 1)] = md.V[:, sp.y_begin - G:sp.y_begin].copy()
+        if hi:
+            recv[("hi", epoch & 1)] = md.V[:, sp.y_end:sp.y_end + G].copy()
+        sweeps = []
+        for s in range(1, steps + 1):
+            b = md.rhs(s)
+            k = 0
+            while True:
+                ghosts_from(epoch & 1)
+                d = md.launch(b, F, omega)
+                store_to_neighbours((epoch + 1) & 1)
+                d = allmax(d)                     # pnorm[e & 3] after the arrival wait
+                epoch += 1
+                k += F
+                if (tol > 0 and d < tol) or k >= k_max:
+                    break
+            ghosts_from(epoch & 1)                # end-of-step unpack into V
+            sweeps.append(k)
+        runs.append((md.V[:, sp.y_begin:sp.y_end].copy(), sweeps))
+    out[rank] = (sp.y0, sp.y1, runs, epoch)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,tol", [(2, 0.0), (3, 1e-11)])
+def test_gloo_p2p_protocol_equals_monolithic(world, tol):
+    F, steps, omega, repeat = 2, 3, 1.7, 2
+    k_max = 6 if tol == 0 else 100000
+    port = _free_port()
+    with mp.Manager() as mgr:
+        out = mgr.dict()
+        mp.spawn(_worker_p2p, args=(world, port, F, steps, k_max, tol, omega, repeat, out), nprocs=world,
+                 join=True)
+        res = dict(out)
+    m = mesh()
+    mono = slab_model.Model(m)
+    sweeps = slab_model.run([mono], lambda: None, lambda x: x, steps, F, k_max, tol, omega)
+    epochs = {res[r][3] for r in range(world)}
+    assert epochs == {repeat * sum(sweeps) // F}      # every rank counted the same launches
+    for rep in range(repeat):                         # a second transient continues the epochs
+        V = np.zeros_like(mono.V)
+        for r in range(world):
+            y0, y1, runs, _ = res[r]
+            Vo, sw = runs[rep]
+            V[:, y0:y1] = Vo
+            assert sw == sweeps, (r, rep, sw, sweeps)
+        np.testing.assert_array_equal(V, mono.V)
