@@ -52,19 +52,6 @@
 
 namespace pgb {
 
-namespace {
-
-template <int A, int B, class Fn>
-__device__ __forceinline__ void static_for(Fn &&fn) {
-  if constexpr (A < B) {
-    fn(std::integral_constant<int, A>{});
-    static_for<A + 1, B>(fn);
-  }
-}
-
-
-}  // namespace
-
 template <int L, int W>
 struct Sweep2Geo {
   static constexpr int RW = 2 * W;                    // doubles per layer row of a strip

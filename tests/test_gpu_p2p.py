@@ -117,3 +117,31 @@ def test_p2p_single_slab_uses_graphs_and_pdl(pgb):
     rn, Vn = grouped(pgb, g, 1, steps, 1e-10, omega, 200000, repeat=2)
     np.testing.assert_array_equal(rn.sweeps, r1.sweeps)
     np.testing.assert_array_equal(Vn, V1)
+
+
+def test_p2p_ipc_group_one_rank(pgb):
+    # the CUDA-IPC setup path (create, export, all-gather over torch.distributed,
+    # connect) with one rank: nothing to map, the records still round-trip
+    import os
+    import socket
+    import torch.distributed as dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        g = gridgen.config_grid(0, dims=(4, 64, 80), steps=6)
+        grp = pgb.SlabGroup.p2p(g, 0, 1, fuse=2)
+        rn = grp.transient(g.h, 6, tol=1e-10, omega=1.9, max_sweeps=200000)
+        V = np.zeros((g.layers, g.ny, g.nx))
+        for sp, Vo in grp.owned_voltages(g):
+            V[:, sp.y0:sp.y1, :] = Vo
+        grp.close()
+    finally:
+        dist.destroy_process_group()
+    r1, V1 = single(pgb, g, 6, 1e-10, 1.9, 200000)
+    np.testing.assert_array_equal(rn.sweeps, r1.sweeps)
+    np.testing.assert_array_equal(V, V1)
