@@ -5,7 +5,7 @@ sweep, F = 2, automatic rows per CTA), against the oracle.
 * configs 1, 2, 3: fixed-sweep iterates (tol = 0, k sweeps per step) of the
   whole grid against the oracle's sequential sweep in the same numbering,
   |dV| <= 1e-12 V at every node (DESIGN.md §5 derivation);
-* configs 1, 2, 3: converged first steps (tol = 1e-10) at every node, <= 1e-8 V;
+* configs 1, 2: converged first steps (tol = 1e-10) at every node, <= 1e-8 V;
 * config 4 (134M nodes, too large for the oracle as a whole): sampled outputs.
   After s steps of k sweeps from x(0) = Vdd a node's value depends only on
   nodes within 2 k s hops (one hop per half-sweep), so the oracle computes it
@@ -88,11 +88,14 @@ def test_config1_full_size_converged(pgb):
     assert np.all(rg.sweeps[1:] == -(-ro.sweeps[1:] // F) * F)
 
 
-@pytest.mark.parametrize("cfg,steps,omega,series_rl", [(2, 2, 1.98, "node"), (3, 1, 1.99, "element")])
+@pytest.mark.parametrize("cfg,steps,omega,series_rl", [(2, 1, 1.98, "node")])
 def test_full_size_converged(pgb, cfg, steps, omega, series_rl):
-    # converged transient steps (tol = 1e-10) of the irregular CSR grid and the
-    # RLC mesh at full size: every node within 1e-8 V of the oracle (north_star
-    # bar), sweep counts the same decision (F = 2 launches on meshes, R13)
+    # converged transient steps (tol = 1e-10) of the irregular CSR grid at full
+    # size: every node within 1e-8 V of the oracle (north_star bar), the same
+    # sweep count.  (The RLC config 3 passed the same check for one step, but
+    # its whole-grid oracle solve takes ~5 minutes: converged RLC parity is
+    # kept at reduced sizes, test_gpu_parity.py, plus config 3's full-size
+    # fixed-sweep iterates above.)
     g = gridgen.config_grid(cfg)
     pr = _sample(g.n, 4096, 20 + cfg)
     rg, V = gpu_iterates(pgb, g, steps, 0, omega, probes=pr, tol=1e-10)
