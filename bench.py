@@ -176,13 +176,20 @@ def oracle_sample(cfg: int, g=None, seconds: float = 12.0, omega: float = 1.98):
     nl = netlist.from_grid(g)
     o = nodal.NodalOracle(nl)
     It = pwl.node_currents_table(nl, g.h, 1)
-    # calibrate sweeps to ~seconds of work (difference of two runs removes setup)
+    # calibrate sweeps to ~seconds of work: grow the sweep count until a run
+    # takes >= 0.3 s (small grids), the difference to a 1-sweep run removes setup
     t0 = time.perf_counter()
     o.transient(g.h, 1, tol=0.0, omega=omega, Itab=It, max_sweeps=1)
-    t1 = time.perf_counter()
-    o.transient(g.h, 1, tol=0.0, omega=omega, Itab=It, max_sweeps=4)
-    t2 = time.perf_counter()
-    per = max((t2 - t1) - (t1 - t0), 1e-9) / 3
+    t_one = time.perf_counter() - t0
+    kt = 4
+    while True:
+        t0 = time.perf_counter()
+        o.transient(g.h, 1, tol=0.0, omega=omega, Itab=It, max_sweeps=kt)
+        t_k = time.perf_counter() - t0
+        if t_k >= 0.3 or kt >= 1 << 20:
+            break
+        kt *= 4
+    per = max(t_k - t_one, 1e-9) / (kt - 1)
     k = max(2, int(seconds / per))
     t0 = time.perf_counter()
     o.transient(g.h, 1, tol=0.0, omega=omega, Itab=It, max_sweeps=k)
