@@ -133,9 +133,6 @@ PG_API int pg_set_stream(pg_grid *g, void *stream);
  *   "pdl"    1 (default): consecutive sweep launches of a single grid use
  *            programmatic dependent launch (the next launch's prologue and
  *            constant-row loads overlap the previous launch's tail); 0: off
- *   "l2ahead" rows of L2 prefetch (cp.async.bulk.prefetch) beyond the shared-
- *            memory ring in the two-level pipeline kernel, 0..16 (default 0:
- *            measured fastest; the prefetch costs 50 % on the 134M-node mesh)
  *   "l2keep" / "l2first" L2 eviction policy of the pipeline kernel, 6-bit
  *            masks over (gx, gy, gz_eff, b, 1/d, V): l2keep bits 0-4 read that
  *            constant array with evict_last, bit 5 writes V with evict_last;

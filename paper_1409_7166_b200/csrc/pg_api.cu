@@ -341,9 +341,6 @@ PG_API int pg_set_option(pg_grid *g, const char *key, int64_t value) {
     g->pipe = value != 0;
   } else if (k == "pdl") {
     g->pdl = value != 0;
-  } else if (k == "l2ahead") {
-    REQUIRE(value >= 0 && value <= 16, "l2ahead must be in 0..16");
-    g->l2ahead = (int)value;
   } else if (k == "l2keep") {
     REQUIRE(value >= -1 && value < 64, "l2keep is a 6-bit mask (gx, gy, gz, b, 1/d, V) or -1 (auto)");
     g->l2keep = (int)value;

@@ -163,7 +163,6 @@ struct pg_grid {
   int use_graph = 1;                   // option "graph": replay captured sweep batches
   int resident = 1;                    // option "resident": one-CTA sweep loop for tiny meshes
   int pipe = 1;                        // option "pipe": two-level pipeline kernel for full F = 2 launches
-  int l2ahead = 0;                     // option "l2ahead": rows of L2 prefetch beyond the ring (k_rb_sweep2; 0: none, measured fastest)
   int l2first = -1;                    // option "l2first": arrays read with evict_first (bit mask, -1: auto)
   int l2keep = -1;                     // option "l2keep": arrays kept in L2 across launches (bit mask, -1: auto)
   int l2promo = 256;                   // option "l2promo": TMA L2 promotion bytes (0, 64, 128, 256)

@@ -132,7 +132,6 @@ cudaError_t launch_rb_sweep2(pg_grid *g, double omega, double tol, int j, int ro
     if (P.p2p && h.has_lo) P.mRlo_b = h.mlo_b[wi];
     if (P.p2p && h.has_hi) P.mRhi_b = h.mhi_b[wi];
   }
-  P.l2ahead = g->l2ahead;
   // L2 policy (auto): a mesh whose per-launch footprint (56 B per storage
   // element) is below twice the L2 streams its reads evict_first and writes V
   // evict_last, so the next launch finds V in L2 (config 1: +4 %); larger

@@ -114,13 +114,15 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
   // footprint, pg_sweep2.cu): evict_last / evict_first hints on the TMA
   // copies; policy 0 = plain copy without a cache hint (measured faster than
   // an explicit evict_normal hint on config 4)
-  const uint64_t pol_last = policy_evict_last(), pol_first = policy_evict_first();
+  const uint64_t pol_last = policy_evict_last(), pol_first = policy_evict_first(),
+                 pol_normal = policy_evict_normal();
   auto pol = [&](int a) -> uint64_t {
-    return (a < 5 && ((P.l2keep >> a) & 1)) ? pol_last : (((P.l2first >> a) & 1) ? pol_first : 0ull);
+    return (a < 5 && ((P.l2keep >> a) & 1)) ? pol_last : (((P.l2first >> a) & 1) ? pol_first : pol_normal);
   };
+  // one copy instruction sequence per call site (the refill code is
+  // replicated in each of the 12 unrolled steps)
   auto tma = [&](void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int y, uint64_t p) {
-    if (p) tma4h(dst, map, bar, c0, y, p);
-    else tma4(dst, map, bar, c0, y);
+    tma4h(dst, map, bar, c0, y, p);
   };
 
   auto c_dst = [&](int r, int a) { return cring + ((r - r_first) % SC) * CST + a * Gm::LAY + (a >= 2 ? RW : 0); };
@@ -212,16 +214,10 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
   // mid) and their stage offsets are a * LAY (+ RW from gz_eff on), so every
   // copy is the same instruction sequence (small code: it is replicated in
   // each of the 12 unrolled steps).
-  const int kL2Ahead = P.l2ahead;
   auto v_copy = [&](int rv_row, int r) {  // V row rv_row into its slot, completing group r
     int rv;
     const CUtensorMap *m = v_src(rv_row, rv);
     tma(vring + ((rv_row - r_first) % SV) * VST, m, c_bar(r), ps, rv, pol(5));
-  };
-  auto v_prefetch = [&](int rv_row) {
-    int rv;
-    const CUtensorMap *m = v_src(rv_row, rv);
-    tma4_prefetch(m, ps, rv);
   };
   if (tid == 0) {
     for (int r = r_first; r < r_first + n_init; ++r) {
@@ -233,40 +229,28 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
       if (v1) v_copy(r + 1, r);
       if (v0) v_copy(r, r);
     }
-    if (kL2Ahead > 0)
-      for (int r = r_first + SC; r < r_first + SC + kL2Ahead && r <= r_last; ++r) {
-        for (int a = 0; a < 5; ++a) tma4_prefetch(mC + a, ps, r);
-        if (r + 1 <= r_last) v_prefetch(r + 1);
-      }
   }
   const int warp = tid >> 5;
   // refill after the barrier of step y: group R = y + 4 (slots of constant row
   // y - 2 and V row y - 7).  Lane 0 of warp w issues op w (w + NWARP, ...):
-  // ops 0..4 constant array a = op (op 0 also posts expect_tx), 5: V row R + 1,
-  // 6: L2 prefetch of group R + PG_L2_AHEAD.
+  // ops 0..4 constant array a = op (op 0 also posts expect_tx), 5: V row
+  // R + 1.  The operands are computed, so each unrolled step holds a single
+  // copy instruction sequence (the loop body is larger than the instruction
+  // cache: measured +4 % for halving the refill code).
   // cs / vs: ring slots of constant row R and V row R + 1 (compile-time in the
   // unrolled steps: (u + 5) mod SC and (u + 6) mod SV)
   auto refill = [&](const int y, const int cs, const int vs) {
     const int R = y + 4;
     if ((tid & 31) == 0 && R >= r_first + SC && R <= r_last) {
       uint64_t *bar = &gbar[cs];
-      double *cdst = cring + cs * CST;
 #pragma unroll 1
-      for (int op = warp; op < 7; op += Gm::NWARP) {
-        if (op < 5) {
-          if (op == 0) mbar_expect_tx(bar, Gm::CBYTES + (R + 1 <= r_last ? Gm::VBYTES : 0u));
-          tma(cdst + op * Gm::LAY + (op >= 2 ? RW : 0), mC + op, bar, ps, R, pol(op));
-        } else if (op == 5) {
-          if (R + 1 <= r_last) {
-            int rv;
-            const CUtensorMap *m = v_src(R + 1, rv);
-            tma(vring + vs * VST, m, bar, ps, rv, pol(5));
-          }
-        } else if (kL2Ahead > 0 && R + kL2Ahead <= r_last) {
-#pragma unroll 1
-          for (int a = 0; a < 5; ++a) tma4_prefetch(mC + a, ps, R + kL2Ahead);
-          if (R + kL2Ahead + 1 <= r_last) v_prefetch(R + kL2Ahead + 1);
-        }
+      for (int op = warp; op < 6; op += Gm::NWARP) {
+        if (op == 0) mbar_expect_tx(bar, Gm::CBYTES + (R + 1 <= r_last ? Gm::VBYTES : 0u));
+        if (op == 5 && R + 1 > r_last) break;
+        int yy = R;
+        const CUtensorMap *m = op < 5 ? mC + op : v_src(R + 1, yy);
+        double *dst = op < 5 ? cring + cs * CST + op * Gm::LAY + (op >= 2 ? RW : 0) : vring + vs * VST;
+        tma(dst, m, bar, ps, yy, pol(op));
       }
     }
   };

@@ -174,7 +174,6 @@ struct FusedParams {
   double *send_lo, *send_hi;
   int32_t has_rlo, has_rhi, G;
   int32_t pre;      // k_rb_sweep2: the previous kernel in the stream is a sweep launch (PDL prologue)
-  int32_t l2ahead;  // k_rb_sweep2: rows of L2 prefetch beyond the ring (0: none)
   int32_t l2keep;   // k_rb_sweep2: bit a < 5: constant array a (gx, gy, gz_eff, b, 1/d) read with L2 evict_last;
                     // bit 5: V written with evict_last (the next launch reads it)
   int32_t l2first;  // k_rb_sweep2: arrays read with evict_first (bits as above, bit 5: V reads); others evict_normal
