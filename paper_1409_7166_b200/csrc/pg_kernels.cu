@@ -137,7 +137,8 @@ struct CsrArgs {
   DevCtl *ctl;
 };
 
-// streamed loads with an L2 eviction policy (createpolicy)
+// streamed loads with an L2 eviction policy (createpolicy); not volatile: they
+// read arrays no kernel of the sweep writes, so the compiler may schedule them
 __device__ __forceinline__ uint64_t pol_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -145,17 +146,17 @@ __device__ __forceinline__ uint64_t pol_first() {
 }
 __device__ __forceinline__ double ldf(const double *p, uint64_t pol) {
   double v;
-  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
   return v;
 }
 __device__ __forceinline__ int32_t ldi(const int32_t *p, uint64_t pol) {
   int32_t v;
-  asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  asm("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
   return v;
 }
 __device__ __forceinline__ int64_t ldl(const int64_t *p, uint64_t pol) {
   int64_t v;
-  asm volatile("ld.global.nc.L2::cache_hint.s64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+  asm("ld.global.nc.L2::cache_hint.s64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
   return v;
 }
 
