@@ -212,12 +212,15 @@ def run_reference(args):
     vals = []
     t_all = 0.0
     for _ in range(args.steps):
+        t0 = time.perf_counter()
         r = oracle_sample(cfg, g, seconds=per_step, omega=omega)
+        t_all += time.perf_counter() - t0
         vals.append(r["value"])
     v = statistics.mean(vals)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": 1e3 * t_all / max(args.steps, 1), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded BASELINE.json recipe)",
             "config": {"workload": f"config{cfg}", "nodes": g.n},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
