@@ -693,8 +693,21 @@ PG_API int pg_group_transient(pg_group *grp, double h, int64_t steps, double tol
     for (pg_grid *g : grp->slabs)
       if ((rc = check_p2p(g))) return rc;
   }
+  // a sweep-batch graph captured inside the group bakes the armed peer
+  // protocol in (and one captured outside does not): recapture on entry / exit
+  auto drop_graphs = [&] {
+    for (pg_grid *g : grp->slabs)
+      if (g->batch_exec) {
+        cudaGraphExecDestroy(g->batch_exec);
+        g->batch_exec = nullptr;
+      }
+  };
+  for (pg_grid *g : grp->slabs) g->group_active = true;
+  drop_graphs();
   const int rc = run_transient(grp->slabs.data(), (int)grp->slabs.size(), grp, h, steps, tol, omega,
                                PG_METHOD_RBSOR, max_sweeps, 0, nullptr, nullptr, PG_MEM_HOST, sweeps_out, stats);
+  for (pg_grid *g : grp->slabs) g->group_active = false;
+  drop_graphs();
   if (grp->p2p())
     for (pg_grid *g : grp->slabs)
       if (g->ctl_host->p2p_timeout) {

@@ -168,6 +168,7 @@ struct pg_grid {
   int l2promo = 256;                   // option "l2promo": TMA L2 promotion bytes (0, 64, 128, 256)
   int pdl = 1;                         // option "pdl": programmatic dependent launch of consecutive sweeps
   bool pdl_ok = false;                 // set by run_transient: single grid, no exchange between launches
+  bool group_active = false;           // inside pg_group_transient (peer exchange armed)
   cudaGraphExec_t batch_exec = nullptr;  // captured batch of `batch` full sweep launches
   cudaStream_t cap_stream = nullptr;     // private stream the batch graph is captured on
   double graph_key[6] = {0, 0, 0, 0, 0, 0};  // omega, tol, method, F, batch, stream of the capture

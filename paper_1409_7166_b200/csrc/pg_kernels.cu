@@ -378,9 +378,9 @@ __global__ void k_ind_update_pads(int64_t npad, const int64_t *idx, const double
 
 // ------------------------------------------------------------------ bookkeeping
 __global__ void k_step_end(DevCtl *c, int64_t s, int32_t launched, int32_t flips, int32_t fused,
-                           int64_t max_sweeps, double tol, int64_t *rec) {
+                           int64_t max_sweeps, double tol, int64_t *rec, int32_t count_epoch) {
   const int64_t ran = c->done ? c->launches_done : launched;
-  c->epoch += ran;  // sweep launches that did work (peer-exchange epochs)
+  if (count_epoch) c->epoch += ran;  // sweep launches that did work in an armed peer group
   int64_t sw = ran * fused;
   if (sw > max_sweeps) sw = max_sweeps;
   if (flips) c->base ^= (int32_t)(ran & 1);
@@ -851,7 +851,9 @@ cudaError_t launch_batch_advance(pg_grid *g, int nb) {
 
 cudaError_t launch_step_end(pg_grid *g, int64_t s, int launched, int flips, int fused,
                             int64_t max_sweeps, double tol) {
-  k_step_end<<<1, 1, 0, g->stream>>>(g->ctl, s, launched, flips, fused, max_sweeps, tol, g->dev_sweeps);
+  const int count_epoch = g->slab && g->hx.G > 0 && g->hx.p2p && g->group_active;
+  k_step_end<<<1, 1, 0, g->stream>>>(g->ctl, s, launched, flips, fused, max_sweeps, tol, g->dev_sweeps,
+                                     count_epoch);
   return cudaGetLastError();
 }
 

@@ -118,7 +118,9 @@ cudaError_t launch_rb_sweep2(pg_grid *g, double omega, double tol, int j, int ro
   P.pre = pdl ? 1 : 0;
   {
     const SlabHalo &h = g->hx;
-    P.p2p = (g->slab && h.G > 0 && h.p2p) ? 1 : 0;
+    // the peer protocol waits on the other slabs: armed only while the group
+    // runs (a slab grid used alone, e.g. pg_dc, sweeps without it)
+    P.p2p = (g->slab && h.G > 0 && h.p2p && g->group_active) ? 1 : 0;
     P.nranks = h.nranks;
     for (int k = 0; k < 2; ++k) {
       P.peer_lo[k] = h.peer_lo[k];

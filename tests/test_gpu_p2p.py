@@ -145,3 +145,20 @@ def test_p2p_ipc_group_one_rank(pgb):
     r1, V1 = single(pgb, g, 6, 1e-10, 1.9, 200000)
     np.testing.assert_array_equal(rn.sweeps, r1.sweeps)
     np.testing.assert_array_equal(V, V1)
+
+
+def test_p2p_slab_grid_alone_is_refused(pgb):
+    # a slab grid of a peer group cannot be swept on its own (its launches
+    # would wait for slabs that are not running, and advance its epoch alone);
+    # the library refuses, and the group keeps working
+    g = gridgen.mesh_grid(2, 40, 30, seed=4, pad_pitch=5, h=10e-12, src_start=5e-12, src_width=30e-12)
+    grp = pgb.SlabGroup.local(g, 2, fuse=2, transport="p2p")
+    r1 = grp.transient(g.h, 2, tol=1e-10, omega=1.8, max_sweeps=200000)
+    G = grp.grids[0]
+    with pytest.raises(pgb.PgError):
+        G.dc(t=20e-12, tol=1e-9, omega=1.9, max_sweeps=20000)
+    with pytest.raises(pgb.PgError):
+        G.transient(g.h, 1, tol=1e-10, omega=1.8)
+    r2 = grp.transient(g.h, 2, tol=1e-10, omega=1.8, max_sweeps=200000)
+    assert np.array_equal(r1.sweeps, r2.sweeps)
+    grp.close()
