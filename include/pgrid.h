@@ -242,12 +242,24 @@ PG_API int pg_group_local(int32_t n, pg_grid *const *slabs, int32_t ghost, pg_gr
  * 8 slabs.  All slabs must run the same transients.  A wait that exceeds ~4 s
  * (a missing peer) makes pg_group_transient return PG_ECUDA.
  *
+ * Arguments and ownership: slabs / slab are grids marked with pg_set_slab
+ * (rank r of nranks, `ghost` rows of each neighbour, the layout of
+ * pg_group_local); the group keeps pointers to them (destroy the group before
+ * the grids) and owns its receive buffers and mapped peer memory
+ * (pg_group_destroy releases them).  A slab grid of a group cannot be swept on
+ * its own (pg_transient / pg_dc return PG_EINVAL).
+ *
  * pg_group_local_p2p: n slabs on the current device in one process (their
  *   "peers" are each other's buffers; the launches are ordered on one stream).
  * pg_group_p2p_create / _export / _connect: one slab per process and GPU;
- *   export this rank's record (CUDA IPC handles of its receive buffers and
- *   control block; *len bytes, blob may be NULL to query the size), gather the
- *   records of all ranks ordered by rank (e.g. torch.distributed), connect. */
+ *   export this rank's record into blob (cap bytes available; *len receives
+ *   the record size; blob may be NULL to query it; the record holds the CUDA
+ *   IPC handles of the receive buffers and control block), gather the records
+ *   of all ranks concatenated in rank order (e.g. torch.distributed
+ *   all_gather), pass them with blob_len = the record size to connect, then
+ *   barrier before the first transient.  Errors: PG_EINVAL for bad ranks,
+ *   ghost rows, options or inconsistent records; PG_ECUDA when a CUDA call
+ *   (IPC mapping) fails. */
 PG_API int pg_group_local_p2p(int32_t n, pg_grid *const *slabs, int32_t ghost, pg_group **out);
 PG_API int pg_group_p2p_create(pg_grid *slab, int32_t nranks, int32_t rank, int32_t ghost, pg_group **out);
 PG_API int pg_group_p2p_export(pg_group *grp, void *blob, int64_t cap, int64_t *len);
