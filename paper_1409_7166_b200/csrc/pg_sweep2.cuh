@@ -158,6 +158,9 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
         __nanosleep(64);
       }
       __threadfence();
+      // the ghost rows arrived through the generic proxy (peer stores); this
+      // CTA reads them with TMA (async proxy)
+      asm volatile("fence.proxy.async.global;" ::: "memory");
     }
     __syncthreads();
     if (j > 0 && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0)  // the global norm, for k_step_end
