@@ -79,6 +79,11 @@ struct JacobiArgs {
 };
 
 __global__ void __launch_bounds__(256) k_jacobi_mesh(JacobiArgs a) {
+  // one row (layer l, row y) of the parity-split layout per blockIdx.y step,
+  // storage position p = threadIdx.x + blockIdx.x * blockDim.x inside the row:
+  // no integer division per node, x neighbours at fixed offsets (the even
+  // node 2p has odd neighbours at HP + p - 1 and HP + p, the odd node 2q + 1
+  // even neighbours at q and q + 1), coalesced loads of every array
   __shared__ double wmax[8];
   a.launch_idx += *(volatile int32_t *)&a.ctl->jbase;
   if (sweep_skip(a.ctl, a.launch_idx, a.tol, true)) return;
@@ -89,22 +94,26 @@ __global__ void __launch_bounds__(256) k_jacobi_mesh(JacobiArgs a) {
   double *Vout = par ? a.V0 : a.V1;
   const double w = a.omega;
   double dmax = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.np;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t l = i / d.layer_stride;
-    const int64_t y = (i - l * d.layer_stride) / d.NXP;
-    const int64_t x = mesh_col(d, i);
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool odd = p >= d.HP;
+  const int h = odd ? p - d.HP : p;
+  const int x = 2 * h + (odd ? 1 : 0);
+  // storage offsets (within the row) of the west / east neighbours
+  const int pw = odd ? h : d.HP + h - 1, pe = odd ? h + 1 : d.HP + h;
+  const bool in_row = p < d.NXP;
+  for (int64_t r = blockIdx.y; r < (int64_t)d.L * d.NY; r += gridDim.y) {
+    if (!in_row) continue;
+    const int64_t l = r / d.NY, y = r - l * d.NY;
+    const int64_t base = l * d.layer_stride + y * d.NXP;
+    const int64_t i = base + p;
     const double vc = __ldg(Vin + i);
     if (x >= d.NX) {
       Vout[i] = vc;
       continue;
     }
     double s = __ldg(a.b + i);
-    if (x + 1 < d.NX) s = fma(__ldg(a.gx + i), __ldg(Vin + mesh_index(d, l, y, x + 1)), s);
-    if (x > 0) {
-      const int64_t j = mesh_index(d, l, y, x - 1);
-      s = fma(__ldg(a.gx + j), __ldg(Vin + j), s);
-    }
+    if (x + 1 < d.NX) s = fma(__ldg(a.gx + i), __ldg(Vin + base + pe), s);
+    if (x > 0) s = fma(__ldg(a.gx + base + pw), __ldg(Vin + base + pw), s);
     if (y + 1 < d.NY) s = fma(__ldg(a.gy + i), __ldg(Vin + i + d.NXP), s);
     if (y > 0) s = fma(__ldg(a.gy + i - d.NXP), __ldg(Vin + i - d.NXP), s);
     if (l + 1 < d.L) s = fma(__ldg(a.gz + i), __ldg(Vin + i + d.layer_stride), s);
@@ -816,7 +825,12 @@ cudaError_t launch_sweep(pg_grid *g, int method, double omega, double tol, int j
     a.omega = omega; a.tol = tol; a.ctl = g->ctl; a.launch_idx = j;
     a.V0 = g->V[0];
     a.V1 = g->V[1];
-    k_jacobi_mesh<<<grid_for(g->np, 256, g->num_sms), 256, 0, g->stream>>>(a);
+    {
+      const int bx = (g->md.NXP + 255) / 256;
+      const int64_t rows = (int64_t)g->md.L * g->md.NY;
+      const int by = (int)std::min<int64_t>(rows, std::max<int64_t>(1, (int64_t)g->num_sms * 8 / bx));
+      k_jacobi_mesh<<<dim3(bx, by), 256, 0, g->stream>>>(a);
+    }
     ++*launches;
   } else {
     CsrArgs a;
