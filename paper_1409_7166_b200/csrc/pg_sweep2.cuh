@@ -428,7 +428,10 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
     if (y + 1 <= r_last) mbar_wait(&gbar[(u + 2) % SC], (uint32_t)(((u + 2) / SC) & 1));
     phaseB(U_, y);
     phaseA(std::integral_constant<int, u + 1>{}, y + 1);
-    fence_proxy_async();
+    // generic accesses to a V slot end 3 (reads) / 5 (writes) bodies before the
+    // barrier after which TMA refills it: a proxy fence every second body
+    // orders them (the fence also waits for this thread's global write-out)
+    if constexpr (u % 2 == 1) fence_proxy_async();
   };
 
   // the first step's north operand: old black of row r_first in the column of
