@@ -34,10 +34,19 @@
 //   update, so they are never stored to shared memory, only written out.
 // * A zero "layer -1" block before the gz_eff array of each constant stage
 //   makes the layer-0 lower via conductance 0 without a branch.
+// * Small loop code: the 12-step body is larger than the instruction cache,
+//   so each refill site holds one copy instruction sequence with computed
+//   operands and an explicit L2 policy (auto: stream the reads, keep the
+//   written V for the next launch), and the proxy fence that orders the
+//   ring's generic accesses before its TMA refills runs every second step.
+// * Programmatic dependent launch (constant rows requested before
+//   griddepcontrol.wait) and, in a peer-memory slab group, the halo exchange
+//   and the global norm fused into the kernel's tail.
 //
 // Streaming step y (u = y - r_first - 1, compile-time modulo 12):
-//   phase A: red_0(y), red_1(y - 3)          | fence.proxy.async; bar 1
+//   phase A: red_0(y), red_1(y - 3)          | (fence.proxy.async); barrier
 //   phase B: black_0(y - 1), black_1(y - 4)  | write row y - 4 (both colours)
+// Phase B(y) and phase A(y + 1) run in one barrier interval (loop body).
 // red_1(r) needs black_0(r - 1 .. r + 1) (steps <= y - 1), black_0(r) needs
 // red_0(r - 1 .. r + 1) (phase A of this step or before), black_1(r) needs
 // red_1(r - 1 .. r + 1).  Cross-warp operands (z neighbours, lanes 31/32 of a
