@@ -18,9 +18,11 @@ working set exceeds the 126 MB L2).
 
 Metric: node-sweeps per second (GNode-sweeps/s), whole job; ms per time step
 is reported in `config`.  `roofline` is for the dominant kernel
-(k_rb_sweep_fused): algorithmic bytes per launch (56 B per node: V read +
-write, gx, gy, gz, b, 1/d, once per launch of F sweeps) / its CUDA-event
-duration inside the timed region.
+(k_rb_sweep2, the two-sweep pipeline; k_csr_sweep on CSR grids, k_rb_cluster
+on meshes small enough for one cluster): algorithmic bytes per launch (56 B
+per node: V read + write, gx, gy, gz, b, 1/d, once per launch of F sweeps) /
+its CUDA-event duration inside the timed region (event pair per time step
+around the sweep launches; graphs and PDL stay on).
 """
 from __future__ import annotations
 
