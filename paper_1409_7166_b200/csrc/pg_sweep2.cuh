@@ -251,9 +251,27 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
   // cache: measured +4 % for halving the refill code).
   // cs / vs: ring slots of constant row R and V row R + 1 (compile-time in the
   // unrolled steps: (u + 5) mod SC and (u + 6) mod SV)
+  // Per-warp copy plan (8 warps or more, no ghost-row sources): warp w < 6
+  // always issues op w, so its map, smem base / stride, row offset and policy
+  // are fixed for the launch and the per-step refill is a handful of
+  // instructions on one lane.
+  constexpr bool kPlan = Gm::NWARP >= 6;
+  const int my_op = warp;
+  const bool my_v = my_op == 5;
+  const CUtensorMap *my_map = my_op < 5 ? mC + my_op : mVin;
+  double *my_base = my_op < 5 ? cring + my_op * Gm::LAY + (my_op >= 2 ? RW : 0) : vring;
+  const int my_stride = my_v ? VST : CST;
+  const uint64_t my_pol = pol(my_op < 6 ? my_op : 0);
+  const bool my_lane = (tid & 31) == 0 && my_op < 6;
   auto refill = [&](const int y, const int cs, const int vs) {
     const int R = y + 4;
-    if ((tid & 31) == 0 && R >= r_first + SC && R <= r_last) {
+    if constexpr (kPlan && !SLAB) {
+      if (my_lane && R >= r_first + SC && R + (my_v ? 1 : 0) <= r_last) {
+        uint64_t *bar = &gbar[cs];
+        if (my_op == 0) mbar_expect_tx(bar, Gm::CBYTES + (R + 1 <= r_last ? Gm::VBYTES : 0u));
+        tma(my_base + (my_v ? vs : cs) * my_stride, my_map, bar, ps, R + (my_v ? 1 : 0), my_pol);
+      }
+    } else if ((tid & 31) == 0 && R >= r_first + SC && R <= r_last) {
       uint64_t *bar = &gbar[cs];
 #pragma unroll 1
       for (int op = warp; op < 6; op += Gm::NWARP) {
@@ -284,6 +302,7 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
   double *vout_o = vout_e + P.HP;
   double *OUT0 = q ? vout_o : vout_e, *OUT1 = q ? vout_e : vout_o;  // red's column for class 0 / 1
   const double w = P.omega;
+  const uint64_t pol_out = (P.l2keep & 32) ? pol_last : policy_evict_normal();
   double dmax = 0.0;
   bool wrote_peer = false;  // this thread stored boundary rows into a neighbour's buffer
   // only the first / last chunk of a slab writes rows for a neighbour
@@ -399,13 +418,9 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
     // row y - 4 is final: red_1 (class k) and black_1 (class k ^ 1)
     if (out && exact_lane) {
       const int64_t ro = (int64_t)(y - 4) * P.NXP;
-      if (P.l2keep & 32) {  // the next launch reads this V buffer: keep it in L2
-        stg_hint((k ? OUT1 : OUT0) + ro, Vownb1, pol_last);
-        stg_hint((k ? OUT0 : OUT1) + ro, b1, pol_last);
-      } else {
-        (k ? OUT1 : OUT0)[ro] = Vownb1;
-        (k ? OUT0 : OUT1)[ro] = b1;
-      }
+      // evict_last when the next launch should find this V buffer in L2
+      stg_hint((k ? OUT1 : OUT0) + ro, Vownb1, pol_out);
+      stg_hint((k ? OUT0 : OUT1) + ro, b1, pol_out);
       if (SLAB && send_cta) {
         const int rr = y - 4;
         const bool red_odd = (q ^ k) != 0;
