@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
   // ordered after them by the per-step proxy fence.  Only the norm and the
   // write-out are masked.  A(r_last + 1) runs without its (never issued) row
   // group and its results are discarded.
-  double aR0 = 0.0, aR1 = 0.0, aVN = 0.0, aGyN = 0.0;  // phase A results phase B needs
+  double aR0 = 0.0, aR1 = 0.0, aVN = 0.0, aGyN = 0.0, aD = 0.0;  // phase A results phase B needs
   auto phaseA = [&](auto U_, const int y) {
     constexpr int u = decltype(U_)::value % 12;
     constexpr int k = u & 1;
@@ -370,9 +370,7 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
                             vring[vY3 + mo + RW], vring[vY3 + mo - RW]);
     vring[vY + me] = r0;
     vring[vY3 + mo] = r1;
-    double dA = fabs(r1 - Vc1);
-    if (!(y >= ys + 3 && y < r_last)) dA = 0.0;  // norm over rows [ys, ye) only
-    dmax = dA > dmax ? dA : dmax;
+    aD = fabs(r1 - Vc1);  // red_1(y - 3): counted with black_1 of the same row next step
     fR0[f0] = r0;
     fR1[f0] = r1;
     fWn[f0] = Vown;
@@ -412,7 +410,10 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
                             vring[vY4 + mo - RW]);
     vring[vYm + me] = b0;
     const bool out = y >= ys + 4;  // row y - 4 owned (y - 4 < ye always)
+    // row y - 4: black_1 now, red_1 from the previous step's phase A; the
+    // norm covers the owned rows [ys, ye) only
     double dB = fabs(b1 - Vcb1);
+    dB = aD > dB ? aD : dB;
     if (!out) dB = 0.0;
     dmax = dB > dmax ? dB : dmax;
     // row y - 4 is final: red_1 (class k) and black_1 (class k ^ 1)
