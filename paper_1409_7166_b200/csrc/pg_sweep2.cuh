@@ -265,11 +265,16 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
   const bool my_lane = (tid & 31) == 0 && my_op < 6;
   auto refill = [&](const int y, const int cs, const int vs) {
     const int R = y + 4;
-    if constexpr (kPlan && !SLAB) {
+    if constexpr (kPlan) {
       if (my_lane && R >= r_first + SC && R + (my_v ? 1 : 0) <= r_last) {
         uint64_t *bar = &gbar[cs];
         if (my_op == 0) mbar_expect_tx(bar, Gm::CBYTES + (R + 1 <= r_last ? Gm::VBYTES : 0u));
-        tma(my_base + (my_v ? vs : cs) * my_stride, my_map, bar, ps, R + (my_v ? 1 : 0), my_pol);
+        int yy = R + (my_v ? 1 : 0);
+        const CUtensorMap *m = my_map;
+        if constexpr (SLAB) {
+          if (my_v) m = v_src(R + 1, yy);  // a slab's ghost rows come from the receive buffers
+        }
+        tma(my_base + (my_v ? vs : cs) * my_stride, m, bar, ps, yy, my_pol);
       }
     } else if ((tid & 31) == 0 && R >= r_first + SC && R <= r_last) {
       uint64_t *bar = &gbar[cs];
