@@ -20,7 +20,7 @@ stalls = {k.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issu
 e = {"kernel": d.get("Kernel Name", key), "workload": workload, "source": rep,
      "dram_bytes_read": rd, "dram_bytes_write": wr, "dram_bytes_per_launch": rd + wr,
      "algorithmic_bytes_per_launch": alg, "traffic_over_algorithmic": (rd + wr) / alg,
-     "duration_us_under_ncu": f("gpu__time_duration.sum") * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3,
+     "duration_us_under_ncu": f("gpu__time_duration.sum") * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3,
                                                            "second": 1e6}.get(units["gpu__time_duration.sum"], 1.0),
      "registers": f("launch__registers_per_thread"), "grid": d["launch__grid_size"], "block": d["launch__block_size"],
      "issue_active_pct": round(f("smsp__issue_active.avg.pct_of_peak_sustained_active"), 1),
