@@ -340,6 +340,7 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
   // write-out are masked.  A(r_last + 1) runs without its (never issued) row
   // group and its results are discarded.
   double aR0 = 0.0, aR1 = 0.0, aVN = 0.0, aGyN = 0.0, aD = 0.0;  // phase A results phase B needs
+  double woR = 0.0, woB = 0.0;                                    // row written out after the body
   auto phaseA = [&](auto U_, const int y) {
     constexpr int u = decltype(U_)::value % 12;
     constexpr int k = u & 1;
@@ -421,7 +422,19 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
     dB = aD > dB ? aD : dB;
     if (!out) dB = 0.0;
     dmax = dB > dmax ? dB : dmax;
-    // row y - 4 is final: red_1 (class k) and black_1 (class k ^ 1)
+    woR = Vownb1;  // row y - 4 is final: written after the body's proxy fence
+    woB = b1;
+    fB0[f0] = b0;
+    cB[f0] = cb;
+  };
+  // loop body of step y: barrier, refill, wait for row group y + 1, B(y) + A(y + 1)
+  // row y - 4 is final: red_1 (class k) and black_1 (class k ^ 1).  Issued
+  // after the body's proxy fence, so the fence does not wait for these stores.
+  auto writeout = [&](auto U_, const int y) {
+    constexpr int u = decltype(U_)::value % 12;
+    constexpr int k = u & 1;
+    const double Vownb1 = woR, b1 = woB;
+    const bool out = y >= ys + 4;
     if (out && exact_lane) {
       const int64_t ro = (int64_t)(y - 4) * P.NXP;
       // evict_last when the next launch should find this V buffer in L2
@@ -447,10 +460,7 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
         }
       }
     }
-    fB0[f0] = b0;
-    cB[f0] = cb;
   };
-  // loop body of step y: barrier, refill, wait for row group y + 1, B(y) + A(y + 1)
   auto body = [&](auto U_, const int y) {
     constexpr int u = decltype(U_)::value;
     __syncthreads();
@@ -462,6 +472,7 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
     // barrier after which TMA refills it: a proxy fence every second body
     // orders them (the fence also waits for this thread's global write-out)
     if constexpr (u % 2 == 1) fence_proxy_async();
+    writeout(U_, y);
   };
 
   // the first step's north operand: old black of row r_first in the column of
