@@ -66,6 +66,8 @@ def parse():
                     help="N > 1: weak = config rows x N (fixed work per GPU), strong = config split")
     ap.add_argument("--opt", action="append", default=[],
                     help="library option key=value (pg_set_option), e.g. fuse=2, lag=3, kernel=4")
+    ap.add_argument("--ref-seconds", type=float, default=None,
+                    help="--impl reference: oracle seconds per bench step (default: ~60 s in total)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -208,7 +210,7 @@ def run_reference(args):
     cfg = args.workload if args.workload is not None else 1
     g = make_grid(cfg)
     omega = args.omega or DEFAULT_OMEGA.get(cfg, 1.9)   # fixed sweeps: omega only sets the arithmetic
-    per_step = max(2.0, 60.0 / max(1, args.steps + args.warmup))
+    per_step = args.ref_seconds or max(2.0, 60.0 / max(1, args.steps + args.warmup))
     for _ in range(args.warmup):
         oracle_sample(cfg, g, seconds=min(per_step, 5.0), omega=omega)
     vals = []
