@@ -412,17 +412,25 @@ PG_API int pg_set_sources(pg_grid *g, int64_t n_src, const int64_t *node, const 
   g->nsrc = g->nsrc_grp = g->npts = 0;
   if (n_src == 0) return PG_OK;
   REQUIRE(node && ptr && t && i, "source arrays are NULL");
-  std::vector<int64_t> nd, pp;
+  // host inputs are read in place; device inputs are copied to the host first
+  std::vector<int64_t> nd_v, pp_v;
   int rc;
-  if ((rc = to_host(node, n_src, mem, nd)) || (rc = to_host(ptr, n_src + 1, mem, pp))) return rc;
+  if (mem == PG_MEM_DEVICE &&
+      ((rc = to_host(node, n_src, mem, nd_v)) || (rc = to_host(ptr, n_src + 1, mem, pp_v))))
+    return rc;
+  const int64_t *nd = mem == PG_MEM_DEVICE ? nd_v.data() : node;
+  const int64_t *pp = mem == PG_MEM_DEVICE ? pp_v.data() : ptr;
   REQUIRE(pp[0] == 0, "ptr[0] must be 0");
   for (int64_t k = 0; k < n_src; ++k) {
     REQUIRE(pp[k + 1] > pp[k], "every source needs at least one breakpoint");
     REQUIRE(nd[k] >= 0 && nd[k] < g->n, "source node index out of range");
   }
   const int64_t npts = pp[n_src];
-  std::vector<double> tt, ii;
-  if ((rc = to_host(t, npts, mem, tt)) || (rc = to_host(i, npts, mem, ii))) return rc;
+  std::vector<double> tt_v, ii_v;
+  if (mem == PG_MEM_DEVICE && ((rc = to_host(t, npts, mem, tt_v)) || (rc = to_host(i, npts, mem, ii_v))))
+    return rc;
+  const double *tt = mem == PG_MEM_DEVICE ? tt_v.data() : t;
+  const double *ii = mem == PG_MEM_DEVICE ? ii_v.data() : i;
   for (int64_t k = 0; k < n_src; ++k)
     for (int64_t q = pp[k] + 1; q < pp[k + 1]; ++q)
       REQUIRE(tt[q] > tt[q - 1], "PWL breakpoint times must be strictly increasing");
@@ -432,7 +440,16 @@ PG_API int pg_set_sources(pg_grid *g, int64_t n_src, const int64_t *node, const 
     CK(cudaMemcpy(iperm_h.data(), g->iperm, sizeof(int64_t) * g->n, cudaMemcpyDeviceToHost));
   }
   std::vector<int64_t> sidx((size_t)n_src);
-  for (int64_t k = 0; k < n_src; ++k) sidx[k] = storage_index(g, nd[k], &iperm_h);
+  if (g->kind == 0 && g->n < ((int64_t)1 << 31)) {
+    // 32-bit divisions (a 64-bit division per coordinate dominated this call)
+    const uint32_t per_layer = (uint32_t)g->md.NY * (uint32_t)g->md.NX, NX = (uint32_t)g->md.NX;
+    for (int64_t k = 0; k < n_src; ++k) {
+      const uint32_t v = (uint32_t)nd[k], l = v / per_layer, r = v - l * per_layer, y = r / NX, x = r - y * NX;
+      sidx[k] = mesh_index(g->md, l, y, x);
+    }
+  } else {
+    for (int64_t k = 0; k < n_src; ++k) sidx[k] = storage_index(g, nd[k], &iperm_h);
+  }
   // sources in storage order (ties: input order, so per-node sums are
   // deterministic); (key, position) pairs sort faster than an indirect stable sort
   std::vector<int64_t> order((size_t)n_src);
