@@ -453,7 +453,23 @@ PG_API int pg_set_sources(pg_grid *g, int64_t n_src, const int64_t *node, const 
   // sources in storage order (ties: input order, so per-node sums are
   // deterministic); (key, position) pairs sort faster than an indirect stable sort
   std::vector<int64_t> order((size_t)n_src);
-  {
+  if (g->kind == 0 && std::is_sorted(nd, nd + n_src)) {
+    // sources in natural node order (the common case): inside each row the
+    // storage order is the even columns, then the odd ones -- a stable
+    // two-way partition per row, no comparison sort
+    int64_t a = 0;
+    while (a < n_src) {
+      const int64_t row = nd[a] / g->md.NX;
+      int64_t b = a;
+      while (b < n_src && nd[b] / g->md.NX == row) ++b;
+      int64_t o = a;
+      for (int64_t k = a; k < b; ++k)
+        if (((nd[k] % g->md.NX) & 1) == 0) order[o++] = k;
+      for (int64_t k = a; k < b; ++k)
+        if (((nd[k] % g->md.NX) & 1) == 1) order[o++] = k;
+      a = b;
+    }
+  } else {
     std::vector<std::pair<int64_t, int64_t>> kp((size_t)n_src);
     for (int64_t k = 0; k < n_src; ++k) kp[k] = {sidx[k], k};
     if (!std::is_sorted(kp.begin(), kp.end())) std::sort(kp.begin(), kp.end());
