@@ -82,7 +82,7 @@ void free_grid(pg_grid *g) {
   void *ptrs[] = {g->gx, g->gy, g->gz, g->lz, g->gze, g->iz, g->rowptr, g->col, g->val, g->perm,
                   g->iperm, g->V[0], g->V[1], g->x0, g->cap, g->invd, g->b, g->pad_idx,
                   g->pad_grp, g->pad_g, g->pad_l, g->pad_ge, g->pad_i, g->src_idx, g->src_grp,
-                  g->src_ptr, g->pwl_t, g->pwl_i, g->ctl, g->dev_sweeps};
+                  g->src_ptr, g->pwl_t, g->pwl_i, g->ctl, g->dev_sweeps, g->user_buf};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t e : g->tev) cudaEventDestroy(e);
@@ -504,9 +504,9 @@ PG_API int pg_set_sources(pg_grid *g, int64_t n_src, const int64_t *node, const 
 PG_API int pg_set_voltages(pg_grid *g, const double *v, int mem) {
   REQUIRE(g != nullptr && v != nullptr, "grid/v is NULL");
   REQUIRE(mem == PG_MEM_HOST || mem == PG_MEM_DEVICE, "bad mem");
-  double *tmp = nullptr;
   int rc;
-  if ((rc = dalloc(&tmp, g->n))) return rc;
+  if (!g->user_buf && (rc = dalloc(&g->user_buf, g->n))) return rc;
+  double *tmp = g->user_buf;
   cudaError_t e = cudaMemcpyAsync(tmp, v, sizeof(double) * g->n,
                                   mem == PG_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
                                   g->stream);
@@ -516,7 +516,6 @@ PG_API int pg_set_voltages(pg_grid *g, const double *v, int mem) {
   if (e == cudaSuccess && g->iz) e = cudaMemsetAsync(g->iz, 0, sizeof(double) * g->np, g->stream);
   if (e == cudaSuccess && g->pad_i) e = cudaMemsetAsync(g->pad_i, 0, sizeof(double) * g->npad, g->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
-  cudaFree(tmp);
   if (e != cudaSuccess) return cuda_fail(e, "pg_set_voltages");
   return PG_OK;
 }
@@ -529,13 +528,14 @@ PG_API int pg_get_voltages(pg_grid *g, double *v, int mem) {
     CK(cudaStreamSynchronize(g->stream));
     return PG_OK;
   }
-  double *tmp = nullptr;
+  // staged through a per-grid buffer kept until pg_destroy: no cudaMalloc /
+  // cudaFree (a device-wide synchronisation) per read-back
   int rc;
-  if ((rc = dalloc(&tmp, g->n))) return rc;
+  if (!g->user_buf && (rc = dalloc(&g->user_buf, g->n))) return rc;
+  double *tmp = g->user_buf;
   cudaError_t e = launch_gather_user(g, tmp);
   if (e == cudaSuccess) e = cudaMemcpyAsync(v, tmp, sizeof(double) * g->n, cudaMemcpyDeviceToHost, g->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
-  cudaFree(tmp);
   if (e != cudaSuccess) return cuda_fail(e, "pg_get_voltages");
   return PG_OK;
 }

@@ -13,7 +13,7 @@ g = gridgen.config_grid(cfg)
 pin = {k: torch.from_numpy(np.ascontiguousarray(getattr(g, k))).pin_memory().numpy() for k in ("gx", "gy", "gz", "cap")}
 out = torch.empty(g.n, dtype=torch.float64).pin_memory().numpy()
 s = g.sources
-for rep in range(3):
+for rep in range(int(sys.argv[3]) if len(sys.argv) > 3 else 3):
     torch.cuda.synchronize(); t0 = time.perf_counter()
     H = P.Grid.mesh(g.layers, g.ny, g.nx, pin["gx"], pin["gy"], pin["gz"], pin["cap"], g.pad_node, g.pad_g, g.vdd,
                     None, None)
