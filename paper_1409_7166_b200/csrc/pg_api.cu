@@ -5,8 +5,10 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <numeric>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "pg_internal.h"
@@ -44,11 +46,107 @@ using namespace pgb;
 
 namespace {
 
+// Device memory of the grids comes from a library-owned stream-ordered pool
+// per device (release threshold 8 GiB), so creating and destroying grids, the
+// per-call scratch of pg_transient and pg_set_sources do not map and unmap
+// device memory each time (cudaMalloc / cudaFree of large buffers took up to
+// ~200 ms now and then inside the end-to-end call).  Blocks are handed out
+// after the pool's stream reached the allocation and returned after a device
+// synchronisation, so they are usable from any stream like cudaMalloc memory.
+// DevCtl stays plain cudaMalloc memory: it is exported over CUDA IPC.
+struct DevPool {
+  bool init = false;
+  cudaMemPool_t pool = nullptr;
+  cudaStream_t s = nullptr;
+};
+std::mutex g_pool_mu;
+DevPool g_pools[64];
+std::unordered_map<void *, int> g_pool_ptrs;  // pool block -> device
+
+DevPool *pool_of(int dev) {
+  if (dev < 0 || dev >= 64) return nullptr;
+  DevPool &d = g_pools[dev];
+  if (!d.init) {
+    d.init = true;
+    cudaMemPoolProps pr = {};
+    pr.allocType = cudaMemAllocationTypePinned;
+    pr.handleTypes = cudaMemHandleTypeNone;
+    pr.location.type = cudaMemLocationTypeDevice;
+    pr.location.id = dev;
+    uint64_t thr = 8ull << 30;
+    if (cudaMemPoolCreate(&d.pool, &pr) != cudaSuccess ||
+        cudaMemPoolSetAttribute(d.pool, cudaMemPoolAttrReleaseThreshold, &thr) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&d.s, cudaStreamNonBlocking) != cudaSuccess) {
+      cudaGetLastError();
+      d.pool = nullptr;
+    }
+  }
+  return d.pool ? &d : nullptr;
+}
+
+void dfree(void *p) {
+  if (!p) return;
+  int dev = -1;
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    auto it = g_pool_ptrs.find(p);
+    if (it != g_pool_ptrs.end()) {
+      dev = it->second;
+      g_pool_ptrs.erase(it);
+    }
+  }
+  if (dev < 0) {
+    cudaFree(p);
+    return;
+  }
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cur != dev) cudaSetDevice(dev);
+  cudaDeviceSynchronize();  // the block may still be in use on any stream (cudaFree semantics)
+  DevPool *d;
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    d = pool_of(dev);
+  }
+  if (d) cudaFreeAsync(p, d->s);
+  if (cur != dev) cudaSetDevice(cur);
+}
+
 template <class T>
-int dalloc(T **p, int64_t count) {
+int dalloc(T **p, int64_t count, bool plain = false) {
   *p = nullptr;
   if (count <= 0) return PG_OK;
-  cudaError_t e = cudaMalloc((void **)p, sizeof(T) * (size_t)count);
+  const size_t bytes = sizeof(T) * (size_t)count;
+  cudaError_t e = cudaErrorMemoryAllocation;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  DevPool *d = nullptr;
+  if (!plain) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    d = pool_of(dev);
+  }
+  if (d) {
+    // sizes rounded to 256 B so that every block keeps cudaMalloc's alignment
+    // (TMA tensor maps and vector loads rely on it); checked below
+    e = cudaMallocFromPoolAsync((void **)p, (bytes + 255) & ~(size_t)255, d->pool, d->s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(d->s);
+    if (e == cudaSuccess && ((uintptr_t)*p & 255)) {
+      cudaFreeAsync(*p, d->s);
+      cudaStreamSynchronize(d->s);
+      *p = nullptr;
+      d = nullptr;
+    } else if (e == cudaSuccess) {
+      std::lock_guard<std::mutex> lk(g_pool_mu);
+      g_pool_ptrs[(void *)*p] = dev;
+    } else {
+      cudaGetLastError();
+      *p = nullptr;
+      d = nullptr;  // pool exhausted or unusable: plain cudaMalloc
+    }
+  }
+  if (!d) {
+    e = cudaMalloc((void **)p, bytes);
+  }
   if (e != cudaSuccess) {
     *p = nullptr;
     set_error(std::string("cudaMalloc of ") + std::to_string(sizeof(T) * (size_t)count) +
@@ -82,9 +180,9 @@ void free_grid(pg_grid *g) {
   void *ptrs[] = {g->gx, g->gy, g->gz, g->lz, g->gze, g->iz, g->rowptr, g->col, g->val, g->perm,
                   g->iperm, g->V[0], g->V[1], g->x0, g->cap, g->invd, g->b, g->pad_idx,
                   g->pad_grp, g->pad_g, g->pad_l, g->pad_ge, g->pad_i, g->src_idx, g->src_grp,
-                  g->src_ptr, g->pwl_t, g->pwl_i, g->ctl, g->dev_sweeps, g->user_buf};
+                  g->src_ptr, g->pwl_t, g->pwl_i, g->ctl, g->dev_sweeps, g->user_buf};  // ctl: plain (dfree -> cudaFree)
   for (void *p : ptrs)
-    if (p) cudaFree(p);
+    if (p) dfree(p);
   for (cudaEvent_t e : g->tev) cudaEventDestroy(e);
   if (g->batch_exec) cudaGraphExecDestroy(g->batch_exec);
   if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
@@ -122,7 +220,7 @@ int common_init(pg_grid *g) {
   CK(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, g->dev));
   int rc;
   if ((rc = dalloc(&g->V[0], g->np)) || (rc = dalloc(&g->V[1], g->np)) || (rc = dalloc(&g->x0, g->np)) ||
-      (rc = dalloc(&g->invd, g->np)) || (rc = dalloc(&g->b, g->np)) || (rc = dalloc(&g->ctl, 1)))
+      (rc = dalloc(&g->invd, g->np)) || (rc = dalloc(&g->b, g->np)) || (rc = dalloc(&g->ctl, 1, true)))
     return rc;
   CK(cudaMemset(g->V[0], 0, sizeof(double) * g->np));
   CK(cudaMemset(g->V[1], 0, sizeof(double) * g->np));
@@ -240,7 +338,7 @@ PG_API int pg_create_mesh(int32_t layers, int32_t ny, int32_t nx, const double *
   if ((rc = dalloc(&stage, n))) return rc;
   struct StageGuard {
     double *p;
-    ~StageGuard() { cudaFree(p); }
+    ~StageGuard() { dfree(p); }
   } stage_guard{stage};
   auto put = [&](double **dst, const double *src) -> int {
     int r = dalloc(dst, g->np);
@@ -404,9 +502,9 @@ PG_API int pg_set_sources(pg_grid *g, int64_t n_src, const int64_t *node, const 
   REQUIRE(n_src >= 0, "n_src must be >= 0");
   REQUIRE(mem == PG_MEM_HOST || mem == PG_MEM_DEVICE, "bad mem");
   for (int64_t *p : {g->src_idx, g->src_grp, g->src_ptr})
-    if (p) cudaFree(p);
+    if (p) dfree(p);
   for (double *p : {g->pwl_t, g->pwl_i})
-    if (p) cudaFree(p);
+    if (p) dfree(p);
   g->src_idx = g->src_grp = g->src_ptr = nullptr;
   g->pwl_t = g->pwl_i = nullptr;
   g->nsrc = g->nsrc_grp = g->npts = 0;
@@ -570,7 +668,7 @@ PG_API int pg_estimate_omega(pg_grid *g, double h, int64_t sweeps, double *rho, 
   if ((rc = dalloc(&hist, sweeps))) return rc;
   struct Free {
     void *p;
-    ~Free() { cudaFree(p); }
+    ~Free() { dfree(p); }
   } fr{hist};
   // Jacobi (omega = 1) on the homogeneous system M e = 0 from the start vector
   // x(0): the differences V^(k) - V^(k-1) obey the same iteration, so the
@@ -690,8 +788,8 @@ int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, d
     double **b;
     bool own_b;
     ~Tmp() {
-      if (*a) cudaFree(*a);
-      if (own_b && *b) cudaFree(*b);
+      if (*a) dfree(*a);
+      if (own_b && *b) dfree(*b);
     }
   } tmp{&d_pidx, &d_pout, mem == PG_MEM_HOST};
   if (n_probe > 0) {
@@ -706,7 +804,7 @@ int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, d
   for (int k = 0; k < ng; ++k) {
     pg_grid *q = gs[k];
     if (q->dev_sweeps_cap < steps + 1) {
-      if (q->dev_sweeps) cudaFree(q->dev_sweeps);
+      if (q->dev_sweeps) dfree(q->dev_sweeps);
       q->dev_sweeps = nullptr;
       q->dev_sweeps_cap = 0;
       if ((rc = dalloc(&q->dev_sweeps, steps + 1))) return rc;
