@@ -1,28 +1,34 @@
 """Benchmark: topology-based power-grid transient (arxiv 1409.7166) on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                    [--workload K] [--tsteps T] [--omega w] [--method rbsor|jacobi]
-                    [--scaling weak|strong] [--opt key=value ...]
+                    [--workload C] [--tsteps T] [--omega w] [--method rbsor|jacobi]
+                    [--scaling strong|weak] [--transport nccl|p2p] [--opt key=value ...]
 
-One bench "step" = one full pass of the hot path over the workload: a
-pg_transient call (Algorithm 1: per backward-Euler time step the fused RHS
-kernels, red-black SOR sweeps (F = 2 per launch) to tol = 1e-10 V, inductor
-update) over T time steps of the BASELINE.json configuration (N = 1: config 1,
-4 x 1024 x 1024 RC mesh, h = 5 ps, 500 steps).  N > 1 (torchrun, one rank per
-GPU): the mesh is split into row slabs, one per GPU, advanced by
-pg_group_transient with an NCCL ghost-row exchange and norm allreduce after
-every sweep launch; weak scaling stacks N copies of the config's rows.
+Workload: BASELINE.json config C (default 4: the 8 x 4096 x 4096 RC mesh,
+134M nodes, h = 5 ps, 200 steps -- the largest single-GPU configuration,
+DESIGN.md §11).  One bench "step" = one window of T consecutive
+backward-Euler time steps of that transient (default T = 8 for config 4, the
+whole transient for the smaller configs): per time step the fused RHS
+kernel, red-black SOR sweeps (F = 2 per launch) to tol = 1e-10 V, and (RLC)
+the inductor update, through pg_transient / pg_transient_continue.  Windows
+continue the transient (pg_transient_continue) and restart it from x(0) when
+it is complete, so W + K windows of T = 8 cover the 200 steps of config 4
+exactly once for the driver's --warmup 5 --steps 20.  N > 1 (torchrun, one
+rank per GPU): the mesh is split into row slabs, one per GPU, advanced by
+pg_group_transient with an exchange after every sweep launch (NCCL halo
+send/recv + norm allreduce, or the peer-memory exchange fused into the
+sweep); strong scaling by default (the config split), weak stacks N copies.
 Inputs are seeded synthetic grids with the BASELINE.json distributions
-(DESIGN.md §6), resident in HBM before the timed region (the ~235 MB per-pass
-working set exceeds the 126 MB L2).
+(DESIGN.md §6), resident in HBM before the timed region (the per-pass working
+set, 56 B per node, exceeds the 126 MB L2 on configs 1-4: no flush needed).
 
 Metric: node-sweeps per second (GNode-sweeps/s), whole job; ms per time step
-is reported in `config`.  `roofline` is for the dominant kernel
-(k_rb_sweep2, the two-sweep pipeline; k_csr_sweep on CSR grids, k_rb_cluster
-on meshes small enough for one cluster): algorithmic bytes per launch (56 B
-per node: V read + write, gx, gy, gz, b, 1/d, once per launch of F sweeps) /
-its CUDA-event duration inside the timed region (event pair per time step
-around the sweep launches; graphs and PDL stay on).
+in `detail`.  `roofline` is for the dominant kernel (k_rb_sweep2, the
+two-sweep pipeline; k_csr_sweep on CSR grids; k_rb_cluster on meshes small
+enough for one cluster): algorithmic bytes per launch (56 B per node: V read +
+write, gx, gy, gz, b, 1/d, once per launch of F sweeps) / its CUDA-event
+duration inside the timed region (an event pair per time step around the
+sweep launches on the grid's stream; graphs and PDL stay on).
 """
 from __future__ import annotations
 
@@ -41,7 +47,19 @@ sys.path.insert(0, ROOT)
 METRIC = "node-updates/sec (GNode-sweeps/s) and ms per time step; fraction of HBM roofline"
 UNIT = "GNode-sweeps/s"
 BYTES_PER_NODE_PASS = 56  # V r/w 16 + gx, gy, gz 24 + b 8 + invd 8 (one streaming pass, F sweeps)
-DEFAULT_OMEGA = {0: 1.9, 1: 1.98, 2: 1.98, 3: 1.99, 4: 1.99}
+DEFAULT_WORKLOAD = 4
+# Young's optimum omega of each config: pg_estimate_omega (8000 Jacobi sweeps of
+# the homogeneous system, R15) on the config's grid, recorded from
+# profiles/r2_probe_omega.log; the same literals parametrise the full-size
+# parity goldens (tools/make_golden_fullsize.py, tests/golden/fullsize_*.npz)
+YOUNG_OMEGA = {
+    1: 1.9639132252348532,
+    2: 1.9603462069765296,
+    3: 1.9511469274691926,
+    4: 1.9724621984718245,
+}
+FALLBACK_OMEGA = 1.9
+DEFAULT_WINDOW = {4: 8}   # time steps per bench step (others: the whole transient)
 
 
 def parse():
@@ -50,9 +68,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", type=int, default=None, help="BASELINE.json config index")
-    ap.add_argument("--tsteps", type=int, default=None, help="time steps per bench step")
+    ap.add_argument("--workload", type=int, default=DEFAULT_WORKLOAD, help="BASELINE.json config index")
+    ap.add_argument("--tsteps", type=int, default=None, help="time steps per bench step (window)")
     ap.add_argument("--omega", type=float, default=None)
+    ap.add_argument("--estimate-omega", action="store_true",
+                    help="estimate Young's omega on the grid at run time instead of the recorded value")
     ap.add_argument("--tol", type=float, default=1e-10)
     ap.add_argument("--method", default="rbsor", choices=["rbsor", "jacobi"])
     ap.add_argument("--slabs", type=int, default=1,
@@ -62,12 +82,12 @@ def parse():
     ap.add_argument("--transport", default=None, choices=["nccl", "copy", "p2p"],
                     help="slab exchange: nccl (N > 1 default), copy (--slabs default), or p2p: "
                          "fused into the sweep kernel over peer memory (CUDA IPC for N > 1)")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="N > 1: weak = config rows x N (fixed work per GPU), strong = config split")
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="N > 1: strong = the config split over the GPUs (default), weak = config rows x N")
     ap.add_argument("--opt", action="append", default=[],
-                    help="library option key=value (pg_set_option), e.g. fuse=2, lag=3, kernel=4")
+                    help="library option key=value (pg_set_option), e.g. fuse=2, lag=3")
     ap.add_argument("--ref-seconds", type=float, default=None,
-                    help="--impl reference: oracle seconds per bench step (default: ~60 s in total)")
+                    help="--impl reference: oracle seconds per bench step (default: ~90 s in total)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -114,7 +134,7 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
-        sm, smax, reasons = [], None, set()
+        sm, smax, reasons, power = [], None, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
@@ -122,6 +142,7 @@ class ClockSampler:
                 continue
             try:
                 s, m = float(parts[0]), float(parts[1])
+                power.append(float(parts[2]))
             except ValueError:
                 continue
             smax = m
@@ -131,11 +152,12 @@ class ClockSampler:
                     reasons.add(nm)
         load = [s for s in sm if smax and s > 0.5 * smax] or sm
         return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_median": statistics.median(power) if power else None}
 
 
 # ------------------------------------------------------------ workloads
-def make_grid(cfg: int, world: int = 1, scaling: str = "weak"):
+def make_grid(cfg: int, world: int = 1, scaling: str = "strong"):
     """BASELINE config `cfg`; for N > 1 ranks under weak scaling the mesh is N
     copies of the config's row count stacked (same per-GPU work), under strong
     scaling the config itself is split."""
@@ -146,89 +168,150 @@ def make_grid(cfg: int, world: int = 1, scaling: str = "weak"):
     return gridgen.config_grid(cfg)
 
 
+def window_of(cfg: int, g, tsteps):
+    return int(tsteps or DEFAULT_WINDOW.get(cfg, g.steps))
+
+
+def omega_of(args, cfg):
+    if args.omega:
+        return args.omega, "--omega"
+    if args.method == "jacobi":
+        return FALLBACK_OMEGA, "fixed (Jacobi weight)"
+    if cfg in YOUNG_OMEGA and not args.estimate_omega:
+        return YOUNG_OMEGA[cfg], ("Young's optimum 2/(1+sqrt(1-rho_J^2)), rho_J from pg_estimate_omega "
+                                  "(8000 Jacobi sweeps) on this grid, recorded (DESIGN.md R15)")
+    return None, "Young (pg_estimate_omega, 8000 Jacobi sweeps, at run time)"
+
+
+def config_dict(cfg, g, T, tol, omega, omega_src, method, opts, world, scaling, transport, slabs):
+    """The workload description both arms print (identical for the same args)."""
+    if world > 1:
+        par = (f"slab{world}: rows split over {world} GPUs ({scaling} scaling), "
+               + ("ghost rows and norm exchanged by the sweep kernel over peer memory (CUDA IPC)"
+                  if transport == "p2p" else "NCCL ghost-row exchange + norm allreduce per sweep launch"))
+    elif slabs > 1:
+        par = (f"1 GPU, {slabs} row slabs exchanged in one process ("
+               + ("pg_group_local_p2p: peer-memory exchange in the sweep kernel" if transport == "p2p"
+                  else "pg_group_local: copies") + ")")
+    else:
+        par = "1 GPU"
+    return {"workload": f"config{cfg}" + (f" x{world} rows (weak scaling)" if world > 1 and scaling == "weak"
+                                          else ""),
+            "nodes": g.n, "mesh": [g.layers, g.ny, g.nx] if hasattr(g, "gx") else None,
+            "grid": "CSR (irregular)" if not hasattr(g, "gx") else ("RLC mesh" if g.is_rlc else "RC mesh"),
+            "h_s": g.h, "time_steps_total": g.steps, "time_steps_per_bench_step": T,
+            "bench_step": ("window of T consecutive time steps continuing the transient "
+                           "(pg_transient_continue), restarted from x(0) after its last step"),
+            "tol_V": tol, "omega": omega, "omega_source": omega_src, "method": method, "options": opts,
+            "l2": "per-sweep working set ~56 B/node x n > 126 MB L2 (no flush needed)",
+            "parallelism": par}
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(kernel: str):
-    """dram bytes per launch of the sweep kernel from the committed ncu
-    capture of the same configuration (profiles/rb_sweep_traffic.json), if any."""
+def ncu_traffic(kernel: str, cfg: int):
+    """DRAM bytes per launch of the sweep kernel from the committed `ncu --set
+    full` capture of the same configuration (profiles/rb_sweep_traffic.json)."""
     p = os.path.join(ROOT, "profiles", "rb_sweep_traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        e = d.get(kernel) if isinstance(d.get(kernel), dict) else None
-        return None if e is None else e.get("dram_bytes_per_launch")
+        e = d.get(f"{kernel}@config{cfg}")
+        return None if not isinstance(e, dict) else e.get("dram_bytes_per_launch")
     except Exception:
         return None
 
 
 # ------------------------------------------------------------- oracle arm
+class OracleSampler:
+    """The oracle (as it stands, plain C, one thread) on the full grid of the
+    workload: time step 1 from x(0), a fixed number of natural-order SOR sweeps."""
+
+    def __init__(self, cfg, g, omega):
+        from oracle import netlist, nodal, pwl
+        self.cfg, self.n = cfg, g.n
+        self.h, self.omega = g.h, omega
+        nl = netlist.from_grid(g)
+        self.o = nodal.NodalOracle(nl)
+        nl.ra = nl.rb = nl.rg = None     # the branch list is not needed any more (memory)
+        self.It = pwl.node_currents_table(nl, g.h, 1)
+        self.t_one = self._time(1)              # call overhead + 1 sweep
+
+    def _time(self, k):
+        t0 = time.perf_counter()
+        self.o.transient(self.h, 1, tol=0.0, omega=self.omega, Itab=self.It, max_sweeps=k)
+        return time.perf_counter() - t0
+
+    def per_sweep(self):
+        """Seconds per sweep: grow the sweep count until a call takes >= 0.3 s
+        (small grids), the difference to the 1-sweep call removes the overhead."""
+        k = 3
+        while True:
+            t = self._time(k)
+            if t >= 0.3 or k >= 1 << 22:
+                return max((t - self.t_one) / (k - 1), 1e-9)
+            k *= 4
+
+    def run(self, k):
+        t0 = time.perf_counter()
+        self.o.transient(self.h, 1, tol=0.0, omega=self.omega, Itab=self.It, max_sweeps=k)
+        dt = time.perf_counter() - t0
+        return {"value": self.n * k / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
+                "sample": f"config{self.cfg} full grid ({self.n} nodes), time step 1 from x(0), {k} fixed "
+                          f"natural-order SOR sweeps (omega={self.omega}) in the plain-C oracle "
+                          f"(oracle/nodal.c), single thread, {dt:.1f} s"}, dt
+
+
 def oracle_sample(cfg: int, g=None, seconds: float = 12.0, omega: float = 1.98):
-    """Time the oracle (as it stands) on a bounded sample of the workload:
-    the full grid, time step 1, fixed natural-order SOR sweeps (single thread)."""
-    import numpy as np
-    from oracle import netlist, nodal, pwl
     if g is None:
         g = make_grid(cfg)
-    nl = netlist.from_grid(g)
-    o = nodal.NodalOracle(nl)
-    It = pwl.node_currents_table(nl, g.h, 1)
-    # calibrate sweeps to ~seconds of work: grow the sweep count until a run
-    # takes >= 0.3 s (small grids), the difference to a 1-sweep run removes setup
-    t0 = time.perf_counter()
-    o.transient(g.h, 1, tol=0.0, omega=omega, Itab=It, max_sweeps=1)
-    t_one = time.perf_counter() - t0
-    kt = 4
-    while True:
-        t0 = time.perf_counter()
-        o.transient(g.h, 1, tol=0.0, omega=omega, Itab=It, max_sweeps=kt)
-        t_k = time.perf_counter() - t0
-        if t_k >= 0.3 or kt >= 1 << 20:
-            break
-        kt *= 4
-    per = max(t_k - t_one, 1e-9) / (kt - 1)
+    s = OracleSampler(cfg, g, omega)
+    per = s.per_sweep()
     k = max(2, int(seconds / per))
-    t0 = time.perf_counter()
-    o.transient(g.h, 1, tol=0.0, omega=omega, Itab=It, max_sweeps=k)
-    dt = time.perf_counter() - t0
-    return {"value": g.n * k / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"config{cfg} full grid ({g.n} nodes), time step 1, {k} fixed natural-order "
-                      f"SOR sweeps (omega={omega}) in the plain-C oracle, single thread, {dt:.1f} s"}
+    return s.run(k)[0]
 
 
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    cfg = args.workload if args.workload is not None else 1
+    cfg = args.workload
     g = make_grid(cfg)
-    omega = args.omega or DEFAULT_OMEGA.get(cfg, 1.9)   # fixed sweeps: omega only sets the arithmetic
-    per_step = args.ref_seconds or max(2.0, 60.0 / max(1, args.steps + args.warmup))
+    T = window_of(cfg, g, args.tsteps)
+    omega, omega_src = omega_of(args, cfg)
+    if omega is None:
+        omega, omega_src = FALLBACK_OMEGA, "fixed (reference arm: no GPU to estimate it)"
+    transport = args.transport or ("nccl" if world > 1 else "copy")
+    conf = config_dict(cfg, g, T, args.tol, omega, omega_src, args.method, dict(kv.split("=", 1) for kv in args.opt),
+                       world, args.scaling, transport, args.slabs)
+    s = OracleSampler(cfg, g, omega)
+    per = s.per_sweep()
+    budget = args.ref_seconds or max(2.0, 90.0 / max(1, args.steps + args.warmup))
+    k = max(1, int(budget / per))
     for _ in range(args.warmup):
-        oracle_sample(cfg, g, seconds=min(per_step, 5.0), omega=omega)
-    vals = []
-    t_all = 0.0
+        s.run(max(1, min(k, int(5.0 / per))))
+    vals, t_all = [], 0.0
     for _ in range(args.steps):
-        t0 = time.perf_counter()
-        r = oracle_sample(cfg, g, seconds=per_step, omega=omega)
-        t_all += time.perf_counter() - t0
+        r, dt = s.run(k)
+        t_all += dt
         vals.append(r["value"])
-    v = statistics.mean(vals)
+    v = float(args.steps) * g.n * k / t_all / 1e9 if t_all > 0 else 0.0
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * t_all / max(args.steps, 1), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic (seeded BASELINE.json recipe)",
-            "config": {"workload": f"config{cfg}", "nodes": g.n},
+            "ms_per_step": 1e3 * t_all / max(args.steps, 1), "higher_is_better": True,
+            "scaling": args.scaling if world > 1 else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded BASELINE.json recipe, gridgen)",
+            "config": conf,
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": r["sample"]},
+                             "sample": f"each bench step: {r['sample']}"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -244,14 +327,16 @@ def run_b200(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg = args.workload if args.workload is not None else 1
+    cfg = args.workload
     g = make_grid(cfg, world, args.scaling)
-    T = args.tsteps or g.steps
+    T = window_of(cfg, g, args.tsteps)
+    TOT = g.steps
     tol = args.tol
     stream = torch.cuda.current_stream()
     opts = dict(kv.split("=", 1) for kv in args.opt)
     fuse = int(opts.get("fuse", 2))
-    p2p = args.transport == "p2p"
+    transport = args.transport or ("nccl" if world > 1 else "copy")
+    p2p = transport == "p2p"
     iopts = {k: int(v) for k, v in opts.items()}
 
     def make_group(device=True):
@@ -281,26 +366,31 @@ def run_b200(args):
     for k, v in opts.items():
         for q in (grp.grids if grp is not None else [G]):
             q.set_option(k, int(v))
-    # relaxation factor: Young's optimum from the library's Jacobi power
-    # iteration (§IV-D refers to Young), unless given; not timed
     t_om = time.perf_counter()
-    if args.omega:
-        omega, omega_src = args.omega, "--omega"
-    elif args.method == "jacobi":
-        omega, omega_src = DEFAULT_OMEGA.get(cfg, 1.9), "DEFAULT_OMEGA"
-    else:
+    omega, omega_src = omega_of(args, cfg)
+    if omega is None:
         _, omega = G.estimate_omega(g.h, 8000)
         if world > 1:
             t = torch.tensor([omega], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             omega = float(t.item())
-        omega_src = "Young (pg_estimate_omega, 8000 Jacobi sweeps)"
     t_om = time.perf_counter() - t_om
 
-    def solve():
+    state = {"done": 0}
+
+    def window():
+        """The next window of T time steps (continuing the transient, or
+        restarting it from x(0) when the remaining steps do not fill a window)."""
+        cont = 0 < state["done"] and state["done"] + T <= TOT
+        if not cont:
+            state["done"] = 0
+        s0 = state["done"]
         if grp is not None:
-            return grp.transient(g.h, T, tol=tol, omega=omega, max_sweeps=200000)
-        return G.transient(g.h, T, tol=tol, omega=omega, method=args.method, max_sweeps=200000)
+            r = grp.transient(g.h, T, tol=tol, omega=omega, max_sweeps=200000, cont=cont)
+        else:
+            r = G.transient(g.h, T, tol=tol, omega=omega, method=args.method, max_sweeps=200000, cont=cont)
+        state["done"] = s0 + T
+        return r, s0
 
     def barrier():
         torch.cuda.synchronize()
@@ -316,8 +406,20 @@ def run_b200(args):
     # `stream` around every time step's sweep launches (read after the run, no
     # extra synchronisation) gives the sweep kernel's time inside the timed region
     set_timing(True)
+    win_ms = {}          # first time step of the window -> device ms (first pass over the transient)
+
+    def timed_window():
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        r, s0 = window()
+        e1.record(stream)
+        e1.synchronize()
+        win_ms.setdefault(s0, e0.elapsed_time(e1))
+        return r
+
     for _ in range(args.warmup):
-        solve()
+        timed_window()
     clocks = ClockSampler(local)
     barrier()
     clocks.start()
@@ -329,7 +431,7 @@ def run_b200(args):
     sweep_launches = 0
     sweeps_per_tstep = []
     for _ in range(args.steps):
-        r = solve()
+        r = timed_window()
         sweeps += int(r.stats.sweeps_total)
         launches += int(r.stats.kernel_launches)
         sweep_ms += float(r.stats.sweep_ms)
@@ -365,22 +467,28 @@ def run_b200(args):
             # time step with V and the constants in shared memory, HBM once per step
             kname = "k_rb_cluster"
             F = sweeps / max(sweep_launches, 1)
+        bpn = f"{BYTES_PER_NODE_PASS} B per node per launch of {F} sweeps"
     else:
-        # CSR sweep (one launch per colour per sweep): rowptr 8 + b 8 + 1/d 8 +
+        # CSR sweep (one launch per colour per sweep): rowptr 4 + b 8 + 1/d 8 +
         # V read + write 16 per row, column index 4 + value 8 per entry
         # (gathered neighbour values counted as cache hits)
         launch_nodes = g.n
         nnz = 2 * int(np.count_nonzero(np.asarray(g.eu) != np.asarray(g.ev)))
-        bytes_per_launch = 40 * g.n + 12 * nnz
+        bytes_per_launch = 36 * g.n + 12 * nnz
         kname = "k_csr_sweep"
+        bpn = "36 B per row + 12 B per off-diagonal entry per sweep"
     achieved = bytes_per_launch / (avg_launch_ms * 1e-3) / 1e9
+    traffic = ncu_traffic(kname, cfg) if grp is None else None
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": ncu_traffic(kname) if hasattr(g, "gx") and cfg == 1 else None,
-            "kernel": kname, "bytes_per_launch": bytes_per_launch,
+            "frac": achieved / peak, "traffic": traffic,
+            "kernel": kname, "bytes_per_launch": bytes_per_launch, "algorithmic_bytes": bpn,
             "bytes_per_node_per_launch": bytes_per_launch / launch_nodes, "sweeps_per_launch": F,
             "bytes_per_node_sweep": bytes_per_launch / launch_nodes / F, "avg_launch_us": avg_launch_ms * 1e3,
             "kernel_node_sweeps_per_s": launch_nodes * F / (avg_launch_ms * 1e-3) / 1e9,
             "sweep_share_of_step": sweep_ms / t1 if t1 > 0 else None, "peak_source": peak_src,
+            "traffic_source": ("ncu --set full of this kernel on this config, dram__bytes_read.sum + "
+                               "dram__bytes_write.sum per launch (profiles/rb_sweep_traffic.json)")
+            if traffic else None,
             "timing": "avg_launch_us = sum over time steps of the CUDA-event time around the step's "
                       "sweep launches (graph batches, programmatic dependent launch; includes the batch "
                       "bookkeeping kernel and queued launches that exit after convergence) / launches "
@@ -390,17 +498,17 @@ def run_b200(args):
                         "node constants in distributed shared memory; HBM is read once per time step, the "
                         "sweep rate is bound by cluster-barrier latency, not by HBM (DESIGN.md section 7)")
 
-    # e2e: public C-ABI call with host buffers (pinned), copies inside the timed region
+    # e2e: the public C-ABI calls a user makes, with HOST buffers (pinned): the
+    # grid built from host arrays (H2D inside pg_create_*), the loads set, one
+    # window of T steps from x(0), the voltages read back (D2H) -- every rep
     e2e = None
-    if not args.no_e2e and grp is not None:
-        # public API with host buffers: this rank's slab built from host arrays,
-        # NCCL group set up, transient, owned voltages read back
+    nrep = max(1, min(args.steps, 2))
+    if not args.no_e2e and grp is not None and world > 1:
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         barrier()
         e0.record(stream)
         e_sweeps = 0
-        nrep = max(1, min(args.steps, 2))
         h2d = d2h = 0
         for _ in range(nrep):
             H = make_group(device=False)
@@ -408,7 +516,7 @@ def run_b200(args):
                 for k, v in opts.items():
                     H.grids[0].set_option(k, int(v))
             rr = H.transient(g.h, T, tol=tol, omega=omega, max_sweeps=200000)
-            Vo = H.owned_voltages(g)
+            H.owned_voltages(g)
             sm = H.specs[0]
             h2d = 8 * g.layers * (sm.hi - sm.lo) * g.nx * 4
             d2h = 8 * g.layers * (sm.hi - sm.lo) * g.nx
@@ -422,17 +530,20 @@ def run_b200(args):
         dist.all_reduce(ns)
         e2e = {"value": float(ns.item()) / (float(te.item()) * 1e-3) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": float(te.item()) / nrep, "per_rank_bytes": True}
+               "ms_per_step": float(te.item()) / nrep, "per_rank_bytes": True,
+               "step": f"slab grid from host arrays + NCCL group + time steps 1..{T} + owned voltages read back"}
     elif not args.no_e2e and args.slabs <= 1:
         pin = {}
-        for name in ("gx", "gy", "gz", "cap", "lz"):
+        for name in ("gx", "gy", "gz", "cap", "lz", "eu", "ev", "eg"):
             a = getattr(g, name, None)
             if a is not None:
-                pt = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
-                pin[name] = pt.numpy()
-        h2d = sum(v.nbytes for v in pin.values()) + g.pad_node.nbytes + g.pad_g.nbytes
+                pin[name] = torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
         s = g.sources
-        h2d += s.node.nbytes + s.ptr.nbytes + s.t.nbytes + s.i.nbytes
+        for name, a in (("pad_node", g.pad_node), ("pad_g", g.pad_g), ("pad_l", getattr(g, "pad_l", None)),
+                        ("src_node", s.node), ("src_ptr", s.ptr), ("src_t", s.t), ("src_i", s.i)):
+            if a is not None:
+                pin[name] = torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+        h2d = sum(v.nbytes for v in pin.values())
         out = torch.empty(g.n, dtype=torch.float64).pin_memory().numpy()
         d2h = out.nbytes
         barrier()
@@ -440,16 +551,17 @@ def run_b200(args):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         e_sweeps = 0
-        for _ in range(max(1, min(args.steps, 2))):
+        for _ in range(nrep):
             if hasattr(g, "gx"):
                 H = P.Grid.mesh(g.layers, g.ny, g.nx, pin["gx"], pin["gy"], pin["gz"], pin["cap"],
-                                g.pad_node, g.pad_g, g.vdd, pin.get("lz"), g.pad_l)
+                                pin["pad_node"], pin["pad_g"], g.vdd, pin.get("lz"), pin.get("pad_l"))
             else:
-                H = P.Grid.from_edge_grid(g)
+                H = P.Grid.csr(g.n, pin["eu"], pin["ev"], pin["eg"], pin["cap"], pin["pad_node"], pin["pad_g"],
+                               g.vdd)
             H.set_stream(stream)
             for k, v in opts.items():
                 H.set_option(k, int(v))
-            H.set_sources(s.node, s.ptr, s.t, s.i)
+            H.set_sources(pin["src_node"], pin["src_ptr"], pin["src_t"], pin["src_i"])
             rr = H.transient(g.h, T, tol=tol, omega=omega, method=args.method, max_sweeps=200000)
             H.voltages(out)
             H.close()
@@ -457,13 +569,12 @@ def run_b200(args):
         e1.record(stream)
         barrier()
         ems = e0.elapsed_time(e1)
-        te = torch.tensor([ems], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        nrep = max(1, min(args.steps, 2))
-        e2e = {"value": float(g.n) * e_sweeps * world / (float(te.item()) * 1e-3) / 1e9, "unit": UNIT,
+        e2e = {"value": float(g.n) * e_sweeps / (ems * 1e-3) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": float(te.item()) / nrep}
+               "ms_per_step": ems / nrep,
+               "step": (f"pg_create_{'mesh' if hasattr(g, 'gx') else 'csr'} + pg_set_sources from pinned host "
+                        f"arrays, pg_transient over time steps 1..{T} from x(0), pg_get_voltages into pinned "
+                        f"host memory, pg_destroy")}
 
     cpu = None
     if rank == 0 and not args.no_cpu:
@@ -473,30 +584,26 @@ def run_b200(args):
             cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": f"failed: {e}"}
 
     spt = np.concatenate(sweeps_per_tstep) if sweeps_per_tstep else np.zeros(1)
+    full = None
+    starts = list(range(0, TOT - T + 1, T))
+    if TOT % T == 0 and all(s in win_ms for s in starts):
+        full = sum(win_ms[s] for s in starts) / TOT
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": args.scaling if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded BASELINE.json recipe, gridgen)",
-            "config": {"workload": f"config{cfg}" + (f" x{world} rows (weak scaling)" if world > 1 and
-                                                     args.scaling == "weak" else ""), "nodes": g.n,
-                       "mesh": [g.layers, g.ny, g.nx] if hasattr(g, "gx") else None,
-                       "h_s": g.h, "time_steps_per_bench_step": T, "tol_V": tol, "omega": omega,
-                       "omega_source": omega_src, "omega_estimate_s": round(t_om, 3),
-                       "method": args.method, "options": opts, "ms_per_time_step": ms_max / args.steps / T,
+            "config": config_dict(cfg, g, T, tol, omega, omega_src, args.method, opts, world, args.scaling,
+                                  transport, args.slabs),
+            "detail": {"ms_per_time_step": ms_max / args.steps / T,
+                       "full_transient_ms_per_time_step": full,
+                       "full_transient_note": (f"all {TOT} time steps, sum of the CUDA-event times of the "
+                                               f"{len(starts)} windows of the first pass (warm-up windows "
+                                               f"included) / {TOT}") if full is not None else None,
                        "sweeps_per_time_step_mean": float(spt.mean()),
                        "sweeps_per_time_step_max": int(spt.max()),
-                       "l2": "per-sweep working set ~56 B/node x n > 126 MB L2 (no flush needed)",
-                       "parallelism": (f"slab{world}: rows split over {world} GPUs, "
-                                       + ("ghost rows and norm exchanged by the sweep kernel over peer "
-                                          "memory (CUDA IPC)" if p2p else
-                                          "NCCL ghost-row exchange + norm allreduce per sweep launch"))
-                       if world > 1
-                       else (f"1 GPU, {args.slabs} row slabs exchanged in one process ("
-                             + ("pg_group_local_p2p: peer-memory exchange in the sweep kernel"
-                                if p2p else "pg_group_local: copies") + ")"
-                             if args.slabs > 1 else "1 GPU")},
+                       "omega_time_s": round(t_om, 3)},
             "clocks": ck, "e2e": e2e, "gpu_launches": launches, "roofline": roof,
             "cpu_baseline": cpu,
         }

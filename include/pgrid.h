@@ -51,7 +51,8 @@ enum {
   PG_ECUDA = -2,     /* CUDA runtime / launch error (message carries cudaGetErrorString) */
   PG_ENOCONV = -3,   /* a time step hit max_sweeps without meeting tol (results still written) */
   PG_ENOMEM = -4,    /* device allocation failed */
-  PG_ESTATE = -5     /* call not valid for this grid (e.g. RLC data on a CSR grid) */
+  PG_ESTATE = -5,    /* call not valid for this grid (e.g. RLC data on a CSR grid) */
+  PG_ENONFINITE = -6 /* an iterate became NaN / Inf (e.g. from non-finite device inputs); results invalid */
 };
 
 enum {
@@ -173,7 +174,9 @@ typedef struct {
  * of length h (> 0).  Each step: fused RHS kernel (PWL loads at t+h, C/h x(t),
  * pad and inductor history) -> relaxation sweeps from V(s-1) until
  * max_i |V_i^(k) - V_i^(k-1)| < tol (Algorithm 1 line 8, infinity norm) or
- * max_sweeps -> inductor companion-current update.  tol <= 0 runs exactly
+ * max_sweeps -> inductor companion-current update.  The RHS kernel and one
+ * pass after the last step check the iterates for NaN / Inf (PG_ENONFINITE).
+ * tol <= 0 runs exactly
  * max_sweeps sweeps per step.  omega in (0, 2) (Eq. (15); 1 = Gauss-Seidel).
  * method: PG_METHOD_RBSOR or PG_METHOD_JACOBI.  When the fused sweep kernel
  * checks convergence every F sweeps (option "fuse"), a step may run up to
@@ -187,6 +190,21 @@ PG_API int pg_transient(pg_grid *g, double h, int64_t steps, double tol, double 
                         int method, int64_t max_sweeps, int64_t n_probe,
                         const int64_t *probe_node, double *probe_out, int mem,
                         int64_t *sweeps_out, pg_stats *stats);
+
+/* Algorithm 1 continued: `steps` more backward-Euler steps from the grid's
+ * current state -- the voltages and inductor currents left by the previous
+ * pg_transient / pg_transient_continue call (steps s0+1 .. s0+steps at
+ * t = s h, s0 = the steps taken since x(0)), or by pg_set_voltages / pg_dc
+ * (s0 = 0: the state is x(0) at t = 0; after pg_dc it is the DC operating
+ * point).  A transient cut into consecutive calls gives the same results
+ * as one call over all its steps (Algorithm 1 line 2 loop; the time
+ * loop only carries V and the inductor currents).  h must equal the h of the
+ * steps taken so far (PG_EINVAL otherwise).  Probes record V(s0 h) at row 0
+ * and V((s0+k) h) at row k.  Other arguments and results as pg_transient.   */
+PG_API int pg_transient_continue(pg_grid *g, double h, int64_t steps, double tol, double omega,
+                                 int method, int64_t max_sweeps, int64_t n_probe,
+                                 const int64_t *probe_node, double *probe_out, int mem,
+                                 int64_t *sweeps_out, pg_stats *stats);
 
 /* ---- Multi-GPU: slab partition of a mesh -------------------
  * A global layers x NY x nx mesh is cut into blocks of rows ("slabs"), one per
@@ -267,6 +285,11 @@ PG_API int pg_group_p2p_connect(pg_group *grp, const void *blobs, int64_t blob_l
 
 PG_API int pg_group_transient(pg_group *grp, double h, int64_t steps, double tol, double omega,
                               int64_t max_sweeps, int64_t *sweeps_out, pg_stats *stats);
+
+/* pg_group_transient continued from every slab's current state (as
+ * pg_transient_continue for a single grid).  Collective.                  */
+PG_API int pg_group_transient_continue(pg_group *grp, double h, int64_t steps, double tol, double omega,
+                                       int64_t max_sweeps, int64_t *sweeps_out, pg_stats *stats);
 
 /* Free the group's buffers and communicator (the slab grids stay).  NULL ok. */
 PG_API void pg_group_destroy(pg_group *grp);

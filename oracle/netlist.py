@@ -180,29 +180,55 @@ class NodeLists:
     lres: np.ndarray = None  # series resistance of the inductor branch (0: pure inductor)
 
 
+def _group_numpy(n, a, b, val):
+    """Reference grouping (stable argsort of the concatenated end list); the
+    oracle uses the equivalent plain-C counting sort ``oracle_group`` (memory:
+    full-size grids), checked equal to this in tests/test_oracle_pins.py."""
+    ends_i, ends_j, vals, br, sg = [], [], [], [], []
+    idx = np.arange(a.size, dtype=np.int64)
+    m = a >= 0
+    ends_i.append(a[m]); ends_j.append(b[m]); vals.append(val[m]); br.append(idx[m]); sg.append(np.ones(m.sum()))
+    m = b >= 0
+    ends_i.append(b[m]); ends_j.append(a[m]); vals.append(val[m]); br.append(idx[m]); sg.append(-np.ones(m.sum()))
+    ei = np.concatenate(ends_i); ej = np.concatenate(ends_j); ev = np.concatenate(vals)
+    eb = np.concatenate(br); es = np.concatenate(sg)
+    o = np.argsort(ei, kind="stable")
+    ei, ej, ev, eb, es = ei[o], ej[o], ev[o], eb[o], es[o]
+    ptr = np.zeros(n + 1, dtype=np.int64)
+    np.add.at(ptr, ei + 1, 1)
+    ptr = np.cumsum(ptr)
+    return ptr, ej.astype(np.int64), ev.astype(np.float64), eb.astype(np.int64), es.astype(np.float64)
+
+
+def group(n, a, b, val, with_branch=True):
+    """Each branch a[k] -> b[k] appears in the list of each trivial endpoint:
+    (ptr, nbr, val, branch, sign), entries of node i in ptr[i]:ptr[i+1] (a-ends
+    in branch order, then b-ends).  Plain-C counting sort (nodal.c)."""
+    import ctypes
+    from . import nodal
+    a = np.ascontiguousarray(a, dtype=np.int64)
+    b = np.ascontiguousarray(b, dtype=np.int64)
+    val = np.ascontiguousarray(val, dtype=np.float64)
+    cnt = int(np.count_nonzero(a >= 0)) + int(np.count_nonzero(b >= 0))
+    ptr = np.zeros(n + 1, dtype=np.int64)
+    nbr = np.empty(cnt, dtype=np.int64)
+    vo = np.empty(cnt, dtype=np.float64)
+    br = np.empty(cnt, dtype=np.int64) if with_branch else None
+    sg = np.empty(cnt, dtype=np.float64) if with_branch else None
+    P64, PD = ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_double)
+    nodal.lib().oracle_group(ctypes.c_int64(n), ctypes.c_int64(a.size), a.ctypes.data_as(P64),
+                             b.ctypes.data_as(P64), val.ctypes.data_as(PD), ptr.ctypes.data_as(P64),
+                             nbr.ctypes.data_as(P64), vo.ctypes.data_as(PD),
+                             br.ctypes.data_as(P64) if with_branch else None,
+                             sg.ctypes.data_as(PD) if with_branch else None)
+    return ptr, nbr, vo, br, sg
+
+
 def node_lists(nl: Netlist) -> NodeLists:
     """Build N_i^R, N_i^L, C_i of Eq. (12) from the branch list."""
     n = nl.n
-
-    def group(a, b, val, extra=None):
-        # each branch appears in the list of each trivial endpoint
-        ends_i, ends_j, vals, br, sg = [], [], [], [], []
-        idx = np.arange(a.size, dtype=np.int64)
-        m = a >= 0
-        ends_i.append(a[m]); ends_j.append(b[m]); vals.append(val[m]); br.append(idx[m]); sg.append(np.ones(m.sum()))
-        m = b >= 0
-        ends_i.append(b[m]); ends_j.append(a[m]); vals.append(val[m]); br.append(idx[m]); sg.append(-np.ones(m.sum()))
-        ei = np.concatenate(ends_i); ej = np.concatenate(ends_j); ev = np.concatenate(vals)
-        eb = np.concatenate(br); es = np.concatenate(sg)
-        o = np.argsort(ei, kind="stable")
-        ei, ej, ev, eb, es = ei[o], ej[o], ev[o], eb[o], es[o]
-        ptr = np.zeros(n + 1, dtype=np.int64)
-        np.add.at(ptr, ei + 1, 1)
-        ptr = np.cumsum(ptr)
-        return ptr, ej.astype(np.int64), ev.astype(np.float64), eb.astype(np.int64), es.astype(np.float64)
-
-    rptr, rnbr, rg, _, _ = group(nl.ra, nl.rb, nl.rg)
-    lptr, lnbr, lval, lbr, lsgn = group(nl.la, nl.lb, nl.lv)
+    rptr, rnbr, rg, _, _ = group(n, nl.ra, nl.rb, nl.rg, with_branch=False)
+    lptr, lnbr, lval, lbr, lsgn = group(n, nl.la, nl.lb, nl.lv)
     lres = np.asarray(nl.lr, dtype=np.float64)[lbr] if lbr.size else np.zeros(0)
     cap = np.zeros(n)
     if np.any((nl.ca >= 0) & (nl.cb >= 0)) or np.any(nl.cb < -1) or np.any(nl.ca < 0):

@@ -17,6 +17,34 @@
 #include <stdlib.h>
 #include <string.h>
 
+/* Per-node branch lists N_i of Eq. (12) from a branch list a[k] -> b[k]:
+ * every branch appears in the list of each trivial endpoint (a >= 0, b >= 0).
+ * Inside a node's list the entries are the a-ends in branch order, then the
+ * b-ends in branch order (a stable counting sort of the concatenated end
+ * list).  ptr[n+1] (caller-zeroed), nbr/val[2m upper bound]; br/sgn may be NULL.
+ * Plain two-pass counting sort: count degrees, prefix-sum, fill.             */
+void oracle_group(int64_t n, int64_t m, const int64_t *a, const int64_t *b, const double *val,
+                  int64_t *ptr, int64_t *nbr, double *vout, int64_t *br, double *sgn) {
+  for (int64_t k = 0; k < m; ++k) {
+    if (a[k] >= 0) ptr[a[k] + 1] += 1;
+    if (b[k] >= 0) ptr[b[k] + 1] += 1;
+  }
+  for (int64_t i = 0; i < n; ++i) ptr[i + 1] += ptr[i];
+  int64_t *fill = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+  memcpy(fill, ptr, sizeof(int64_t) * (size_t)n);
+  for (int pass = 0; pass < 2; ++pass)
+    for (int64_t k = 0; k < m; ++k) {
+      const int64_t i = pass == 0 ? a[k] : b[k], j = pass == 0 ? b[k] : a[k];
+      if (i < 0) continue;
+      const int64_t q = fill[i]++;
+      nbr[q] = j;
+      vout[q] = val[k];
+      if (br) br[q] = k;
+      if (sgn) sgn[q] = pass == 0 ? 1.0 : -1.0;
+    }
+  free(fill);
+}
+
 static double v_of(int64_t j, const double *V, const double *vd) {
   if (j >= 0) return V[j];
   if (j == -1) return 0.0;
@@ -163,6 +191,12 @@ void oracle_inductor_update(int64_t nl, const int64_t *la, const int64_t *lb,
  * Iload: [(steps+1) * n] per-node load currents I_i(s h).
  * Vout:  [(steps+1) * n] nodal voltages V(s) (V(0) [and V(1)] copied in).
  * sweeps_out[s]: inner iterations k taken at step s.
+ * dtrace (nullable, [(steps+1) * 6], Gauss-Seidel/SOR only): the stopping
+ *   record of step s -- ||V^(k-1) - V^(k-2)|| (NAN if k = 1), ||V^(k) -
+ *   V^(k-1)||, then the norms of 4 further sweeps continued on a scratch copy
+ *   of V^(k) (diagnostic only: V(s) stays V^(k)).  The GPU tests its stopping
+ *   criterion every F sweeps (R13); these let a test compute the
+ *   sweep at which that criterion first holds.
  * Returns 0, or -(s) if step s hit max_sweeps without meeting tol.          */
 int64_t oracle_transient(int64_t n, const int64_t *order, const int64_t *rptr,
                          const int64_t *rnbr, const double *rg, const int64_t *lptr,
@@ -172,7 +206,7 @@ int64_t oracle_transient(int64_t n, const int64_t *order, const int64_t *rptr,
                          const double *vd, int form, int method, double h,
                          int64_t steps, double tol, double omega, int64_t max_sweeps,
                          const double *Iload, const double *V0, const double *V1,
-                         double *il, double *Vout, int64_t *sweeps_out) {
+                         double *il, double *Vout, int64_t *sweeps_out, double *dtrace) {
   double *d = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
   double *known = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
   double *tmp = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
@@ -198,9 +232,10 @@ int64_t oracle_transient(int64_t n, const int64_t *order, const int64_t *rptr,
                                 known);
     memcpy(Vs, Vt, sizeof(double) * (size_t)n); /* Algorithm 1 line 3: V^(0)(s) = V(s-1) */
     int64_t k = 0;
-    double dmax;
+    double dmax = NAN, dprev = NAN;
     do {
       ++k;
+      dprev = dmax;
       if (method == 0) {
         dmax = oracle_sweep(n, order, rptr, rnbr, rg, lptr, lnbr, lval, lres, h, d, known, omega, Vs);
       } else {
@@ -209,6 +244,17 @@ int64_t oracle_transient(int64_t n, const int64_t *order, const int64_t *rptr,
       }
     } while (!(dmax < tol) && k < max_sweeps); /* line 8: until ||V^(k) - V^(k-1)|| < tol */
     sweeps_out[s] = k;
+    if (dtrace) {
+      double *r = dtrace + s * 6;
+      r[0] = dprev;
+      r[1] = dmax;
+      for (int e = 2; e < 6; ++e) r[e] = NAN;
+      if (method == 0) {
+        memcpy(tmp, Vs, sizeof(double) * (size_t)n);
+        for (int e = 2; e < 6; ++e)
+          r[e] = oracle_sweep(n, order, rptr, rnbr, rg, lptr, lnbr, lval, lres, h, d, known, omega, tmp);
+      }
+    }
     if (!(dmax < tol) && status == 0) status = -s;
     if (form == 0 && nind > 0) oracle_inductor_update(nind, la, lb, lv, lr, vd, h, Vs, il);
   }

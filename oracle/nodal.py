@@ -69,6 +69,7 @@ class TransientResult:
     sweeps: np.ndarray     # [steps+1]
     il: np.ndarray         # inductor currents after the last step
     status: int
+    dtrace: np.ndarray = None  # [steps+1, 6] stopping record (nodal.c oracle_transient), if asked
 
 
 class NodalOracle:
@@ -137,7 +138,8 @@ class NodalOracle:
     # -- Algorithm 1 ----------------------------------------------------------
     def transient(self, h: float, steps: int, tol: float = 1e-10, omega: float = 1.0,
                   form: str = "companion", method: str = "gs", order=None,
-                  Itab=None, V0=None, V1=None, il0=None, max_sweeps: int = 1_000_000):
+                  Itab=None, V0=None, V1=None, il0=None, max_sweeps: int = 1_000_000,
+                  trace: bool = False):
         nl = self.nl
         n = nl.n
         if Itab is None:
@@ -158,6 +160,7 @@ class NodalOracle:
         il = _cd(np.zeros(nl.la.size) if il0 is None else il0).copy()
         Vout = np.zeros((steps + 1, n))
         sw = np.zeros(steps + 1, dtype=np.int64)
+        dt = np.full((steps + 1, 6), np.nan) if trace else None
         o = None if order is None else _c64(order)
         st = lib().oracle_transient(
             ctypes.c_int64(n), _p64(o) if o is not None else None,
@@ -168,8 +171,9 @@ class NodalOracle:
             ctypes.c_int(f), ctypes.c_int(0 if method == "gs" else 1),
             ctypes.c_double(h), ctypes.c_int64(steps), ctypes.c_double(tol),
             ctypes.c_double(omega), ctypes.c_int64(max_sweeps), _pd(Itab), _pd(V0),
-            _pd(V1) if f == 1 else None, _pd(il), _pd(Vout), _p64(sw))
-        return TransientResult(V=Vout, sweeps=sw, il=il, status=int(st))
+            _pd(V1) if f == 1 else None, _pd(il), _pd(Vout), _p64(sw),
+            _pd(dt) if trace else None)
+        return TransientResult(V=Vout, sweeps=sw, il=il, status=int(st), dtrace=dt)
 
 
 def red_black_order(layers: int, ny: int, nx: int) -> np.ndarray:

@@ -29,27 +29,32 @@ def node_currents(nl, t: float) -> np.ndarray:
 
 
 def node_currents_table(nl, h: float, steps: int) -> np.ndarray:
-    """[steps+1, n] table of I_i(s*h), s = 0..steps (vectorised over sources
-    with the same breakpoint count; falls back to the loop otherwise)."""
+    """[steps+1, n] table of I_i(s*h), s = 0..steps."""
     tab = np.zeros((steps + 1, nl.n))
-    ts = np.arange(steps + 1, dtype=np.float64) * h
-    cnt = np.diff(nl.iptr)
-    if nl.ia.size == 0:
-        return tab
-    if np.all(cnt == cnt[0]):
-        k = int(cnt[0])
-        T = nl.it.reshape(-1, k)
-        I = nl.ii.reshape(-1, k)
-        for s, t in enumerate(ts):
-            v = _interp_rows(T, I, t)
-            np.add.at(tab[s], nl.ia[nl.ia >= 0], v[nl.ia >= 0])
-            nb = nl.ib >= 0
-            if nb.any():
-                np.add.at(tab[s], nl.ib[nb], -v[nb])
-        return tab
-    for s, t in enumerate(ts):
-        tab[s] = node_currents(nl, t)
+    for s in range(steps + 1):
+        tab[s] = node_currents_at(nl, s * h)
     return tab
+
+
+def node_currents_at(nl, t: float) -> np.ndarray:
+    """I_i(t) for every trivial node (as ``node_currents``), vectorised over
+    sources with the same breakpoint count; falls back to the loop otherwise."""
+    out = np.zeros(nl.n)
+    if nl.ia.size == 0:
+        return out
+    cnt = np.diff(nl.iptr)
+    if not np.all(cnt == cnt[0]):
+        return node_currents(nl, t)
+    k = int(cnt[0])
+    T = nl.it.reshape(-1, k)
+    I = nl.ii.reshape(-1, k)
+    v = _interp_rows(T, I, t)
+    na = nl.ia >= 0
+    np.add.at(out, nl.ia[na], v[na])
+    nb = nl.ib >= 0
+    if nb.any():
+        np.add.at(out, nl.ib[nb], -v[nb])
+    return out
 
 
 def _interp_rows(T: np.ndarray, I: np.ndarray, t: float) -> np.ndarray:

@@ -13,7 +13,7 @@ LIB_PATH = os.environ.get("PGB200_LIB") or os.path.join(HERE, "lib", "libpgb200.
 
 PG_MEM_HOST = 0
 PG_MEM_DEVICE = 1
-PG_OK, PG_EINVAL, PG_ECUDA, PG_ENOCONV, PG_ENOMEM, PG_ESTATE = 0, -1, -2, -3, -4, -5
+PG_OK, PG_EINVAL, PG_ECUDA, PG_ENOCONV, PG_ENOMEM, PG_ESTATE, PG_ENONFINITE = 0, -1, -2, -3, -4, -5, -6
 PG_METHOD_RBSOR = 0
 PG_METHOD_JACOBI = 1
 
@@ -44,6 +44,8 @@ SIGNATURES = {
     "pg_set_option": (_c_int, [_vp, ctypes.c_char_p, _i64]),
     "pg_transient": (_c_int, [_vp, _dbl, _i64, _dbl, _dbl, _c_int, _i64, _i64, _vp, _vp, _c_int,
                               _vp, ctypes.POINTER(PgStats)]),
+    "pg_transient_continue": (_c_int, [_vp, _dbl, _i64, _dbl, _dbl, _c_int, _i64, _i64, _vp, _vp,
+                                       _c_int, _vp, ctypes.POINTER(PgStats)]),
     "pg_info": (_c_int, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i32), ctypes.POINTER(_i32),
                          ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),
     "pg_destroy": (None, [_vp]),
@@ -58,6 +60,8 @@ SIGNATURES = {
     "pg_group_p2p_export": (_c_int, [_vp, _vp, _i64, ctypes.POINTER(_i64)]),
     "pg_group_p2p_connect": (_c_int, [_vp, _vp, _i64]),
     "pg_group_transient": (_c_int, [_vp, _dbl, _i64, _dbl, _dbl, _i64, _vp, ctypes.POINTER(PgStats)]),
+    "pg_group_transient_continue": (_c_int, [_vp, _dbl, _i64, _dbl, _dbl, _i64, _vp,
+                                             ctypes.POINTER(PgStats)]),
     "pg_group_destroy": (None, [_vp]),
     "pg_last_error": (ctypes.c_char_p, []),
 }

@@ -56,6 +56,16 @@ def _d(x):
     return _Arr(x, np.float64)
 
 
+def _len(x) -> int:
+    return 0 if x is None else int(x.numel() if _is_torch(x) else np.size(x))
+
+
+def _need(name, x, n):
+    """The C side reads / writes exactly n elements: refuse other sizes."""
+    if x is not None and _len(x) != n:
+        raise ValueError(f"{name} has {_len(x)} elements, expected {n}")
+
+
 def _i(x):
     return _Arr(x, np.int64)
 
@@ -80,13 +90,18 @@ class Grid:
     def mesh(cls, layers, ny, nx, gx, gy, gz, cap, pad_node, pad_g, vdd=1.0, lz=None,
              pad_l=None) -> "Grid":
         lib = L.load()
+        n = int(layers) * int(ny) * int(nx)
+        for name, a in (("gx", gx), ("gy", gy), ("gz", gz), ("cap", cap), ("lz", lz)):
+            _need(name, a, n)
+        npad = _len(pad_node)
+        _need("pad_g", pad_g, npad)
+        _need("pad_l", pad_l, npad)
         mem = _mem_of(gx, gy, gz, cap, lz)
         pmem = _mem_of(pad_node, pad_g, pad_l)
         if pmem != mem:
             raise ValueError("pads must live in the same memory as the grid arrays")
         A = [_d(gx), _d(gy), _d(gz), _d(lz), _d(cap)]
         pn, pg, pl = _i(pad_node), _d(pad_g), _d(pad_l)
-        npad = 0 if pad_node is None else int(len(pad_node))
         out = ctypes.c_void_p()
         L.check(lib.pg_create_mesh(int(layers), int(ny), int(nx), A[0].ptr, A[1].ptr, A[2].ptr,
                                    A[3].ptr, A[4].ptr, npad, pn.ptr, pg.ptr, pl.ptr, float(vdd),
@@ -107,6 +122,11 @@ class Grid:
     @classmethod
     def csr(cls, n, bu, bv, bg, cap, pad_node, pad_g, vdd=1.0) -> "Grid":
         lib = L.load()
+        m = _len(bu)
+        _need("bv", bv, m)
+        _need("bg", bg, m)
+        _need("cap", cap, int(n))
+        _need("pad_g", pad_g, _len(pad_node))
         mem = _mem_of(bu, bv, bg, cap, pad_node, pad_g)
         u, v, w, c = _i(bu), _i(bv), _d(bg), _d(cap)
         pn, pg = _i(pad_node), _d(pad_g)
@@ -127,17 +147,24 @@ class Grid:
 
     # ------------------------------------------------------------------ state
     def set_sources(self, node, ptr, t, i):
+        ns = _len(node)
+        _need("ptr", ptr, ns + 1)
+        npts = int(ptr[-1]) if ns > 0 else _len(t)
+        _need("t", t, npts)
+        _need("i", i, npts)
         mem = _mem_of(node, ptr, t, i)
         a, b, c, d = _i(node), _i(ptr), _d(t), _d(i)
         L.check(self._lib.pg_set_sources(self._h, int(len(node)), a.ptr, b.ptr, c.ptr, d.ptr, mem))
 
     def set_voltages(self, v):
+        _need("v", v, self.n)
         a = _d(v)
         L.check(self._lib.pg_set_voltages(self._h, a.ptr, _mem_of(v)))
 
     def voltages(self, out=None):
         if out is None:
             out = np.empty(self.n)
+        _need("out", out, self.n)
         mem = _mem_of(out)
         L.check(self._lib.pg_get_voltages(self._h, _ptr_of(out), mem))
         return out
@@ -162,7 +189,9 @@ class Grid:
 
     # -------------------------------------------------------------- Algorithm 1
     def transient(self, h, steps, tol=1e-10, omega=1.0, method="rbsor", max_sweeps=100000,
-                  probes=None, probe_out=None, raise_on_noconv=True) -> TransientResult:
+                  probes=None, probe_out=None, raise_on_noconv=True, cont=False) -> TransientResult:
+        """pg_transient (from x(0)) or, with cont=True, pg_transient_continue
+        (from the state the previous call left)."""
         m = {"rbsor": L.PG_METHOD_RBSOR, "jacobi": L.PG_METHOD_JACOBI}[method]
         npr = 0 if probes is None else int(len(probes))
         if npr and probe_out is None:
@@ -171,14 +200,16 @@ class Grid:
                 probe_out = torch.empty((steps + 1, npr), dtype=torch.float64, device=probes.device)
             else:
                 probe_out = np.empty((steps + 1, npr))
+        if npr:
+            _need("probe_out", probe_out, (int(steps) + 1) * npr)
         mem = _mem_of(probes, probe_out) if npr else L.PG_MEM_HOST
         pa = _i(probes)
         sweeps = np.zeros(steps + 1, dtype=np.int64)
         st = L.PgStats()
-        code = self._lib.pg_transient(self._h, float(h), int(steps), float(tol), float(omega), m,
-                                      int(max_sweeps), npr, pa.ptr,
-                                      _ptr_of(probe_out) if npr else None, mem,
-                                      sweeps.ctypes.data, ctypes.byref(st))
+        fn = self._lib.pg_transient_continue if cont else self._lib.pg_transient
+        code = fn(self._h, float(h), int(steps), float(tol), float(omega), m, int(max_sweeps), npr,
+                  pa.ptr, _ptr_of(probe_out) if npr else None, mem, sweeps.ctypes.data,
+                  ctypes.byref(st))
         if code not in (L.PG_OK, L.PG_ENOCONV) or (code == L.PG_ENOCONV and raise_on_noconv):
             L.check(code)
         return TransientResult(probes=probe_out if npr else None, sweeps=sweeps, stats=st,

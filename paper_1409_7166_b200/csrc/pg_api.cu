@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -84,7 +85,9 @@ DevPool *pool_of(int dev) {
   return d.pool ? &d : nullptr;
 }
 
-void dfree(void *p) {
+// synced: the caller already synchronized the device (free_grid does it once
+// for all of a grid's blocks instead of once per block)
+void dfree(void *p, bool synced = false) {
   if (!p) return;
   int dev = -1;
   {
@@ -102,7 +105,7 @@ void dfree(void *p) {
   int cur = 0;
   cudaGetDevice(&cur);
   if (cur != dev) cudaSetDevice(dev);
-  cudaDeviceSynchronize();  // the block may still be in use on any stream (cudaFree semantics)
+  if (!synced) cudaDeviceSynchronize();  // the block may still be in use on any stream (cudaFree semantics)
   DevPool *d;
   {
     std::lock_guard<std::mutex> lk(g_pool_mu);
@@ -130,6 +133,15 @@ int dalloc(T **p, int64_t count, bool plain = false) {
     // (TMA tensor maps and vector loads rely on it); checked below
     e = cudaMallocFromPoolAsync((void **)p, (bytes + 255) & ~(size_t)255, d->pool, d->s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(d->s);
+    if (e != cudaSuccess) {
+      // the pool's cached free blocks may be what is missing: release them to
+      // the device and retry once before falling back to cudaMalloc
+      cudaGetLastError();
+      cudaStreamSynchronize(d->s);
+      cudaMemPoolTrimTo(d->pool, 0);
+      e = cudaMallocFromPoolAsync((void **)p, (bytes + 255) & ~(size_t)255, d->pool, d->s);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(d->s);
+    }
     if (e == cudaSuccess && ((uintptr_t)*p & 255)) {
       cudaFreeAsync(*p, d->s);
       cudaStreamSynchronize(d->s);
@@ -175,19 +187,38 @@ int upload(T *dst, const std::vector<T> &v) {
   return PG_OK;
 }
 
+std::atomic<int> g_live_grids[64];  // grids alive per device (the pool is trimmed when none is)
+
 void free_grid(pg_grid *g) {
   if (!g) return;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  const bool other = g->dev >= 0 && cur != g->dev;
+  if (other) cudaSetDevice(g->dev);
+  cudaDeviceSynchronize();  // every block below may still be in use on some stream
   void *ptrs[] = {g->gx, g->gy, g->gz, g->lz, g->gze, g->iz, g->rowptr, g->col, g->val, g->perm,
                   g->iperm, g->V[0], g->V[1], g->x0, g->cap, g->invd, g->b, g->pad_idx,
                   g->pad_grp, g->pad_g, g->pad_l, g->pad_ge, g->pad_i, g->src_idx, g->src_grp,
-                  g->src_ptr, g->pwl_t, g->pwl_i, g->ctl, g->dev_sweeps, g->user_buf};  // ctl: plain (dfree -> cudaFree)
+                  g->src_ptr, g->pwl_t, g->pwl_i, g->pad_tile, g->src_tile, g->ctl, g->dev_sweeps,
+                  g->user_buf};  // ctl: plain (dfree -> cudaFree)
   for (void *p : ptrs)
-    if (p) dfree(p);
+    if (p) dfree(p, true);
   for (cudaEvent_t e : g->tev) cudaEventDestroy(e);
   if (g->batch_exec) cudaGraphExecDestroy(g->batch_exec);
   if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
   if (g->ctl_host) cudaFreeHost(g->ctl_host);
   if (g->done_host) cudaFreeHost(g->done_host);
+  if (g->counted && g->dev >= 0 && g->dev < 64 && g_live_grids[g->dev].fetch_sub(1) == 1) {
+    // the last grid of this device: hand the pool's cached memory back to the
+    // device, so other users of cudaMalloc (NCCL, torch, halo buffers) can have it
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    DevPool *d = pool_of(g->dev);
+    if (d) {
+      cudaStreamSynchronize(d->s);
+      cudaMemPoolTrimTo(d->pool, 0);
+    }
+  }
+  if (other) cudaSetDevice(cur);
   delete g;
 }
 
@@ -217,7 +248,12 @@ std::vector<int64_t> groups_of(const std::vector<int64_t> &sidx) {
 
 int common_init(pg_grid *g) {
   CK(cudaGetDevice(&g->dev));
+  if (g->dev >= 0 && g->dev < 64) {
+    g_live_grids[g->dev].fetch_add(1);
+    g->counted = true;
+  }
   CK(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, g->dev));
+  g->ntile = (g->np + kRhsTile - 1) / kRhsTile;
   int rc;
   if ((rc = dalloc(&g->V[0], g->np)) || (rc = dalloc(&g->V[1], g->np)) || (rc = dalloc(&g->x0, g->np)) ||
       (rc = dalloc(&g->invd, g->np)) || (rc = dalloc(&g->b, g->np)) || (rc = dalloc(&g->ctl, 1, true)))
@@ -265,10 +301,16 @@ int set_pads(pg_grid *g, int64_t n_pads, const int64_t *pad_node, const double *
   std::vector<int64_t> grp = groups_of(s2);
   g->npad = n_pads;
   g->npad_grp = (int64_t)grp.size() - 1;
+  std::vector<int64_t> gnode((size_t)g->npad_grp);
+  for (int64_t q = 0; q < g->npad_grp; ++q) gnode[q] = s2[grp[q]];
+  const std::vector<int64_t> tiles = rhs_tile_starts(gnode, g->np);
   if ((rc = dalloc(&g->pad_idx, n_pads)) || (rc = dalloc(&g->pad_grp, (int64_t)grp.size())) ||
-      (rc = dalloc(&g->pad_g, n_pads)) || (rc = dalloc(&g->pad_ge, n_pads)))
+      (rc = dalloc(&g->pad_g, n_pads)) || (rc = dalloc(&g->pad_ge, n_pads)) ||
+      (rc = dalloc(&g->pad_tile, (int64_t)tiles.size())))
     return rc;
-  if ((rc = upload(g->pad_idx, s2)) || (rc = upload(g->pad_grp, grp)) || (rc = upload(g->pad_g, g2))) return rc;
+  if ((rc = upload(g->pad_idx, s2)) || (rc = upload(g->pad_grp, grp)) || (rc = upload(g->pad_g, g2)) ||
+      (rc = upload(g->pad_tile, tiles)))
+    return rc;
   if (pad_l && n_pads > 0) {
     if ((rc = dalloc(&g->pad_l, n_pads)) || (rc = dalloc(&g->pad_i, n_pads))) return rc;
     if ((rc = upload(g->pad_l, l2))) return rc;
@@ -501,11 +543,11 @@ PG_API int pg_set_sources(pg_grid *g, int64_t n_src, const int64_t *node, const 
   REQUIRE(g != nullptr, "grid is NULL");
   REQUIRE(n_src >= 0, "n_src must be >= 0");
   REQUIRE(mem == PG_MEM_HOST || mem == PG_MEM_DEVICE, "bad mem");
-  for (int64_t *p : {g->src_idx, g->src_grp, g->src_ptr})
+  for (int64_t *p : {g->src_idx, g->src_grp, g->src_ptr, g->src_tile})
     if (p) dfree(p);
   for (double *p : {g->pwl_t, g->pwl_i})
     if (p) dfree(p);
-  g->src_idx = g->src_grp = g->src_ptr = nullptr;
+  g->src_idx = g->src_grp = g->src_ptr = g->src_tile = nullptr;
   g->pwl_t = g->pwl_i = nullptr;
   g->nsrc = g->nsrc_grp = g->npts = 0;
   if (n_src == 0) return PG_OK;
@@ -529,9 +571,12 @@ PG_API int pg_set_sources(pg_grid *g, int64_t n_src, const int64_t *node, const 
     return rc;
   const double *tt = mem == PG_MEM_DEVICE ? tt_v.data() : t;
   const double *ii = mem == PG_MEM_DEVICE ? ii_v.data() : i;
-  for (int64_t k = 0; k < n_src; ++k)
+  for (int64_t k = 0; k < n_src; ++k) {
+    for (int64_t q = pp[k]; q < pp[k + 1]; ++q)
+      REQUIRE(std::isfinite(tt[q]) && std::isfinite(ii[q]), "PWL breakpoints and values must be finite");
     for (int64_t q = pp[k] + 1; q < pp[k + 1]; ++q)
       REQUIRE(tt[q] > tt[q - 1], "PWL breakpoint times must be strictly increasing");
+  }
   std::vector<int64_t> iperm_h;
   if (g->kind == 1) {
     iperm_h.resize((size_t)g->n);
@@ -587,11 +632,15 @@ PG_API int pg_set_sources(pg_grid *g, int64_t n_src, const int64_t *node, const 
   }
   p2[n_src] = off;
   std::vector<int64_t> grp = groups_of(s2);
+  std::vector<int64_t> gnode(grp.size() - 1);
+  for (size_t q = 0; q + 1 < grp.size(); ++q) gnode[q] = s2[grp[q]];
+  const std::vector<int64_t> tiles = rhs_tile_starts(gnode, g->np);
   if ((rc = dalloc(&g->src_idx, n_src)) || (rc = dalloc(&g->src_grp, (int64_t)grp.size())) ||
-      (rc = dalloc(&g->src_ptr, n_src + 1)) || (rc = dalloc(&g->pwl_t, npts)) || (rc = dalloc(&g->pwl_i, npts)))
+      (rc = dalloc(&g->src_ptr, n_src + 1)) || (rc = dalloc(&g->pwl_t, npts)) || (rc = dalloc(&g->pwl_i, npts)) ||
+      (rc = dalloc(&g->src_tile, (int64_t)tiles.size())))
     return rc;
   if ((rc = upload(g->src_idx, s2)) || (rc = upload(g->src_grp, grp)) || (rc = upload(g->src_ptr, p2)) ||
-      (rc = upload(g->pwl_t, t2)) || (rc = upload(g->pwl_i, i2)))
+      (rc = upload(g->pwl_t, t2)) || (rc = upload(g->pwl_i, i2)) || (rc = upload(g->src_tile, tiles)))
     return rc;
   g->nsrc = n_src;
   g->nsrc_grp = (int64_t)grp.size() - 1;
@@ -602,6 +651,11 @@ PG_API int pg_set_sources(pg_grid *g, int64_t n_src, const int64_t *node, const 
 PG_API int pg_set_voltages(pg_grid *g, const double *v, int mem) {
   REQUIRE(g != nullptr && v != nullptr, "grid/v is NULL");
   REQUIRE(mem == PG_MEM_HOST || mem == PG_MEM_DEVICE, "bad mem");
+  if (mem == PG_MEM_HOST) {
+    bool ok = true;
+    for (int64_t k = 0; k < g->n; ++k) ok &= std::isfinite(v[k]);
+    REQUIRE(ok, "voltages must be finite");
+  }
   int rc;
   if (!g->user_buf && (rc = dalloc(&g->user_buf, g->n))) return rc;
   double *tmp = g->user_buf;
@@ -615,6 +669,8 @@ PG_API int pg_set_voltages(pg_grid *g, const double *v, int mem) {
   if (e == cudaSuccess && g->pad_i) e = cudaMemsetAsync(g->pad_i, 0, sizeof(double) * g->npad, g->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
   if (e != cudaSuccess) return cuda_fail(e, "pg_set_voltages");
+  g->traj_steps = 0;
+  g->traj_h = 0.0;
   return PG_OK;
 }
 
@@ -648,14 +704,28 @@ PG_API int pg_transient(pg_grid *g, double h, int64_t steps, double tol, double 
                             probe_node, probe_out, mem, sweeps_out, stats);
 }
 
+PG_API int pg_transient_continue(pg_grid *g, double h, int64_t steps, double tol, double omega, int method,
+                                 int64_t max_sweeps, int64_t n_probe, const int64_t *probe_node,
+                                 double *probe_out, int mem, int64_t *sweeps_out, pg_stats *stats) {
+  REQUIRE(g != nullptr, "grid is NULL");
+  REQUIRE(!g->slab, "slab grids are driven through a pg_group (pg_group_transient_continue)");
+  pg_grid *gs[1] = {g};
+  return pgb::run_transient(gs, 1, nullptr, h, steps, tol, omega, method, max_sweeps, n_probe,
+                            probe_node, probe_out, mem, sweeps_out, stats, 0.0, true);
+}
+
 PG_API int pg_dc(pg_grid *g, double t, double tol, double omega, int method, int64_t max_sweeps,
                  pg_stats *stats) {
   REQUIRE(g != nullptr, "grid is NULL");
   REQUIRE(!g->slab, "slab grids are driven through a pg_group");
   REQUIRE(std::isfinite(t), "t must be finite");
   pg_grid *gs[1] = {g};
-  return pgb::run_transient(gs, 1, nullptr, INFINITY, 1, tol, omega, method, max_sweeps, 0, nullptr,
-                            nullptr, PG_MEM_HOST, nullptr, stats, t);
+  const int rc = pgb::run_transient(gs, 1, nullptr, INFINITY, 1, tol, omega, method, max_sweeps, 0, nullptr,
+                                    nullptr, PG_MEM_HOST, nullptr, stats, t);
+  // the DC point is the state a following pg_transient_continue starts from (t = 0)
+  g->traj_steps = 0;
+  g->traj_h = 0.0;
+  return rc;
 }
 
 PG_API int pg_estimate_omega(pg_grid *g, double h, int64_t sweeps, double *rho, double *omega_opt) {
@@ -749,7 +819,7 @@ int batch_graph(pg_grid *g, int method, double omega, double tol, int F) {
 int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, double tol,
                   double omega, int method, int64_t max_sweeps, int64_t n_probe,
                   const int64_t *probe_node, double *probe_out, int mem, int64_t *sweeps_out,
-                  pg_stats *stats, double t_dc) {
+                  pg_stats *stats, double t_dc, bool cont) {
   pg_grid *g = gs[0];
   const bool dc = std::isinf(h);  // DC analysis (pg_dc): one solve of G v = b(t_dc)
   REQUIRE(h > 0.0 && (std::isfinite(h) || dc), "h must be finite and > 0");
@@ -765,7 +835,11 @@ int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, d
     REQUIRE(gs[k] != nullptr, "grid is NULL");
     REQUIRE(!gs[k]->slab || method == PG_METHOD_RBSOR, "slab grids support the red-black sweep only");
     REQUIRE(gs[k]->stream == g->stream, "grids of a group must share one stream");
+    REQUIRE(!cont || gs[k]->traj_steps == 0 || gs[k]->traj_h == h,
+            "pg_transient_continue: h differs from the h of the steps taken so far");
   }
+  // first step index of this call: steps s0 + 1 .. s0 + steps at t = s h
+  const int64_t s0 = cont ? g->traj_steps : 0;
 
   int rc;
   // ---- probes
@@ -845,11 +919,13 @@ int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, d
   CK(cudaEventRecord(ev0, st));
   for (int k = 0; k < ng; ++k) {
     pg_grid *q = gs[k];
-    CK(cudaMemcpyAsync(q->V[0], q->x0, sizeof(double) * q->np, cudaMemcpyDeviceToDevice, st));
+    // a new transient starts from x(0) with zero inductor currents; a
+    // continuation keeps V (ping-pong parity included) and the currents
+    if (!cont) CK(cudaMemcpyAsync(q->V[0], q->x0, sizeof(double) * q->np, cudaMemcpyDeviceToDevice, st));
     CK(cudaMemsetAsync(q->dev_sweeps, 0, sizeof(int64_t) * (steps + 1), st));
-    if (q->iz) CK(cudaMemsetAsync(q->iz, 0, sizeof(double) * q->np, st));
-    if (q->pad_i) CK(cudaMemsetAsync(q->pad_i, 0, sizeof(double) * q->npad, st));
-    CK(launch_reset_state(q));
+    if (!cont && q->iz) CK(cudaMemsetAsync(q->iz, 0, sizeof(double) * q->np, st));
+    if (!cont && q->pad_i) CK(cudaMemsetAsync(q->pad_i, 0, sizeof(double) * q->npad, st));
+    CK(launch_reset_state(q, cont));
     CK(launch_setup(q, h));
     launches += 4;
   }
@@ -870,8 +946,8 @@ int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, d
   };
   for (int64_t s = 1; s <= steps; ++s) {
     for (int k = 0; k < ng; ++k) {
-      CK(launch_rhs(gs[k], h, dc ? t_dc : (double)s * h));
-      launches += 1 + (gs[k]->npad > 0) + (gs[k]->nsrc > 0);
+      CK(launch_rhs(gs[k], h, dc ? t_dc : (double)(s0 + s) * h));
+      ++launches;
     }
     // option "timing": an event pair around the step's sweep launches (read
     // after the run, so timing adds no synchronisation and keeps the graphs)
@@ -942,6 +1018,10 @@ int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, d
       ++launches;
     }
   }
+  for (int k = 0; k < ng; ++k) {
+    CK(launch_check_finite(gs[k]));
+    ++launches;
+  }
   CK(cudaEventRecord(ev1, st));
   for (int k = 1; k < ng; ++k)
     CK(cudaMemcpyAsync(gs[k]->ctl_host, gs[k]->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, st));
@@ -983,9 +1063,19 @@ int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, d
     stats->sweeps_per_launch = F;
   }
   for (int k = 0; k < ng; ++k) {
+    gs[k]->traj_steps = dc ? 0 : s0 + steps;
+    gs[k]->traj_h = dc ? 0.0 : h;
+  }
+  for (int k = 0; k < ng; ++k) {
     if (gs[k]->ctl_host->diag_bad) {
       set_error("a node has a non-positive diagonal d_i (no capacitance and no conductive path; Lemma 1)");
       return PG_EINVAL;
+    }
+  }
+  for (int k = 0; k < ng; ++k) {
+    if (gs[k]->ctl_host->nonfinite) {
+      set_error("an iterate became non-finite (NaN or Inf); results are invalid");
+      return PG_ENONFINITE;
     }
   }
   if (c.failed) {

@@ -681,8 +681,8 @@ PG_API int pg_group_p2p_connect(pg_group *grp, const void *blobs, int64_t blob_l
   return attach_halo(grp);
 }
 
-PG_API int pg_group_transient(pg_group *grp, double h, int64_t steps, double tol, double omega,
-                              int64_t max_sweeps, int64_t *sweeps_out, pg_stats *stats) {
+static int group_transient(pg_group *grp, double h, int64_t steps, double tol, double omega,
+                           int64_t max_sweeps, int64_t *sweeps_out, pg_stats *stats, bool cont) {
   REQ(grp != nullptr, "group is NULL");
   for (pg_grid *g : grp->slabs)
     REQ(2 * sweeps_per_launch(g, PG_METHOD_RBSOR) <= grp->G,
@@ -705,7 +705,8 @@ PG_API int pg_group_transient(pg_group *grp, double h, int64_t steps, double tol
   for (pg_grid *g : grp->slabs) g->group_active = true;
   drop_graphs();
   const int rc = run_transient(grp->slabs.data(), (int)grp->slabs.size(), grp, h, steps, tol, omega,
-                               PG_METHOD_RBSOR, max_sweeps, 0, nullptr, nullptr, PG_MEM_HOST, sweeps_out, stats);
+                               PG_METHOD_RBSOR, max_sweeps, 0, nullptr, nullptr, PG_MEM_HOST, sweeps_out, stats,
+                               0.0, cont);
   for (pg_grid *g : grp->slabs) g->group_active = false;
   drop_graphs();
   if (grp->p2p())
@@ -715,6 +716,16 @@ PG_API int pg_group_transient(pg_group *grp, double h, int64_t steps, double tol
         return PG_ECUDA;
       }
   return rc;
+}
+
+PG_API int pg_group_transient(pg_group *grp, double h, int64_t steps, double tol, double omega,
+                              int64_t max_sweeps, int64_t *sweeps_out, pg_stats *stats) {
+  return group_transient(grp, h, steps, tol, omega, max_sweeps, sweeps_out, stats, false);
+}
+
+PG_API int pg_group_transient_continue(pg_group *grp, double h, int64_t steps, double tol, double omega,
+                                       int64_t max_sweeps, int64_t *sweeps_out, pg_stats *stats) {
+  return group_transient(grp, h, steps, tol, omega, max_sweeps, sweeps_out, stats, true);
 }
 
 PG_API void pg_group_destroy(pg_group *grp) {

@@ -39,9 +39,11 @@ struct DevCtl {
   unsigned long long sig;
   unsigned long long pnorm[4];
   int32_t p2p_timeout;     // a peer wait gave up (watchdog), results invalid
+  int32_t nonfinite;       // an iterate held NaN / Inf (checked by the RHS kernel and at the end of a call)
 };
 
 constexpr int kRing = 4;
+constexpr int kRhsTile = 2048;  // storage elements per tile of the fused RHS kernel
 constexpr int kMaxLayers = 8;   // CTA of the mesh sweep = 32 lanes x L warps
 
 // Mesh storage layout ("parity-split rows"), DESIGN.md §7.  Layer-major
@@ -100,8 +102,9 @@ struct pg_grid {
   double vdd = 1.0;
   bool rlc = false;
   cudaStream_t stream = nullptr;
-  int dev = 0;
+  int dev = -1;               // set by creation (common_init)
   int num_sms = 148;
+  bool counted = false;      // counted in the per-device live-grid count (pool trimming)
 
   // ---- mesh store (padded natural layout, SoA)
   pgb::MeshDims md{};
@@ -133,6 +136,15 @@ struct pg_grid {
   int64_t nsrc = 0, nsrc_grp = 0, npts = 0;
   int64_t *src_idx = nullptr, *src_grp = nullptr, *src_ptr = nullptr;
   double *pwl_t = nullptr, *pwl_i = nullptr;
+  // first pad / source group of every RHS tile of kRhsTile storage elements
+  // (ntile + 1 entries each; the fused RHS kernel's per-tile ranges)
+  int64_t ntile = 0;
+  int64_t *pad_tile = nullptr, *src_tile = nullptr;
+
+  // ---- trajectory: time steps of length traj_h completed since x(0) (the
+  // state pg_transient_continue resumes from); 0 after create / set_voltages / dc
+  int64_t traj_steps = 0;
+  double traj_h = 0.0;
 
   // ---- control
   pgb::DevCtl *ctl = nullptr;
@@ -191,7 +203,8 @@ cudaError_t launch_step_end(pg_grid *g, int64_t s, int launched, int flips, int 
                             int64_t max_sweeps, double tol);
 cudaError_t launch_inductor_update(pg_grid *g, double h);
 cudaError_t launch_probe(pg_grid *g, const int64_t *probe_idx, int64_t n_probe, double *out);
-cudaError_t launch_reset_state(pg_grid *g);
+cudaError_t launch_reset_state(pg_grid *g, bool keep_base = false);
+cudaError_t launch_check_finite(pg_grid *g);
 cudaError_t launch_gather_user(pg_grid *g, double *dst_user_order);
 cudaError_t launch_scatter_user(pg_grid *g, const double *src_user_order, double *dst_storage);
 int sweeps_per_launch(pg_grid *g, int method);
@@ -231,7 +244,9 @@ struct Exchange {
 int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, double tol,
                   double omega, int method, int64_t max_sweeps, int64_t n_probe,
                   const int64_t *probe_node, double *probe_out, int mem, int64_t *sweeps_out,
-                  pg_stats *stats, double t_dc = 0.0);
+                  pg_stats *stats, double t_dc = 0.0, bool cont = false);
+// first group of every RHS tile: tiles[t] = first q with node_of_group[q] >= t * kRhsTile
+std::vector<int64_t> rhs_tile_starts(const std::vector<int64_t> &group_node, int64_t np);
 // upload / download helpers (pg_api.cu)
 int dalloc_bytes(void **p, size_t bytes);
 

@@ -1,8 +1,8 @@
 // Device kernels of the B200 power-grid transient solver (sm_100a).
 //
 // Hot path per backward-Euler step (Algorithm 1):
-//   k_rhs_*            fused RHS: C_i/h x_i(t) + pad G0 Vdd (+ companion history)
-//                      - PWL loads I_i(t+h)                       (Eq. (2) / (12))
+//   k_rhs_fused        fused RHS: C_i/h x_i(t) + pad G0 Vdd (+ companion history)
+//                      - PWL loads I_i(t+h), one launch per step   (Eq. (2) / (12))
 //   (pg_sweep_fused.cu) k_rb_sweep_fused: F red-black SOR sweeps per streaming
 //                      pass (Eq. (13) in red-black numbering + Eq. (15)), fused
 //                      warp-shuffle max|dV| reduction                  (line 7-8)
@@ -14,6 +14,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cooperative_groups.h>
 
 #include "pg_internal.h"
@@ -229,47 +230,6 @@ __global__ void __launch_bounds__(256) k_csr_jacobi(CsrArgs a) {
 }
 
 // ------------------------------------------------------------------ RHS (fused)
-// b_i = (C_i/h) x_i(t) - [RLC] sum_vias alpha i(t)   (+ pads / loads below)
-__global__ void k_rhs_dense(int64_t np, const double *__restrict__ cap, double inv_h,
-                            double *V0, double *V1, DevCtl *ctl, double *__restrict__ b,
-                            const double *__restrict__ lz, const double *__restrict__ gze,
-                            const double *__restrict__ iz, int64_t layer_stride, int32_t L) {
-  const double *V = ctl->base ? V1 : V0;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    ctl->done = 0;
-    ctl->launches_done = 0;
-    ctl->dmax[0] = 0ull;
-    ctl->jbase = 0;
-  }
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < np;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    double bb = cap[i] * inv_h * V[i];
-    if (lz != nullptr) {
-      const int64_t l = i / layer_stride;
-      if (l + 1 < L) bb -= lz[i] * inv_h * gze[i] * iz[i];           // current leaving down->up
-      if (l > 0) {
-        const int64_t j = i - layer_stride;
-        bb += lz[j] * inv_h * gze[j] * iz[j];                          // current arriving from below
-      }
-    }
-    b[i] = bb;
-  }
-}
-
-__global__ void k_rhs_pads(int64_t ngrp, const int64_t *__restrict__ grp, const int64_t *__restrict__ idx,
-                           const double *__restrict__ ge, const double *__restrict__ pl,
-                           const double *__restrict__ pi, double vdd, double inv_h, double *b) {
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < ngrp;
-       q += (int64_t)gridDim.x * blockDim.x) {
-    double bb = 0.0;
-    for (int64_t k = grp[q]; k < grp[q + 1]; ++k) {
-      bb += ge[k] * vdd;
-      if (pl != nullptr) bb -= pl[k] * inv_h * ge[k] * pi[k];
-    }
-    b[idx[grp[q]]] += bb;
-  }
-}
-
 __device__ __forceinline__ double pwl_eval(const double *t, const double *v, int64_t s, int64_t e,
                                            double tt) {
   if (tt <= t[s]) return v[s];
@@ -283,15 +243,104 @@ __device__ __forceinline__ double pwl_eval(const double *t, const double *v, int
   return v[e - 1];
 }
 
-__global__ void k_rhs_src(int64_t ngrp, const int64_t *__restrict__ grp, const int64_t *__restrict__ idx,
-                          const int64_t *__restrict__ ptr, const double *__restrict__ pt,
-                          const double *__restrict__ pv, double tt, double *b) {
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < ngrp;
-       q += (int64_t)gridDim.x * blockDim.x) {
-    double bb = 0.0;
-    for (int64_t k = grp[q]; k < grp[q + 1]; ++k) bb += pwl_eval(pt, pv, ptr[k], ptr[k + 1], tt);
-    b[idx[grp[q]]] -= bb;
+// One kernel per time step builds the whole right-hand side of Eq. (12) at
+// t + h (Eq. (2): b = (C/h) x(t) + G0 Vdd - i(t+h); Eq. (10): the
+// companion history of every inductor):
+//   b_i = (C_i/h) V_i(t)
+//         - [RLC vias] alpha i_z(t) of the via above + alpha i_z(t) of the via below
+//         + sum over the node's pads (g_e Vdd - [series L] alpha i_pad(t))
+//         - sum over the node's loads I_k(t + h)            (PWL, reading R8)
+// Storage elements are processed in tiles of kRhsTile: the dense term goes to
+// a shared-memory tile, then the tile's pad groups and load groups (sorted by
+// storage index, one group per node, ranges precomputed per tile on the host)
+// add into it -- each node's terms in a fixed order, no atomics, so the sum is
+// deterministic -- and the tile is written once.  V(t) is also checked for
+// NaN / Inf here (ctl->nonfinite).
+struct RhsArgs {
+  int64_t np;
+  const double *cap;
+  double inv_h;
+  const double *V0, *V1;
+  DevCtl *ctl;
+  double *b;
+  const double *lz, *gze, *iz;   // RLC vias (lz == nullptr: RC)
+  int64_t layer_stride;
+  int32_t L;
+  const int64_t *pad_tile, *pad_grp, *pad_idx;
+  const double *pad_ge, *pad_l, *pad_i;
+  double vdd;
+  const int64_t *src_tile, *src_grp, *src_idx, *src_ptr;
+  const double *pwl_t, *pwl_i;
+  double t;
+  int64_t ntile;
+};
+
+__global__ void __launch_bounds__(256) k_rhs_fused(RhsArgs a) {
+  __shared__ double bt[kRhsTile];
+  const double *V = a.ctl->base ? a.V1 : a.V0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    a.ctl->done = 0;
+    a.ctl->launches_done = 0;
+    a.ctl->dmax[0] = 0ull;
+    a.ctl->jbase = 0;
   }
+  bool bad = false;
+  for (int64_t tile = blockIdx.x; tile < a.ntile; tile += gridDim.x) {
+    const int64_t i0 = tile * kRhsTile;
+    const int n = (int)min((int64_t)kRhsTile, a.np - i0);
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+      const int64_t i = i0 + k;
+      const double v = V[i];
+      bad |= !(fabs(v) <= 1.7976931348623157e308);
+      double bb = a.cap[i] * a.inv_h * v;
+      if (a.lz != nullptr) {
+        const int64_t l = i / a.layer_stride;
+        if (l + 1 < a.L) bb -= a.lz[i] * a.inv_h * a.gze[i] * a.iz[i];    // current leaving down->up
+        if (l > 0) {
+          const int64_t j = i - a.layer_stride;
+          bb += a.lz[j] * a.inv_h * a.gze[j] * a.iz[j];                    // current arriving from below
+        }
+      }
+      bt[k] = bb;
+    }
+    __syncthreads();
+    if (a.pad_tile != nullptr) {
+      const int64_t q1 = a.pad_tile[tile + 1];
+      for (int64_t q = a.pad_tile[tile] + threadIdx.x; q < q1; q += blockDim.x) {
+        double bb = 0.0;
+        for (int64_t k = a.pad_grp[q]; k < a.pad_grp[q + 1]; ++k) {
+          bb += a.pad_ge[k] * a.vdd;
+          if (a.pad_l != nullptr) bb -= a.pad_l[k] * a.inv_h * a.pad_ge[k] * a.pad_i[k];
+        }
+        bt[a.pad_idx[a.pad_grp[q]] - i0] += bb;
+      }
+      __syncthreads();
+    }
+    if (a.src_tile != nullptr) {
+      const int64_t q1 = a.src_tile[tile + 1];
+      for (int64_t q = a.src_tile[tile] + threadIdx.x; q < q1; q += blockDim.x) {
+        double bb = 0.0;
+        for (int64_t k = a.src_grp[q]; k < a.src_grp[q + 1]; ++k)
+          bb += pwl_eval(a.pwl_t, a.pwl_i, a.src_ptr[k], a.src_ptr[k + 1], a.t);
+        bt[a.src_idx[a.src_grp[q]] - i0] -= bb;
+      }
+      __syncthreads();
+    }
+    for (int k = threadIdx.x; k < n; k += blockDim.x) a.b[i0 + k] = bt[k];
+    __syncthreads();
+  }
+  if (bad) a.ctl->nonfinite = 1;
+}
+
+// one pass over the current iterate: flags NaN / Inf (end of a transient call;
+// the RHS kernel checks V(t) of every other step)
+__global__ void k_check_finite(int64_t np, const double *V0, const double *V1, DevCtl *ctl) {
+  const double *V = ctl->base ? V1 : V0;
+  bool bad = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < np;
+       i += (int64_t)gridDim.x * blockDim.x)
+    bad |= !(fabs(V[i]) <= 1.7976931348623157e308);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) ctl->nonfinite = 1;
 }
 
 // -------------------------------------------------------------- per-h setup
@@ -612,13 +661,17 @@ cudaError_t launch_rb_resident(pg_grid *g, double omega, double tol, int64_t max
   a.R = p.R;
   a.HPx = (g->md.NX + 1) / 2;
   const size_t smem = sizeof(double) * (size_t)p.R * g->md.L * g->md.NX;
-  static bool attr = false;
-  if (!attr) {
+  // function attributes apply to the device current when they are set: set
+  // once per device (the flags are atomics, so concurrent grids on other
+  // threads at worst set them twice)
+  static std::atomic<bool> attr_set[64];
+  if (g->dev < 0 || g->dev >= 64) return cudaErrorInvalidDevice;
+  if (!attr_set[g->dev].load(std::memory_order_acquire)) {
     cudaError_t e = cudaFuncSetAttribute(k_rb_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(k_rb_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr_set[g->dev].store(true, std::memory_order_release);
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.ncta);
@@ -683,8 +736,9 @@ __global__ void k_scatter_perm(const int64_t *iperm, const double *src, int64_t 
     dst[iperm[k]] = src[k];
 }
 
-__global__ void k_reset_state(DevCtl *c) {
-  c->base = 0;
+__global__ void k_reset_state(DevCtl *c, int32_t keep_base) {
+  if (!keep_base) c->base = 0;
+  c->nonfinite = 0;
   c->done = 0;
   c->failed = 0;
   c->sweeps_total = 0;
@@ -788,19 +842,55 @@ cudaError_t launch_setup(pg_grid *g, double h) {
 // right-hand side of the step ending at time t (loads evaluated at t); h may
 // be +inf (DC analysis: capacitors open, inductor history dropped)
 cudaError_t launch_rhs(pg_grid *g, double h, double t) {
-  const double inv_h = 1.0 / h;
-  const int B = 256;
+  RhsArgs a;
+  a.np = g->np;
+  a.cap = g->cap;
+  a.inv_h = 1.0 / h;
+  a.V0 = g->V[0];
+  a.V1 = g->V[1];
+  a.ctl = g->ctl;
+  a.b = g->b;
   const bool rlc_vias = g->kind == 0 && g->lz != nullptr;
-  k_rhs_dense<<<grid_for(g->np, B, g->num_sms), B, 0, g->stream>>>(
-      g->np, g->cap, inv_h, g->V[0], g->V[1], g->ctl, g->b, rlc_vias ? g->lz : nullptr, g->gze,
-      g->iz, g->kind == 0 ? g->md.layer_stride : 1, g->kind == 0 ? g->md.L : 1);
-  if (g->npad > 0)
-    k_rhs_pads<<<grid_for(g->npad_grp, B, g->num_sms), B, 0, g->stream>>>(
-        g->npad_grp, g->pad_grp, g->pad_idx, g->pad_ge, g->pad_l, g->pad_i, g->vdd, inv_h, g->b);
-  if (g->nsrc > 0)
-    k_rhs_src<<<grid_for(g->nsrc_grp, B, g->num_sms), B, 0, g->stream>>>(
-        g->nsrc_grp, g->src_grp, g->src_idx, g->src_ptr, g->pwl_t, g->pwl_i, t, g->b);
+  a.lz = rlc_vias ? g->lz : nullptr;
+  a.gze = g->gze;
+  a.iz = g->iz;
+  a.layer_stride = g->kind == 0 ? g->md.layer_stride : 1;
+  a.L = g->kind == 0 ? g->md.L : 1;
+  a.pad_tile = g->npad > 0 ? g->pad_tile : nullptr;
+  a.pad_grp = g->pad_grp;
+  a.pad_idx = g->pad_idx;
+  a.pad_ge = g->pad_ge;
+  a.pad_l = g->pad_l;
+  a.pad_i = g->pad_i;
+  a.vdd = g->vdd;
+  a.src_tile = g->nsrc > 0 ? g->src_tile : nullptr;
+  a.src_grp = g->src_grp;
+  a.src_idx = g->src_idx;
+  a.src_ptr = g->src_ptr;
+  a.pwl_t = g->pwl_t;
+  a.pwl_i = g->pwl_i;
+  a.t = t;
+  a.ntile = g->ntile;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(g->ntile, (int64_t)g->num_sms * 8));
+  k_rhs_fused<<<grid, 256, 0, g->stream>>>(a);
   return cudaGetLastError();
+}
+
+cudaError_t launch_check_finite(pg_grid *g) {
+  k_check_finite<<<grid_for(g->np, 256, g->num_sms), 256, 0, g->stream>>>(g->np, g->V[0], g->V[1], g->ctl);
+  return cudaGetLastError();
+}
+
+std::vector<int64_t> rhs_tile_starts(const std::vector<int64_t> &group_node, int64_t np) {
+  const int64_t ntile = (np + kRhsTile - 1) / kRhsTile;
+  std::vector<int64_t> t((size_t)ntile + 1);
+  size_t q = 0;
+  for (int64_t k = 0; k <= ntile; ++k) {
+    const int64_t lo = k * (int64_t)kRhsTile;
+    while (q < group_node.size() && group_node[q] < lo) ++q;
+    t[(size_t)k] = (int64_t)q;
+  }
+  return t;
 }
 
 cudaError_t launch_sweep(pg_grid *g, int method, double omega, double tol, int j, int nsweeps,
@@ -890,8 +980,8 @@ cudaError_t launch_probe(pg_grid *g, const int64_t *probe_idx, int64_t n_probe, 
   return cudaGetLastError();
 }
 
-cudaError_t launch_reset_state(pg_grid *g) {
-  k_reset_state<<<1, 1, 0, g->stream>>>(g->ctl);
+cudaError_t launch_reset_state(pg_grid *g, bool keep_base) {
+  k_reset_state<<<1, 1, 0, g->stream>>>(g->ctl, keep_base ? 1 : 0);
   return cudaGetLastError();
 }
 

@@ -213,11 +213,14 @@ class SlabGroup:
 
     # -------------------------------------------------------------- transient
     def transient(self, h, steps, tol=1e-10, omega=1.0, max_sweeps=100000,
-                  raise_on_noconv=True) -> GroupResult:
+                  raise_on_noconv=True, cont=False) -> GroupResult:
+        """pg_group_transient (from x(0)) or, with cont=True,
+        pg_group_transient_continue (from the slabs' current state)."""
         sweeps = np.zeros(steps + 1, dtype=np.int64)
         st = L.PgStats()
-        code = self._lib.pg_group_transient(self._h, float(h), int(steps), float(tol), float(omega),
-                                            int(max_sweeps), sweeps.ctypes.data, ctypes.byref(st))
+        fn = self._lib.pg_group_transient_continue if cont else self._lib.pg_group_transient
+        code = fn(self._h, float(h), int(steps), float(tol), float(omega),
+                  int(max_sweeps), sweeps.ctypes.data, ctypes.byref(st))
         if code not in (L.PG_OK, L.PG_ENOCONV) or (code == L.PG_ENOCONV and raise_on_noconv):
             L.check(code)
         return GroupResult(sweeps=sweeps, stats=st, status=code)

@@ -62,3 +62,35 @@ def test_last_error_without_gpu(libpath):
     assert rc == _lib.PG_EINVAL
     assert b"layers" in lib.pg_last_error()
     assert out.value is None
+
+
+def test_binding_refuses_mismatched_buffer_sizes(libpath):
+    # the C side reads / writes exactly the sizes the grid implies: the binding
+    # checks every buffer length before the call (no device needed: it raises
+    # before reaching the library)
+    import numpy as np
+    import paper_1409_7166_b200 as P
+    n = 2 * 3 * 4
+    ok = np.zeros(n)
+    with pytest.raises(ValueError):
+        P.Grid.mesh(2, 3, 4, ok, ok, np.zeros(n - 1), ok, np.array([0]), np.array([1.0]))
+    with pytest.raises(ValueError):
+        P.Grid.mesh(2, 3, 4, ok, ok, ok, ok, np.array([0, 1]), np.array([1.0]))
+    with pytest.raises(ValueError):
+        P.Grid.mesh(2, 3, 4, ok, ok, ok, ok, np.array([0]), np.array([1.0]), lz=np.zeros(3))
+    with pytest.raises(ValueError):
+        P.Grid.csr(5, np.array([0, 1]), np.array([1]), np.array([1.0, 1.0]), np.zeros(5), np.array([0]),
+                   np.array([1.0]))
+    g = P.Grid.__new__(P.Grid)           # a handle-less grid: only the size checks run
+    g._lib = P.load()
+    g.info = lambda: dict(n=n)
+    with pytest.raises(ValueError):
+        g.voltages(np.empty(n - 1))
+    with pytest.raises(ValueError):
+        g.set_voltages(np.ones(n + 1))
+    with pytest.raises(ValueError):
+        g.set_sources(np.array([1, 2]), np.array([0, 3]), np.zeros(3), np.zeros(3))
+    with pytest.raises(ValueError):
+        g.set_sources(np.array([1]), np.array([0, 3]), np.zeros(2), np.zeros(3))
+    with pytest.raises(ValueError):
+        g.transient(1e-12, 3, probes=np.array([0, 1]), probe_out=np.empty((3, 2)))

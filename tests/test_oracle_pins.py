@@ -454,3 +454,66 @@ def test_edge_grid_spanning_and_deletion():
     V, _ = dense.direct_companion(nl, g.h, steps, It, _v0(nl))
     r = nodal.NodalOracle(nl).transient(g.h, steps, tol=1e-13, omega=1.6, Itab=It)
     np.testing.assert_allclose(r.V, V, atol=1e-9)
+
+
+# ------------------------------------------------ round 2: oracle plumbing pins
+def test_group_counting_sort_equals_stable_argsort():
+    # oracle_group (plain-C counting sort used for full-size node lists) equals
+    # the stable-argsort grouping on random branch lists with ground / source ends
+    rng = np.random.default_rng(5)
+    for n, m in [(1, 0), (1, 3), (5, 7), (60, 400), (300, 50)]:
+        a = rng.integers(-4, n, m)
+        b = rng.integers(-4, n, m)
+        v = rng.random(m)
+        want = netlist._group_numpy(n, a, b, v)
+        got = netlist.group(n, a, b, v)
+        for x, y in zip(want, got):
+            np.testing.assert_array_equal(x, y)
+
+
+@pytest.mark.parametrize("cfg,series_rl", [(1, "node"), (3, "element"), (3, "node"), (2, "node")])
+def test_transient_cut_at_step_boundaries_is_identical(cfg, series_rl):
+    # Algorithm 1's time loop carries only V and the inductor currents: the
+    # step-by-step chaining tools/make_golden_fullsize.py uses (V(s-1), i_L(s-1)
+    # and the load rows I((s-1)h), I(sh) passed in) reproduces one call bit for bit
+    g = gridgen.config_grid(cfg, dims=(2, 12, 14), steps=6)
+    nl = netlist.from_grid(g, series_rl)
+    o = nodal.NodalOracle(nl)
+    order = nodal.red_black_order(g.layers, g.ny, g.nx) if nl.n == g.n else None
+    It = pwl.node_currents_table(nl, g.h, 6)
+    r = o.transient(g.h, 6, tol=1e-11, omega=1.6, order=order, Itab=It, trace=True)
+    V, il = np.full(nl.n, 1.0), np.zeros(nl.la.size)
+    for s in range(1, 7):
+        It2 = np.stack([pwl.node_currents_at(nl, (s - 1) * g.h), pwl.node_currents_at(nl, s * g.h)])
+        q = o.transient(g.h, 1, tol=1e-11, omega=1.6, order=order, Itab=It2, V0=V, il0=il, trace=True)
+        V, il = q.V[1].copy(), q.il.copy()
+        assert np.array_equal(V, r.V[s]) and q.sweeps[1] == r.sweeps[s]
+        np.testing.assert_array_equal(q.dtrace[1], r.dtrace[s])
+    np.testing.assert_array_equal(il, r.il)
+    np.testing.assert_array_equal(It[3], pwl.node_currents(nl, 3 * g.h))
+
+
+def test_stopping_record():
+    # dtrace: the last sweep is the first below tol (Algorithm 1 line 8), the
+    # sweep before it is not, and the continued sweeps are the sweeps the
+    # oracle would have run next (checked by re-running with more sweeps)
+    g = gridgen.config_grid(1, dims=(2, 10, 12), steps=3)
+    nl = netlist.from_grid(g)
+    o = nodal.NodalOracle(nl)
+    It = pwl.node_currents_table(nl, g.h, 3)
+    tol = 1e-9
+    r = o.transient(g.h, 3, tol=tol, omega=1.5, Itab=It, trace=True)
+    for s in range(1, 4):
+        k = r.sweeps[s]
+        assert r.dtrace[s, 1] < tol and (k == 1 or r.dtrace[s, 0] >= tol)
+    # step 1 continued: fixed k + e sweeps reproduce the recorded norms
+    k = int(r.sweeps[1])
+    d = o.diag(g.h)
+    kn = o.known_companion(g.h, np.full(nl.n, 1.0), It[1])
+    V = np.full(nl.n, 1.0)
+    norms = []
+    for _ in range(k + 4):
+        V, dm = o.sweep(g.h, d, kn, V, omega=1.5)
+        norms.append(dm)
+    np.testing.assert_array_equal(np.array(norms[k - 2:k + 4]) if k >= 2 else norms[k - 1:k + 4],
+                                  r.dtrace[1] if k >= 2 else r.dtrace[1, 1:])

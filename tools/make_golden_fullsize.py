@@ -1,0 +1,146 @@
+"""Write the full-size converged-waveform goldens (tests/golden/fullsize_*.npz)
+from the ORACLE ONLY (gridgen + oracle/; nothing from the CUDA path).
+
+    python tools/make_golden_fullsize.py JOB [--resume]
+
+JOB is one of the entries of JOBS below.  The oracle (plain-C nodal SOR,
+PAPER.md §IV Eq. (13)/(15), Algorithm 1) runs the BASELINE.json config at full
+size for `steps` backward-Euler steps from x(0) = Vdd, converged to `tol`
+(Algorithm 1 line 8, infinity norm), one step per oracle call: V(s-1), the
+inductor currents and the load table rows I((s-1)h), I(sh) are passed in, which
+is exactly the oracle's own time loop (nodal.c oracle_transient) cut at step
+boundaries -- so the run can be checkpointed (/tmp) and resumed.
+
+Stored per step: V at the sampled nodes (65 536 seeded random nodes plus the
+all-layer 3 x 3 columns around the 32 earliest-starting loads), the sweep
+count, and the stopping record (dtrace: the norm of the last two sweeps and
+of 4 more sweeps continued on a copy, for the every-F-sweeps stopping test of
+the GPU, R13).  omega is the bench's omega for that config (Young's
+estimate, R15, a literal here); tests read it from the golden.
+"""
+from __future__ import annotations
+
+import argparse
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import gridgen  # noqa: E402
+from oracle import netlist, nodal, pwl  # noqa: E402
+
+# Young's omega of each config as bench.py uses it (pg_estimate_omega with 8000
+# Jacobi sweeps on the config's grid; R15, profiles/r2_probe_omega.log)
+OMEGA = {
+    1: 1.9639132252348532,
+    2: 1.9603462069765296,
+    3: 1.9511469274691926,
+    4: 1.9724621984718245,
+}
+
+JOBS = {
+    # name: (config, steps, tol, series_rl, order)
+    "c1": (1, 20, 1e-10, "node", "redblack"),
+    "c2": (2, 6, 1e-10, "node", "redblack"),
+    "c3_element": (3, 20, 1e-10, "element", "redblack"),
+    "c3_node_tight": (3, 20, 1e-13, "node", "natural"),
+    "c4": (4, 3, 1e-10, "node", "redblack"),
+}
+
+
+def sample_nodes(g, cfg):
+    L, NY, NX = g.layers, g.ny, g.nx
+    n = L * NY * NX
+    rng = np.random.default_rng(1000 + cfg)
+    rnd = rng.choice(n, size=65536, replace=False)
+    s = g.sources
+    first = np.argsort(s.t[s.ptr[:-1]], kind="stable")[:32]
+    cols = []
+    for q in first:
+        nd = int(s.node[q])
+        r = nd % (NY * NX)
+        y, x = divmod(r, NX)
+        for l in range(L):
+            for dy in (-1, 0, 1):
+                for dx in (-1, 0, 1):
+                    yy, xx = y + dy, x + dx
+                    if 0 <= yy < NY and 0 <= xx < NX:
+                        cols.append((l * NY + yy) * NX + xx)
+    return np.unique(np.concatenate([rnd, np.array(cols, dtype=np.int64)])).astype(np.int64)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("job", choices=sorted(JOBS))
+    ap.add_argument("--resume", action="store_true")
+    ap.add_argument("--scratch", default="/tmp/pg_golden")
+    a = ap.parse_args()
+    cfg, steps, tol, series_rl, order_name = JOBS[a.job]
+    omega = OMEGA[cfg]
+    os.makedirs(a.scratch, exist_ok=True)
+    ck = os.path.join(a.scratch, f"{a.job}.ckpt.npz")
+    out = os.path.join(ROOT, "tests", "golden", f"fullsize_{a.job}.npz")
+
+    t0 = time.time()
+    g = gridgen.config_grid(cfg)
+    nodes = sample_nodes(g, cfg)
+    h = g.h
+    nl = netlist.from_grid(g, series_rl)
+    o = nodal.NodalOracle(nl)
+    nl.ra = nl.rb = nl.rg = None          # the branch list is no longer needed (memory)
+    order = nodal.red_black_order(g.layers, g.ny, g.nx) if order_name == "redblack" else None
+    if order is not None and nl.n != g.n:
+        raise SystemExit("red-black order covers mesh nodes only")
+    del g
+    print(f"[{a.job}] setup {time.time() - t0:.1f} s, n = {nl.n}, samples = {nodes.size}", flush=True)
+
+    Vs = np.zeros((steps + 1, nodes.size))
+    sweeps = np.zeros(steps + 1, dtype=np.int64)
+    dtrace = np.full((steps + 1, 6), np.nan)
+    wall = np.zeros(steps + 1)
+    V = np.full(nl.n, float(nl.vd[0]))
+    il = np.zeros(nl.la.size)
+    s0 = 1
+    if a.resume and os.path.exists(ck):
+        z = np.load(ck)
+        s0 = int(z["s_done"]) + 1
+        V, il = z["V"].copy(), z["il"].copy()
+        Vs[:s0], sweeps[:s0], dtrace[:s0], wall[:s0] = z["Vs"][:s0], z["sweeps"][:s0], z["dtrace"][:s0], z["wall"][:s0]
+        print(f"[{a.job}] resumed after step {s0 - 1}", flush=True)
+    Vs[0] = V[nodes]
+    I_prev = pwl.node_currents_at(nl, (s0 - 1) * h)
+    for s in range(s0, steps + 1):
+        ts = time.time()
+        I_now = pwl.node_currents_at(nl, s * h)
+        Itab = np.stack([I_prev, I_now])
+        r = o.transient(h, 1, tol=tol, omega=omega, order=order, Itab=Itab, V0=V, il0=il,
+                        max_sweeps=1_000_000, trace=True)
+        if r.status != 0:
+            raise SystemExit(f"step {s} did not converge")
+        V = r.V[1].copy()
+        il = r.il.copy()
+        del r.V
+        Vs[s] = V[nodes]
+        sweeps[s] = r.sweeps[1]
+        dtrace[s] = r.dtrace[1]
+        wall[s] = time.time() - ts
+        I_prev = I_now
+        np.savez(ck + ".tmp.npz", s_done=s, V=V, il=il, Vs=Vs, sweeps=sweeps, dtrace=dtrace, wall=wall)
+        os.replace(ck + ".tmp.npz", ck)
+        print(f"[{a.job}] step {s}: {sweeps[s]} sweeps, last |dV| {dtrace[s, 1]:.3e}, "
+              f"min V {V[:nodes.max() + 1].min():.6f}, {wall[s]:.0f} s", flush=True)
+    np.savez_compressed(
+        out, job=a.job, config=cfg, steps=steps, tol=tol, omega=omega, h=h, series_rl=series_rl,
+        order=order_name, nodes=nodes, V=Vs, sweeps=sweeps, dtrace=dtrace, oracle_seconds=wall,
+        provenance=("tools/make_golden_fullsize.py: gridgen.config_grid(%d) -> oracle.netlist.from_grid("
+                    "series_rl=%r) -> oracle.nodal.NodalOracle.transient (plain-C SOR, %s order), "
+                    "one step per call from x(0) = Vdd" % (cfg, series_rl, order_name)))
+    print(f"[{a.job}] wrote {out} ({time.time() - t0:.0f} s)", flush=True)
+
+
+if __name__ == "__main__":
+    main()
