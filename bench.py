@@ -225,7 +225,9 @@ def ncu_traffic(kernel: str, cfg: int):
         with open(p) as f:
             d = json.load(f)
         e = d.get(f"{kernel}@config{cfg}")
-        return None if not isinstance(e, dict) else e.get("dram_bytes_per_launch")
+        if not isinstance(e, dict):
+            return None
+        return e.get("dram_bytes_per_launch") * e.get("colour_launches_per_sweep", 1)
     except Exception:
         return None
 

@@ -255,13 +255,15 @@ int common_init(pg_grid *g) {
   CK(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, g->dev));
   g->ntile = (g->np + kRhsTile - 1) / kRhsTile;
   int rc;
+  // b and 1/d get 8 elements of slack: the staged CSR sweep bulk-copies
+  // 16-byte-rounded row ranges that may end one element past np
   if ((rc = dalloc(&g->V[0], g->np)) || (rc = dalloc(&g->V[1], g->np)) || (rc = dalloc(&g->x0, g->np)) ||
-      (rc = dalloc(&g->invd, g->np)) || (rc = dalloc(&g->b, g->np)) || (rc = dalloc(&g->ctl, 1, true)))
+      (rc = dalloc(&g->invd, g->np + 8)) || (rc = dalloc(&g->b, g->np + 8)) || (rc = dalloc(&g->ctl, 1, true)))
     return rc;
   CK(cudaMemset(g->V[0], 0, sizeof(double) * g->np));
   CK(cudaMemset(g->V[1], 0, sizeof(double) * g->np));
-  CK(cudaMemset(g->b, 0, sizeof(double) * g->np));
-  CK(cudaMemset(g->invd, 0, sizeof(double) * g->np));
+  CK(cudaMemset(g->b, 0, sizeof(double) * (g->np + 8)));
+  CK(cudaMemset(g->invd, 0, sizeof(double) * (g->np + 8)));
   CK(cudaMemset(g->ctl, 0, sizeof(DevCtl)));
   CK(cudaMallocHost((void **)&g->ctl_host, sizeof(DevCtl)));
   CK(cudaMallocHost((void **)&g->done_host, sizeof(int32_t) * 8));
@@ -441,11 +443,32 @@ PG_API int pg_create_csr(int64_t n, int64_t m, const int64_t *bu, const int64_t 
   if ((rc = common_init(g))) return rc;
   std::vector<double> cp((size_t)n);
   for (int64_t k = 0; k < n; ++k) cp[H.iperm[k]] = c[k];
-  if ((rc = dalloc(&g->rowptr, n + 1)) || (rc = dalloc(&g->col, (int64_t)H.col.size())) ||
-      (rc = dalloc(&g->val, (int64_t)H.val.size())) || (rc = dalloc(&g->perm, n)) ||
+  const int64_t nnz = (int64_t)H.col.size();
+  REQUIRE(nnz < (int64_t)INT32_MAX - 64, "CSR grids are limited to 2^31 - 64 stored entries");
+  // int32 row pointers (4 B per row) and 8 elements of zero slack after
+  // rowptr / col / val: the staged sweep bulk-copies 16-byte-rounded ranges
+  std::vector<int32_t> rp32((size_t)n + 1 + 8, (int32_t)nnz);
+  for (int64_t k = 0; k <= n; ++k) rp32[k] = (int32_t)H.rowptr[k];
+  std::vector<int32_t> col_p(H.col);
+  col_p.resize((size_t)nnz + 8, 0);
+  std::vector<double> val_p(H.val);
+  val_p.resize((size_t)nnz + 8, 0.0);
+  // every kCsrR-row tile of every colour must fit the staged sweep's entry buffer
+  bool fits = true;
+  for (int32_t c = 0; c + 1 < (int32_t)H.color_ptr.size() && fits; ++c)
+    for (int64_t r0 = H.color_ptr[c]; r0 < H.color_ptr[c + 1]; r0 += kCsrR) {
+      const int64_t r1 = std::min<int64_t>(H.color_ptr[c + 1], r0 + kCsrR);
+      if (H.rowptr[r1] - H.rowptr[r0] > kCsrE) {
+        fits = false;
+        break;
+      }
+    }
+  g->csr_staged_ok = fits;
+  if ((rc = dalloc(&g->rowptr, (int64_t)rp32.size())) || (rc = dalloc(&g->col, (int64_t)col_p.size())) ||
+      (rc = dalloc(&g->val, (int64_t)val_p.size())) || (rc = dalloc(&g->perm, n)) ||
       (rc = dalloc(&g->iperm, n)) || (rc = dalloc(&g->cap, n)))
     return rc;
-  if ((rc = upload(g->rowptr, H.rowptr)) || (rc = upload(g->col, H.col)) || (rc = upload(g->val, H.val)) ||
+  if ((rc = upload(g->rowptr, rp32)) || (rc = upload(g->col, col_p)) || (rc = upload(g->val, val_p)) ||
       (rc = upload(g->perm, H.perm)) || (rc = upload(g->iperm, H.iperm)) || (rc = upload(g->cap, cp)))
     return rc;
   if ((rc = set_pads(g, n_pads, pad_node, pad_g, nullptr, mem, &H.iperm))) return rc;
@@ -502,6 +525,8 @@ PG_API int pg_set_option(pg_grid *g, const char *key, int64_t value) {
       set_error("re-encoding the slab halo tensor maps failed");
       return PG_ECUDA;
     }
+  } else if (k == "csr_stage") {
+    g->csr_stage = value != 0;
   } else if (k == "graph") {
     g->use_graph = value != 0;
   } else if (k == "timing") {

@@ -44,6 +44,9 @@ struct DevCtl {
 
 constexpr int kRing = 4;
 constexpr int kRhsTile = 2048;  // storage elements per tile of the fused RHS kernel
+// staged CSR sweep: rows per tile and entry capacity per tile (6 per row)
+constexpr int kCsrR = 512;
+constexpr int kCsrE = 3072;
 constexpr int kMaxLayers = 8;   // CTA of the mesh sweep = 32 lanes x L warps
 
 // Mesh storage layout ("parity-split rows"), DESIGN.md §7.  Layer-major
@@ -116,7 +119,8 @@ struct pg_grid {
   // ---- csr store (colour-permuted)
   int32_t ncolor = 1;
   std::vector<int64_t> color_ptr;                        // host, ncolor+1
-  int64_t *rowptr = nullptr;
+  int32_t *rowptr = nullptr;   // int32: nnz < 2^31 (checked at creation)
+  bool csr_staged_ok = false;   // every tile of every colour fits the staged CSR sweep's buffers
   int32_t *col = nullptr;
   double *val = nullptr;
   int64_t *perm = nullptr;    // storage -> user
@@ -180,6 +184,7 @@ struct pg_grid {
   int l2keep = -1;                     // option "l2keep": arrays kept in L2 across launches (bit mask, -1: auto)
   int l2promo = 256;                   // option "l2promo": TMA L2 promotion bytes (0, 64, 128, 256)
   int pdl = 1;                         // option "pdl": programmatic dependent launch of consecutive sweeps
+  int csr_stage = 1;                   // option "csr_stage": bulk-copy staged CSR sweep (k_csr_sweep_staged)
   bool pdl_ok = false;                 // set by run_transient: single grid, no exchange between launches
   bool group_active = false;           // inside pg_group_transient (peer exchange armed)
   cudaGraphExec_t batch_exec = nullptr;  // captured batch of `batch` full sweep launches

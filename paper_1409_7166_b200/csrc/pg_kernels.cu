@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(256) k_jacobi_mesh(JacobiArgs a) {
 
 // ------------------------------------------------------------------ CSR sweeps
 struct CsrArgs {
-  const int64_t *rowptr;
+  const int32_t *rowptr;
   const int32_t *col;
   const double *val, *b, *invd;
   double *V0, *V1;  // GS: in place on V[base]; Jacobi: V[(base+j)&1] -> the other
@@ -164,11 +164,6 @@ __device__ __forceinline__ int32_t ldi(const int32_t *p, uint64_t pol) {
   asm("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
   return v;
 }
-__device__ __forceinline__ int64_t ldl(const int64_t *p, uint64_t pol) {
-  int64_t v;
-  asm("ld.global.nc.L2::cache_hint.s64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
-  return v;
-}
 
 __global__ void __launch_bounds__(256) k_csr_sweep(CsrArgs a) {
   __shared__ double wmax[8];
@@ -183,8 +178,8 @@ __global__ void __launch_bounds__(256) k_csr_sweep(CsrArgs a) {
   for (int64_t i = a.r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.r1;
        i += (int64_t)gridDim.x * blockDim.x) {
     double s = ldf(a.b + i, pf);
-    const int64_t k1 = ldl(a.rowptr + i + 1, pf);
-    for (int64_t k = ldl(a.rowptr + i, pf); k < k1; ++k) s = fma(ldf(a.val + k, pf), V[ldi(a.col + k, pf)], s);
+    const int32_t k1 = ldi(a.rowptr + i + 1, pf);
+    for (int32_t k = ldi(a.rowptr + i, pf); k < k1; ++k) s = fma(ldf(a.val + k, pf), V[ldi(a.col + k, pf)], s);
     const double vc = V[i];
     const double vn = fma(a.omega, s * ldf(a.invd + i, pf) - vc, vc);
     V[i] = vn;
@@ -212,8 +207,8 @@ __global__ void __launch_bounds__(256) k_csr_jacobi(CsrArgs a) {
   for (int64_t i = a.r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.r1;
        i += (int64_t)gridDim.x * blockDim.x) {
     double s = __ldg(a.b + i);
-    const int64_t k1 = a.rowptr[i + 1];
-    for (int64_t k = a.rowptr[i]; k < k1; ++k) s = fma(__ldg(a.val + k), __ldg(Vin + __ldg(a.col + k)), s);
+    const int32_t k1 = a.rowptr[i + 1];
+    for (int32_t k = a.rowptr[i]; k < k1; ++k) s = fma(__ldg(a.val + k), __ldg(Vin + __ldg(a.col + k)), s);
     const double vc = __ldg(Vin + i);
     const double vn = fma(a.omega, s * __ldg(a.invd + i) - vc, vc);
     Vout[i] = vn;
@@ -225,6 +220,152 @@ __global__ void __launch_bounds__(256) k_csr_jacobi(CsrArgs a) {
   if (threadIdx.x == 0) {
     double m = 0.0;
     for (int k = 0; k < (int)(blockDim.x >> 5); ++k) m = fmax(m, wmax[k]);
+    atomicMax(&a.ctl->dmax[a.launch_idx & (kRing - 1)], d2u(m));
+  }
+}
+
+// ------------------------------------------------- staged CSR sweep (bulk copies)
+// Multi-colour Gauss-Seidel / SOR of one colour's rows (Eq. (13)/(15) on an
+// arbitrary graph, colour-permuted rows, §IV), with the row data of
+// every tile of kCsrR rows -- row pointers, b, 1/d, column indices, values: all
+// contiguous in the colour-permuted store -- moved into shared memory by 1-D
+// bulk copies (cp.async.bulk, mbarrier completion, L2 evict_first) one tile
+// ahead of the compute (two stages per CTA, persistent CTAs).  The only
+// dependent global loads left are the gathers V[col] (the other colours' rows,
+// L2-resident for these grid sizes); each thread keeps the gathers of its two
+// rows in flight together.  Per-row arithmetic and summation order are those
+// of k_csr_sweep (bit-identical results).  Ranges are copied from 16-byte
+// aligned starts and rounded up to 16 bytes (the arrays carry zero slack).
+struct __align__(16) CsrStage {
+  int32_t rp[kCsrR + 8];
+  double b[kCsrR + 2];
+  double invd[kCsrR + 2];
+  int32_t col[kCsrE + 8];
+  double val[kCsrE + 4];
+};
+constexpr int kCsrT = 256;       // threads per CTA: two rows each
+constexpr int kCsrU = 6;         // gathers per row issued together (mesh-like degrees <= 6)
+
+__device__ __forceinline__ uint32_t csr_su32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void csr_bulk(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+      ::"r"(csr_su32(dst)), "l"(src), "r"(bytes), "r"(csr_su32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t r16(int64_t bytes) { return (uint32_t)((bytes + 15) & ~(int64_t)15); }
+
+__device__ void csr_issue(const CsrArgs &a, CsrStage *st, uint64_t *bar, int64_t t, uint64_t pol) {
+  const int64_t r0 = a.r0 + t * kCsrR, r1 = min(a.r1, r0 + kCsrR);
+  const int64_t k0 = a.rowptr[r0], k1 = a.rowptr[r1];
+  const int64_t ra = r0 & ~3ll, rb = r0 & ~1ll, ca = k0 & ~3ll, va = k0 & ~1ll;
+  const uint32_t n_rp = r16(4 * (r1 + 1 - ra)), n_b = r16(8 * (r1 - rb)), n_c = r16(4 * (k1 - ca)),
+                 n_v = r16(8 * (k1 - va));
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(csr_su32(bar)),
+               "r"(n_rp + 2 * n_b + n_c + n_v)
+               : "memory");
+  csr_bulk(st->rp, a.rowptr + ra, n_rp, bar, pol);
+  csr_bulk(st->b, a.b + rb, n_b, bar, pol);
+  csr_bulk(st->invd, a.invd + rb, n_b, bar, pol);
+  if (n_c) csr_bulk(st->col, a.col + ca, n_c, bar, pol);
+  if (n_v) csr_bulk(st->val, a.val + va, n_v, bar, pol);
+}
+
+__global__ void __launch_bounds__(kCsrT, 2) k_csr_sweep_staged(CsrArgs a) {
+  extern __shared__ __align__(16) unsigned char csr_smem[];
+  CsrStage *st = reinterpret_cast<CsrStage *>(csr_smem);
+  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ double wmax[kCsrT / 32];
+  a.launch_idx += *(volatile int32_t *)&a.ctl->jbase;
+  if (sweep_skip(a.ctl, a.launch_idx, a.tol, a.first != 0)) return;
+  zero_next_slot(a.ctl, a.launch_idx, a.first != 0);
+  double *V = (*(volatile int32_t *)&a.ctl->base) ? a.V1 : a.V0;
+  const int64_t ntiles = (a.r1 - a.r0 + kCsrR - 1) / kCsrR;
+  const int tid = threadIdx.x;
+  const uint64_t pf = pol_first();
+  if (tid == 0) {
+    for (int k = 0; k < 2; ++k)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(csr_su32(&bar[k])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (blockIdx.x < ntiles) csr_issue(a, &st[0], &bar[0], blockIdx.x, pf);
+    if (blockIdx.x + gridDim.x < ntiles) csr_issue(a, &st[1], &bar[1], blockIdx.x + gridDim.x, pf);
+  }
+  double dmax = 0.0;
+  int it = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    const int sg = it & 1;
+    CsrStage &S = st[sg];
+    {
+      const uint32_t par = (uint32_t)((it >> 1) & 1);
+      uint32_t done = 0;
+      while (!done)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(csr_su32(&bar[sg])), "r"(par)
+            : "memory");
+    }
+    const int64_t r0 = a.r0 + t * kCsrR;
+    const int nr = (int)min((int64_t)kCsrR, a.r1 - r0);
+    const int oa = (int)(r0 & 3), ob = (int)(r0 & 1);
+    const int32_t k0 = S.rp[oa];
+    const int32_t ca = k0 & ~3, va = k0 & ~1;
+    // two rows per thread, their gathers issued together
+    const int q0 = tid, q1 = tid + kCsrT;
+    const bool h0 = q0 < nr, h1 = q1 < nr;
+    int32_t e0 = h0 ? S.rp[oa + q0] : 0, f0 = h0 ? S.rp[oa + q0 + 1] : 0;
+    int32_t e1 = h1 ? S.rp[oa + q1] : 0, f1 = h1 ? S.rp[oa + q1 + 1] : 0;
+    double s0 = h0 ? S.b[ob + q0] : 0.0, s1 = h1 ? S.b[ob + q1] : 0.0;
+    while (e0 < f0 || e1 < f1) {
+      double v0[kCsrU], w0[kCsrU], v1[kCsrU], w1[kCsrU];
+#pragma unroll
+      for (int u = 0; u < kCsrU; ++u) {
+        const bool p0 = e0 + u < f0, p1 = e1 + u < f1;
+        v0[u] = p0 ? __ldg(V + S.col[e0 + u - ca]) : 0.0;
+        w0[u] = p0 ? S.val[e0 + u - va] : 0.0;
+        v1[u] = p1 ? __ldg(V + S.col[e1 + u - ca]) : 0.0;
+        w1[u] = p1 ? S.val[e1 + u - va] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kCsrU; ++u) {
+        if (e0 + u < f0) s0 = fma(w0[u], v0[u], s0);
+        if (e1 + u < f1) s1 = fma(w1[u], v1[u], s1);
+      }
+      e0 += kCsrU;
+      e1 += kCsrU;
+    }
+    if (h0) {
+      const int64_t i = r0 + q0;
+      const double vc = V[i];
+      const double vn = fma(a.omega, s0 * S.invd[ob + q0] - vc, vc);
+      V[i] = vn;
+      dmax = fmax(dmax, fabs(vn - vc));
+    }
+    if (h1) {
+      const int64_t i = r0 + q1;
+      const double vc = V[i];
+      const double vn = fma(a.omega, s1 * S.invd[ob + q1] - vc, vc);
+      V[i] = vn;
+      dmax = fmax(dmax, fabs(vn - vc));
+    }
+    // every thread is done reading stage sg: refill it (generic-proxy reads
+    // ordered before the async-proxy writes)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (tid == 0 && t + 2 * (int64_t)gridDim.x < ntiles) csr_issue(a, &S, &bar[sg], t + 2 * gridDim.x, pf);
+  }
+  dmax = warp_max(dmax);
+  if ((tid & 31) == 0) wmax[tid >> 5] = dmax;
+  __syncthreads();
+  if (tid == 0) {
+    double m = 0.0;
+    for (int k = 0; k < kCsrT / 32; ++k) m = fmax(m, wmax[k]);
     atomicMax(&a.ctl->dmax[a.launch_idx & (kRing - 1)], d2u(m));
   }
 }
@@ -376,12 +517,12 @@ __global__ void k_diag_mesh(MeshDims d, const double *gx, const double *gy, cons
   }
 }
 
-__global__ void k_diag_csr(int64_t n, const int64_t *rowptr, const double *val, const double *cap,
+__global__ void k_diag_csr(int64_t n, const int32_t *rowptr, const double *val, const double *cap,
                            double inv_h, double *out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0;
-    for (int64_t k = rowptr[i]; k < rowptr[i + 1]; ++k) s += val[k];
+    for (int32_t k = rowptr[i]; k < rowptr[i + 1]; ++k) s += val[k];
     out[i] = s + cap[i] * inv_h;
   }
 }
@@ -929,12 +1070,29 @@ cudaError_t launch_sweep(pg_grid *g, int method, double omega, double tol, int j
     a.V0 = g->V[0];
     a.V1 = g->V[1];
     if (method == PG_METHOD_RBSOR) {
+      const bool staged = g->csr_stage && g->csr_staged_ok;
+      if (staged) {
+        static std::atomic<bool> attr_set[64];
+        if (g->dev < 0 || g->dev >= 64) return cudaErrorInvalidDevice;
+        if (!attr_set[g->dev].load(std::memory_order_acquire)) {
+          cudaError_t e = cudaFuncSetAttribute(k_csr_sweep_staged, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)(2 * sizeof(CsrStage)));
+          if (e != cudaSuccess) return e;
+          attr_set[g->dev].store(true, std::memory_order_release);
+        }
+      }
       for (int c = 0; c < g->ncolor; ++c) {
         a.r0 = g->color_ptr[c];
         a.r1 = g->color_ptr[c + 1];
         a.first = c == 0;
         const int64_t rows = a.r1 - a.r0;
-        k_csr_sweep<<<grid_for(rows, 256, g->num_sms), 256, 0, g->stream>>>(a);
+        if (staged) {
+          const int64_t tiles = (rows + kCsrR - 1) / kCsrR;
+          const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 2 * (int64_t)g->num_sms));
+          k_csr_sweep_staged<<<grid, kCsrT, 2 * sizeof(CsrStage), g->stream>>>(a);
+        } else {
+          k_csr_sweep<<<grid_for(rows, 256, g->num_sms), 256, 0, g->stream>>>(a);
+        }
         ++*launches;
       }
     } else {
