@@ -286,6 +286,17 @@ PG_API int pg_group_p2p_connect(pg_group *grp, const void *blobs, int64_t blob_l
 PG_API int pg_group_transient(pg_group *grp, double h, int64_t steps, double tol, double omega,
                               int64_t max_sweeps, int64_t *sweeps_out, pg_stats *stats);
 
+/* Self-test of a connected CUDA-IPC peer group (no kernel waits on another
+ * rank, so it may run with all ranks on one GPU): phase 0 writes this rank's
+ * mark (0x5EED0000 + rank) into its control block and, through the mapped
+ * peer pointers, into element 0 of the neighbours' receive buffers; after a
+ * host barrier over all ranks, phase 1 reads every rank's mark through the
+ * mapped control blocks into out[0..nranks) and the marks the neighbours
+ * stored into this rank's lower / upper receive buffers into out[nranks],
+ * out[nranks+1] (-1 without that neighbour).  Call before the first
+ * transient (the first transient reseeds the receive buffers).          */
+PG_API int pg_group_p2p_selftest(pg_group *grp, int32_t phase, int64_t *out);
+
 /* pg_group_transient continued from every slab's current state (as
  * pg_transient_continue for a single grid).  Collective.                  */
 PG_API int pg_group_transient_continue(pg_group *grp, double h, int64_t steps, double tol, double omega,

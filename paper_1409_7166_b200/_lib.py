@@ -62,6 +62,7 @@ SIGNATURES = {
     "pg_group_transient": (_c_int, [_vp, _dbl, _i64, _dbl, _dbl, _i64, _vp, ctypes.POINTER(PgStats)]),
     "pg_group_transient_continue": (_c_int, [_vp, _dbl, _i64, _dbl, _dbl, _i64, _vp,
                                              ctypes.POINTER(PgStats)]),
+    "pg_group_p2p_selftest": (_c_int, [_vp, _i32, _vp]),
     "pg_group_destroy": (None, [_vp]),
     "pg_last_error": (ctypes.c_char_p, []),
 }

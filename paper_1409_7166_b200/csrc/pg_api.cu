@@ -809,9 +809,13 @@ namespace pgb {
 // relative to ctl->jbase, then jbase += batch), captured on a private stream
 // and cached per (omega, tol, method, F, batch, stream).  Replaying it replaces
 // `batch` + 1 host launches by one graph launch (small grids are launch-bound).
-int batch_graph(pg_grid *g, int method, double omega, double tol, int F) {
-  const double key[6] = {omega, tol, (double)method, (double)F, (double)g->batch,
-                         (double)(uintptr_t)g->stream};
+int batch_graph(pg_grid *g, int method, double omega, double tol, int F, Exchange *ex) {
+  // ex: a host-driven exchange after every sweep launch (NCCL norm allreduce
+  // + halo send/recv) captured into the same graph, so the host leaves the
+  // per-launch loop; its per-launch buffers depend on the launch index only
+  // modulo the norm ring (batch % kRing == 0), so one capture serves every batch
+  const double key[7] = {omega, tol, (double)method, (double)F, (double)g->batch,
+                         (double)(uintptr_t)g->stream, (double)(uintptr_t)ex};
   if (g->batch_exec && std::memcmp(key, g->graph_key, sizeof(key)) == 0) return PG_OK;
   if (g->batch_exec) {
     cudaGraphExecDestroy(g->batch_exec);
@@ -823,7 +827,10 @@ int batch_graph(pg_grid *g, int method, double omega, double tol, int F) {
   cudaGraph_t graph = nullptr;
   int64_t dummy = 0;
   cudaError_t e = cudaStreamBeginCapture(g->cap_stream, cudaStreamCaptureModeThreadLocal);
-  for (int b = 0; e == cudaSuccess && b < g->batch; ++b) e = launch_sweep(g, method, omega, tol, b, F, &dummy);
+  for (int b = 0; e == cudaSuccess && b < g->batch; ++b) {
+    e = launch_sweep(g, method, omega, tol, b, F, &dummy);
+    if (e == cudaSuccess && ex) e = ex->after_sweep(b, b, &dummy);
+  }
   if (e == cudaSuccess) e = launch_batch_advance(g, g->batch);
   cudaError_t e2 = cudaStreamEndCapture(g->cap_stream, &graph);
   g->stream = user;
@@ -929,7 +936,11 @@ int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, d
   // a single grid, or one slab per process whose exchange is fused into the
   // sweep kernels (peer memory), has nothing to do between sweep launches
   const bool quiet = ng == 1 && (ex == nullptr || ex->fused());
-  const bool graph_ok = g->use_graph && quiet;
+  // a host-driven exchange of one slab per process (NCCL) is captured into
+  // the batch graph together with the sweeps (NCCL calls are capturable)
+  const bool captured_ex = ng == 1 && ex != nullptr && !ex->fused() && ex->capturable() &&
+                           g->batch % kRing == 0;
+  const bool graph_ok = g->use_graph && (quiet || captured_ex);
   // consecutive sweep launches may overlap (PDL): launch j > 0 of a batch
   // directly follows launch j - 1 in the stream
   for (int k = 0; k < ng; ++k) gs[k]->pdl_ok = false;
@@ -1003,7 +1014,7 @@ int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, d
       // captured CUDA graph; launch indices are relative to ctl->jbase
       const bool full = nb == g->batch && (j + nb) * F <= max_sweeps;
       if (full && graph_ok && (j > 0 || g->batch_exec != nullptr)) {
-        if ((rc = batch_graph(g, method, omega, tol, F))) return rc;
+        if ((rc = batch_graph(g, method, omega, tol, F, captured_ex ? ex : nullptr))) return rc;
         CK(cudaGraphLaunch(g->batch_exec, st));
         launches += nb + 1;
       } else {

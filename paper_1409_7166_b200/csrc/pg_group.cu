@@ -203,6 +203,28 @@ __global__ void k_halo_unpack_p2p(MeshDims d, double *V0, double *V1, DevCtl *c,
   }
 }
 
+// pg_group_p2p_selftest: phase 0 marks this rank's control block and stores the
+// mark into element 0 of the neighbours' receive buffers through the mapped
+// pointers; phase 1 reads every rank's mark through its mapped control block
+// and the neighbours' marks from this rank's own receive buffers (no waiting:
+// the caller orders the phases with a host barrier)
+__global__ void k_p2p_mark(DevCtl *own, int64_t token, double *peer_lo, double *peer_hi) {
+  own->ipc_token = token;
+  if (peer_lo) peer_lo[0] = (double)token;
+  if (peer_hi) peer_hi[0] = (double)token;
+  __threadfence_system();
+}
+__global__ void k_p2p_read(unsigned long long *const *sig_all, int n, const double *recv_lo,
+                           const double *recv_hi, int64_t *out) {
+  for (int r = 0; r < n; ++r) {
+    const DevCtl *c = reinterpret_cast<const DevCtl *>(reinterpret_cast<const char *>(sig_all[r]) -
+                                                       offsetof(DevCtl, sig));
+    out[r] = *(volatile const int64_t *)&c->ipc_token;
+  }
+  out[n] = recv_lo ? (int64_t)*(volatile const double *)recv_lo : -1;
+  out[n + 1] = recv_hi ? (int64_t)*(volatile const double *)recv_hi : -1;
+}
+
 // local transport: max of the launch's norm slot over all slabs, written back
 __global__ void k_group_max(DevCtl **ctls, int n, int slot) {
   unsigned long long m = 0ull;
@@ -236,6 +258,10 @@ struct pg_group : public pgb::Exchange {
   bool has_hi(int k) const { return (local() ? k : rank) < nranks - 1; }
 
   bool fused() const override { return p2p(); }
+  // NCCL: one 8-byte allreduce and grouped send/recv of fixed buffers per
+  // launch -- captured into the sweep-batch graph (the local copy transport
+  // and its k_group_max over a device pointer table are capturable too)
+  bool capturable() const override { return kind == 0 || kind == 1; }
 
   cudaError_t after_sweep(int j, int jr, int64_t *launches) override {
     // peer-memory exchange: the sweep kernel itself stored the boundary rows
@@ -679,6 +705,38 @@ PG_API int pg_group_p2p_connect(pg_group *grp, const void *blobs, int64_t blob_l
   }
   g->hx = h;
   return attach_halo(grp);
+}
+
+PG_API int pg_group_p2p_selftest(pg_group *grp, int32_t phase, int64_t *out) {
+  REQ(grp != nullptr && grp->kind == 3, "not an ipc peer-memory group");
+  REQ(phase == 0 || phase == 1, "phase must be 0 (mark) or 1 (read)");
+  REQ(phase == 0 || out != nullptr, "out is NULL");
+  pg_grid *g = grp->slabs[0];
+  REQ(g->hx.p2p, "pg_group_p2p_connect has not run");
+  const int64_t token = 0x5EED0000ll + grp->rank;
+  if (phase == 0) {
+    k_p2p_mark<<<1, 1, 0, g->stream>>>(g->ctl, token, g->hx.peer_lo[0], g->hx.peer_hi[0]);
+    CKR(cudaGetLastError());
+    CKR(cudaStreamSynchronize(g->stream));
+    return PG_OK;
+  }
+  const int n = grp->nranks;
+  unsigned long long **d_sig = nullptr;
+  int64_t *d_out = nullptr;
+  CKR(cudaMalloc(&d_sig, sizeof(void *) * n));
+  CKR(cudaMalloc(&d_out, sizeof(int64_t) * (n + 2)));
+  cudaError_t e = cudaMemcpy(d_sig, g->hx.sig_all, sizeof(void *) * n, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    k_p2p_read<<<1, 1, 0, g->stream>>>(d_sig, n, g->hx.has_lo ? grp->recv_lo[0] : nullptr,
+                                       g->hx.has_hi ? grp->recv_hi[0] : nullptr, d_out);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+  if (e == cudaSuccess) e = cudaMemcpy(out, d_out, sizeof(int64_t) * (n + 2), cudaMemcpyDeviceToHost);
+  cudaFree(d_sig);
+  cudaFree(d_out);
+  if (e != cudaSuccess) return cuda_fail(e, "pg_group_p2p_selftest");
+  return PG_OK;
 }
 
 static int group_transient(pg_group *grp, double h, int64_t steps, double tol, double omega,

@@ -40,6 +40,7 @@ struct DevCtl {
   unsigned long long pnorm[4];
   int32_t p2p_timeout;     // a peer wait gave up (watchdog), results invalid
   int32_t nonfinite;       // an iterate held NaN / Inf (checked by the RHS kernel and at the end of a call)
+  int64_t ipc_token;       // pg_group_p2p_selftest: this rank's mark, read by the peers through their mappings
 };
 
 constexpr int kRing = 4;
@@ -189,7 +190,7 @@ struct pg_grid {
   bool group_active = false;           // inside pg_group_transient (peer exchange armed)
   cudaGraphExec_t batch_exec = nullptr;  // captured batch of `batch` full sweep launches
   cudaStream_t cap_stream = nullptr;     // private stream the batch graph is captured on
-  double graph_key[6] = {0, 0, 0, 0, 0, 0};  // omega, tol, method, F, batch, stream of the capture
+  double graph_key[7] = {0, 0, 0, 0, 0, 0, 0};  // omega, tol, method, F, batch, stream, exchange of the capture
 };
 
 namespace pgb {
@@ -245,6 +246,9 @@ struct Exchange {
   // the exchange happens inside the sweep kernels (nothing between launches):
   // a single slab per process may then use graph batches and PDL
   virtual bool fused() const { return false; }
+  // after_sweep may be captured into a CUDA graph (its buffers do not depend on
+  // the launch index beyond j % kRing)
+  virtual bool capturable() const { return false; }
 };
 int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, double tol,
                   double omega, int method, int64_t max_sweeps, int64_t n_probe,

@@ -225,6 +225,13 @@ class SlabGroup:
             L.check(code)
         return GroupResult(sweeps=sweeps, stats=st, status=code)
 
+    def p2p_selftest(self, phase: int):
+        """pg_group_p2p_selftest (CUDA-IPC groups): phase 0 marks, phase 1
+        returns the marks read through the mappings (nranks + 2 int64)."""
+        out = np.zeros(self.specs[0].nranks + 2, dtype=np.int64)
+        L.check(self._lib.pg_group_p2p_selftest(self._h, int(phase), out.ctypes.data))
+        return out
+
     def owned_voltages(self, m) -> List[Tuple[SlabSpec, np.ndarray]]:
         """[(spec, V)] per slab of this process: V[l, y - y0, x] for owned rows."""
         out = []

@@ -162,3 +162,54 @@ def test_p2p_slab_grid_alone_is_refused(pgb):
     r2 = grp.transient(g.h, 2, tol=1e-10, omega=1.8, max_sweeps=200000)
     assert np.array_equal(r1.sweeps, r2.sweeps)
     grp.close()
+
+
+def _ipc_rank(rank, world, port, q):
+    # one process per rank, all on cuda:0: the CUDA-IPC export / all-gather /
+    # cudaIpcOpenMemHandle connect path across processes, then the self-test
+    # (plain stores and loads through the mappings, no kernel waits on another
+    # rank -- B200_PROFILING.md forbids waiting ranks on one GPU)
+    import os
+    import torch
+    import torch.distributed as dist
+    import paper_1409_7166_b200 as P
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = gridgen.mesh_grid(2, 48, 40, seed=3, pad_pitch=5, h=10e-12, src_start=5e-12, src_width=30e-12)
+        grp = P.SlabGroup.p2p(g, rank, world, fuse=2)
+        grp.p2p_selftest(0)
+        torch.cuda.synchronize()
+        dist.barrier()
+        out = grp.p2p_selftest(1)
+        dist.barrier()
+        grp.close()
+        q.put((rank, out.tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_p2p_ipc_mapping_across_processes(pgb, world):
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_ipc_rank, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in range(world))
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        out = res[r]
+        assert out[:world] == [0x5EED0000 + k for k in range(world)]          # every control block
+        assert out[world] == (0x5EED0000 + r - 1 if r > 0 else -1)            # lower neighbour's store
+        assert out[world + 1] == (0x5EED0000 + r + 1 if r < world - 1 else -1)  # upper neighbour's store

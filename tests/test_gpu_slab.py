@@ -109,13 +109,28 @@ def test_nccl_group_single_rank(pgb):
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ.setdefault("MASTER_PORT", "29531")
     dist.init_process_group("gloo", rank=0, world_size=1)
+    res = {}
     try:
-        grp = P.SlabGroup.nccl(g, 0, 1, fuse=2)
-        rn = grp.transient(g.h, 6, tol=1e-10, omega=1.8, max_sweeps=200000)
-        (sp, Vn), = grp.owned_voltages(g)
-        grp.close()
+        # graph = 1: full batches of sweep launches replayed from a CUDA graph
+        # with the NCCL allreduce (and send/recv) captured after every launch;
+        # graph = 0: host-enqueued; and the transient cut into two calls
+        for graph in (1, 0):
+            grp = P.SlabGroup.nccl(g, 0, 1, fuse=2)
+            grp.grids[0].set_option("graph", graph)
+            rn = grp.transient(g.h, 6, tol=1e-10, omega=1.8, max_sweeps=200000)
+            (sp, Vn), = grp.owned_voltages(g)
+            r2 = grp.transient(g.h, 2, tol=1e-10, omega=1.8, max_sweeps=200000)
+            r3 = grp.transient(g.h, 4, tol=1e-10, omega=1.8, max_sweeps=200000, cont=True)
+            (sp, Vc), = grp.owned_voltages(g)
+            grp.close()
+            res[graph] = (rn, Vn, np.concatenate([r2.sweeps, r3.sweeps[1:]]), Vc)
     finally:
         dist.destroy_process_group()
     r1, V1 = single(P, g, 6, 1e-10, 1.8, 200000, 2)
-    np.testing.assert_array_equal(rn.sweeps, r1.sweeps)
-    np.testing.assert_array_equal(Vn, V1)
+    assert r1.sweeps.max() > 8 * 2      # several sweep batches per step: the graph path runs
+    for graph in (1, 0):
+        rn, Vn, sc, Vc = res[graph]
+        np.testing.assert_array_equal(rn.sweeps, r1.sweeps)
+        np.testing.assert_array_equal(Vn, V1)
+        np.testing.assert_array_equal(sc, r1.sweeps)
+        np.testing.assert_array_equal(Vc, V1)
