@@ -197,6 +197,9 @@ void oracle_inductor_update(int64_t nl, const int64_t *la, const int64_t *lb,
  *   of V^(k) (diagnostic only: V(s) stays V^(k)).  The GPU tests its stopping
  *   criterion every F sweeps (R13); these let a test compute the
  *   sweep at which that criterion first holds.
+ * check_every: Algorithm 1 line 8 is evaluated after every sweep (1, the
+ *   paper) or only after sweeps k that are multiples of check_every (DESIGN.md
+ *   R13: the GPU tests once per launch of F fused sweeps).
  * Returns 0, or -(s) if step s hit max_sweeps without meeting tol.          */
 int64_t oracle_transient(int64_t n, const int64_t *order, const int64_t *rptr,
                          const int64_t *rnbr, const double *rg, const int64_t *lptr,
@@ -206,7 +209,8 @@ int64_t oracle_transient(int64_t n, const int64_t *order, const int64_t *rptr,
                          const double *vd, int form, int method, double h,
                          int64_t steps, double tol, double omega, int64_t max_sweeps,
                          const double *Iload, const double *V0, const double *V1,
-                         double *il, double *Vout, int64_t *sweeps_out, double *dtrace) {
+                         double *il, double *Vout, int64_t *sweeps_out, double *dtrace,
+                         int64_t check_every) {
   double *d = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
   double *known = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
   double *tmp = (double *)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
@@ -242,7 +246,7 @@ int64_t oracle_transient(int64_t n, const int64_t *order, const int64_t *rptr,
         dmax = oracle_jacobi(n, rptr, rnbr, rg, lptr, lnbr, lval, lres, h, d, known, omega, Vs, tmp);
         memcpy(Vs, tmp, sizeof(double) * (size_t)n);
       }
-    } while (!(dmax < tol) && k < max_sweeps); /* line 8: until ||V^(k) - V^(k-1)|| < tol */
+    } while (!(k % check_every == 0 && dmax < tol) && k < max_sweeps); /* line 8: until ||V^(k) - V^(k-1)|| < tol */
     sweeps_out[s] = k;
     if (dtrace) {
       double *r = dtrace + s * 6;

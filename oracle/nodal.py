@@ -139,7 +139,7 @@ class NodalOracle:
     def transient(self, h: float, steps: int, tol: float = 1e-10, omega: float = 1.0,
                   form: str = "companion", method: str = "gs", order=None,
                   Itab=None, V0=None, V1=None, il0=None, max_sweeps: int = 1_000_000,
-                  trace: bool = False):
+                  trace: bool = False, check_every: int = 1):
         nl = self.nl
         n = nl.n
         if Itab is None:
@@ -172,7 +172,7 @@ class NodalOracle:
             ctypes.c_double(h), ctypes.c_int64(steps), ctypes.c_double(tol),
             ctypes.c_double(omega), ctypes.c_int64(max_sweeps), _pd(Itab), _pd(V0),
             _pd(V1) if f == 1 else None, _pd(il), _pd(Vout), _p64(sw),
-            _pd(dt) if trace else None)
+            _pd(dt) if trace else None, ctypes.c_int64(max(1, int(check_every))))
         return TransientResult(V=Vout, sweeps=sw, il=il, status=int(st), dtrace=dt)
 
 

@@ -208,16 +208,10 @@ void free_grid(pg_grid *g) {
   if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
   if (g->ctl_host) cudaFreeHost(g->ctl_host);
   if (g->done_host) cudaFreeHost(g->done_host);
-  if (g->counted && g->dev >= 0 && g->dev < 64 && g_live_grids[g->dev].fetch_sub(1) == 1) {
-    // the last grid of this device: hand the pool's cached memory back to the
-    // device, so other users of cudaMalloc (NCCL, torch, halo buffers) can have it
-    std::lock_guard<std::mutex> lk(g_pool_mu);
-    DevPool *d = pool_of(g->dev);
-    if (d) {
-      cudaStreamSynchronize(d->s);
-      cudaMemPoolTrimTo(d->pool, 0);
-    }
-  }
+  if (g->counted && g->dev >= 0 && g->dev < 64) g_live_grids[g->dev].fetch_sub(1);
+  // the pool keeps up to its release threshold of freed memory cached for the
+  // next grid (re-mapping ~10 GB for a config-4-sized grid costs ~1 s); an
+  // allocation the pool cannot serve trims it before falling back to cudaMalloc
   if (other) cudaSetDevice(cur);
   delete g;
 }
@@ -324,6 +318,16 @@ int set_pads(pg_grid *g, int64_t n_pads, const int64_t *pad_node, const double *
 
 }  // namespace
 
+namespace pgb {
+int dalloc_bytes(void **p, size_t bytes) {
+  unsigned char *q = nullptr;
+  const int rc = dalloc(&q, (int64_t)bytes);
+  *p = q;
+  return rc;
+}
+void dfree_bytes(void *p) { dfree(p); }
+}  // namespace pgb
+
 extern "C" {
 
 PG_API const char *pg_last_error(void) { return g_err.c_str(); }
@@ -341,27 +345,6 @@ PG_API int pg_create_mesh(int32_t layers, int32_t ny, int32_t nx, const double *
   REQUIRE(n_pads >= 0 && (n_pads == 0 || (pad_node && pad_g)), "bad pad arrays");
   REQUIRE(std::isfinite(vdd), "vdd must be finite");
   const int64_t n = (int64_t)layers * ny * nx;
-  if (mem == PG_MEM_HOST) {  // value checks (device inputs are trusted)
-    bool ok_val = true, ok_x = true, ok_y = true, ok_z = true, ok_l = true;
-    int64_t k = 0;
-    for (int32_t l = 0; l < layers; ++l)
-      for (int32_t y = 0; y < ny; ++y) {
-        for (int32_t x = 0; x < nx; ++x, ++k)
-          ok_val &= gx[k] >= 0 && gy[k] >= 0 && gz[k] >= 0 && cap[k] >= 0 && std::isfinite(cap[k]);
-        ok_x &= gx[k - 1] == 0.0;
-        if (y == ny - 1)
-          for (int32_t x = 0; x < nx; ++x) ok_y &= gy[k - nx + x] == 0.0;
-        if (l == layers - 1)
-          for (int32_t x = 0; x < nx; ++x) ok_z &= gz[k - nx + x] == 0.0;
-      }
-    if (lz)
-      for (int64_t q = 0; q < n; ++q) ok_l &= lz[q] >= 0.0 && std::isfinite(lz[q]);
-    REQUIRE(ok_val, "conductances and capacitances must be >= 0");
-    REQUIRE(ok_x, "gx must be 0 in the last column");
-    REQUIRE(ok_y, "gy must be 0 in the last row");
-    REQUIRE(ok_z, "gz must be 0 in the top layer");
-    REQUIRE(ok_l, "lz must be finite and >= 0");
-  }
   pg_grid *g = new pg_grid();
   GridGuard guard{g};
   g->kind = 0;
@@ -379,28 +362,44 @@ PG_API int pg_create_mesh(int32_t layers, int32_t ny, int32_t nx, const double *
   if ((rc = common_init(g))) return rc;
   const cudaMemcpyKind kind = mem == PG_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
   double *stage = nullptr;  // user-order staging buffer, scattered into the storage layout
-  if ((rc = dalloc(&stage, n))) return rc;
+  int32_t *d_bad = nullptr;  // value-check flags of the inputs (checked on the device)
+  if ((rc = dalloc(&stage, n)) || (rc = dalloc(&d_bad, 1))) return rc;
   struct StageGuard {
     double *p;
-    ~StageGuard() { dfree(p); }
-  } stage_guard{stage};
-  auto put = [&](double **dst, const double *src) -> int {
+    int32_t *q;
+    ~StageGuard() {
+      dfree(p);
+      dfree(q);
+    }
+  } stage_guard{stage, d_bad};
+  CK(cudaMemset(d_bad, 0, sizeof(int32_t)));
+  // which: 0 gx, 1 gy, 2 gz (>= 0, finite, zero on the open boundary), 3 cap, 4 lz (>= 0, finite)
+  auto put = [&](double **dst, const double *src, int which) -> int {
     int r = dalloc(dst, g->np);
     if (r) return r;
     CK(cudaMemset(*dst, 0, sizeof(double) * g->np));
     CK(cudaMemcpy(stage, src, sizeof(double) * n, kind));
+    CK(mesh_check_async(g, stage, which, d_bad));
     CK(launch_scatter_user(g, stage, *dst));
     return PG_OK;
   };
-  if ((rc = put(&g->gx, gx)) || (rc = put(&g->gy, gy)) || (rc = put(&g->gz, gz)) || (rc = put(&g->cap, cap)))
+  if ((rc = put(&g->gx, gx, 0)) || (rc = put(&g->gy, gy, 1)) || (rc = put(&g->gz, gz, 2)) ||
+      (rc = put(&g->cap, cap, 3)))
     return rc;
   if ((rc = dalloc(&g->gze, g->np))) return rc;
   CK(cudaMemcpy(g->gze, g->gz, sizeof(double) * g->np, cudaMemcpyDeviceToDevice));
   if (lz) {
-    if ((rc = put(&g->lz, lz)) || (rc = dalloc(&g->iz, g->np))) return rc;
+    if ((rc = put(&g->lz, lz, 4)) || (rc = dalloc(&g->iz, g->np))) return rc;
     CK(cudaMemset(g->iz, 0, sizeof(double) * g->np));
     g->rlc = true;
   }
+  int32_t bad = 0;
+  CK(cudaMemcpy(&bad, d_bad, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  REQUIRE(!(bad & (1 << 0)), "gx must be finite, >= 0 and 0 in the last column");
+  REQUIRE(!(bad & (1 << 1)), "gy must be finite, >= 0 and 0 in the last row");
+  REQUIRE(!(bad & (1 << 2)), "gz must be finite, >= 0 and 0 in the top layer");
+  REQUIRE(!(bad & (1 << 3)), "cap must be finite and >= 0");
+  REQUIRE(!(bad & (1 << 4)), "lz must be finite and >= 0");
   if ((rc = set_pads(g, n_pads, pad_node, pad_g, pad_l, mem, nullptr))) return rc;
   CK(cudaDeviceSynchronize());
   guard.g = nullptr;
@@ -568,108 +567,68 @@ PG_API int pg_set_sources(pg_grid *g, int64_t n_src, const int64_t *node, const 
   REQUIRE(g != nullptr, "grid is NULL");
   REQUIRE(n_src >= 0, "n_src must be >= 0");
   REQUIRE(mem == PG_MEM_HOST || mem == PG_MEM_DEVICE, "bad mem");
-  for (int64_t *p : {g->src_idx, g->src_grp, g->src_ptr, g->src_tile})
-    if (p) dfree(p);
-  for (double *p : {g->pwl_t, g->pwl_i})
-    if (p) dfree(p);
-  g->src_idx = g->src_grp = g->src_ptr = g->src_tile = nullptr;
-  g->pwl_t = g->pwl_i = nullptr;
-  g->nsrc = g->nsrc_grp = g->npts = 0;
-  if (n_src == 0) return PG_OK;
-  REQUIRE(node && ptr && t && i, "source arrays are NULL");
-  // host inputs are read in place; device inputs are copied to the host first
-  std::vector<int64_t> nd_v, pp_v;
+  REQUIRE(n_src == 0 || (node && ptr && t && i), "source arrays are NULL");
+  int64_t npts = 0;
+  if (n_src > 0) {
+    if (mem == PG_MEM_HOST)
+      npts = ptr[n_src];
+    else
+      CK(cudaMemcpy(&npts, ptr + n_src, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    REQUIRE(npts >= n_src, "ptr[n_src] must be >= n_src (every source needs at least one breakpoint)");
+  }
+  // the store is built on the device (pg_store.cu): host inputs are copied
+  // there first (pinned host buffers at full PCIe / C2C speed)
+  const int64_t *d_node = node, *d_ptr = ptr;
+  const double *d_t = t, *d_i = i;
+  void *tmp[4] = {nullptr, nullptr, nullptr, nullptr};
+  struct TmpGuard {
+    void **p;
+    ~TmpGuard() {
+      for (int k = 0; k < 4; ++k)
+        if (p[k]) dfree(p[k]);
+    }
+  } tg{tmp};
   int rc;
-  if (mem == PG_MEM_DEVICE &&
-      ((rc = to_host(node, n_src, mem, nd_v)) || (rc = to_host(ptr, n_src + 1, mem, pp_v))))
-    return rc;
-  const int64_t *nd = mem == PG_MEM_DEVICE ? nd_v.data() : node;
-  const int64_t *pp = mem == PG_MEM_DEVICE ? pp_v.data() : ptr;
-  REQUIRE(pp[0] == 0, "ptr[0] must be 0");
-  for (int64_t k = 0; k < n_src; ++k) {
-    REQUIRE(pp[k + 1] > pp[k], "every source needs at least one breakpoint");
-    REQUIRE(nd[k] >= 0 && nd[k] < g->n, "source node index out of range");
-  }
-  const int64_t npts = pp[n_src];
-  std::vector<double> tt_v, ii_v;
-  if (mem == PG_MEM_DEVICE && ((rc = to_host(t, npts, mem, tt_v)) || (rc = to_host(i, npts, mem, ii_v))))
-    return rc;
-  const double *tt = mem == PG_MEM_DEVICE ? tt_v.data() : t;
-  const double *ii = mem == PG_MEM_DEVICE ? ii_v.data() : i;
-  for (int64_t k = 0; k < n_src; ++k) {
-    for (int64_t q = pp[k]; q < pp[k + 1]; ++q)
-      REQUIRE(std::isfinite(tt[q]) && std::isfinite(ii[q]), "PWL breakpoints and values must be finite");
-    for (int64_t q = pp[k] + 1; q < pp[k + 1]; ++q)
-      REQUIRE(tt[q] > tt[q - 1], "PWL breakpoint times must be strictly increasing");
-  }
-  std::vector<int64_t> iperm_h;
-  if (g->kind == 1) {
-    iperm_h.resize((size_t)g->n);
-    CK(cudaMemcpy(iperm_h.data(), g->iperm, sizeof(int64_t) * g->n, cudaMemcpyDeviceToHost));
-  }
-  std::vector<int64_t> sidx((size_t)n_src);
-  if (g->kind == 0 && g->n < ((int64_t)1 << 31)) {
-    // 32-bit divisions (a 64-bit division per coordinate dominated this call)
-    const uint32_t per_layer = (uint32_t)g->md.NY * (uint32_t)g->md.NX, NX = (uint32_t)g->md.NX;
-    for (int64_t k = 0; k < n_src; ++k) {
-      const uint32_t v = (uint32_t)nd[k], l = v / per_layer, r = v - l * per_layer, y = r / NX, x = r - y * NX;
-      sidx[k] = mesh_index(g->md, l, y, x);
+  if (n_src > 0 && mem == PG_MEM_HOST) {
+    int64_t *a = nullptr, *b = nullptr;
+    double *c = nullptr, *d = nullptr;
+    if ((rc = dalloc(&a, n_src)) || (rc = dalloc(&b, n_src + 1)) || (rc = dalloc(&c, npts)) ||
+        (rc = dalloc(&d, npts))) {
+      for (void *p : {(void *)a, (void *)b, (void *)c, (void *)d})
+        if (p) dfree(p);
+      return rc;
     }
+    tmp[0] = a, tmp[1] = b, tmp[2] = c, tmp[3] = d;
+    CK(cudaMemcpyAsync(a, node, sizeof(int64_t) * n_src, cudaMemcpyHostToDevice, g->stream));
+    CK(cudaMemcpyAsync(b, ptr, sizeof(int64_t) * (n_src + 1), cudaMemcpyHostToDevice, g->stream));
+    CK(cudaMemcpyAsync(c, t, sizeof(double) * npts, cudaMemcpyHostToDevice, g->stream));
+    CK(cudaMemcpyAsync(d, i, sizeof(double) * npts, cudaMemcpyHostToDevice, g->stream));
+    d_node = a, d_ptr = b, d_t = c, d_i = d;
+  }
+  int64_t *old_i64[4] = {g->src_idx, g->src_grp, g->src_ptr, g->src_tile};
+  double *old_d[2] = {g->pwl_t, g->pwl_i};
+  if (n_src > 0) {
+    int32_t bad = 0;
+    std::string err;
+    if ((rc = build_sources_device(g, n_src, d_node, d_ptr, d_t, d_i, npts, &bad, err))) {
+      set_error("pg_set_sources: " + err);
+      return rc;
+    }
+    REQUIRE(!(bad & 1), "ptr[0] must be 0");
+    REQUIRE(!(bad & 2), "every source needs at least one breakpoint");
+    REQUIRE(!(bad & 4), "source node index out of range");
+    REQUIRE(!(bad & 8), "PWL breakpoint times must be strictly increasing");
+    REQUIRE(!(bad & 16), "PWL breakpoints and values must be finite");
   } else {
-    for (int64_t k = 0; k < n_src; ++k) sidx[k] = storage_index(g, nd[k], &iperm_h);
+    g->src_idx = g->src_grp = g->src_ptr = g->src_tile = nullptr;
+    g->pwl_t = g->pwl_i = nullptr;
+    g->nsrc = g->nsrc_grp = g->npts = 0;
   }
-  // sources in storage order (ties: input order, so per-node sums are
-  // deterministic); (key, position) pairs sort faster than an indirect stable sort
-  std::vector<int64_t> order((size_t)n_src);
-  if (g->kind == 0 && std::is_sorted(nd, nd + n_src)) {
-    // sources in natural node order (the common case): inside each row the
-    // storage order is the even columns, then the odd ones -- a stable
-    // two-way partition per row, no comparison sort
-    int64_t a = 0;
-    while (a < n_src) {
-      const int64_t row = nd[a] / g->md.NX;
-      int64_t b = a;
-      while (b < n_src && nd[b] / g->md.NX == row) ++b;
-      int64_t o = a;
-      for (int64_t k = a; k < b; ++k)
-        if (((nd[k] % g->md.NX) & 1) == 0) order[o++] = k;
-      for (int64_t k = a; k < b; ++k)
-        if (((nd[k] % g->md.NX) & 1) == 1) order[o++] = k;
-      a = b;
-    }
-  } else {
-    std::vector<std::pair<int64_t, int64_t>> kp((size_t)n_src);
-    for (int64_t k = 0; k < n_src; ++k) kp[k] = {sidx[k], k};
-    if (!std::is_sorted(kp.begin(), kp.end())) std::sort(kp.begin(), kp.end());
-    for (int64_t k = 0; k < n_src; ++k) order[k] = kp[k].second;
-  }
-  std::vector<int64_t> s2(n_src), p2(n_src + 1);
-  std::vector<double> t2((size_t)npts), i2((size_t)npts);
-  int64_t off = 0;
-  for (int64_t k = 0; k < n_src; ++k) {
-    const int64_t o = order[k];
-    s2[k] = sidx[o];
-    p2[k] = off;
-    for (int64_t q = pp[o]; q < pp[o + 1]; ++q, ++off) {
-      t2[off] = tt[q];
-      i2[off] = ii[q];
-    }
-  }
-  p2[n_src] = off;
-  std::vector<int64_t> grp = groups_of(s2);
-  std::vector<int64_t> gnode(grp.size() - 1);
-  for (size_t q = 0; q + 1 < grp.size(); ++q) gnode[q] = s2[grp[q]];
-  const std::vector<int64_t> tiles = rhs_tile_starts(gnode, g->np);
-  if ((rc = dalloc(&g->src_idx, n_src)) || (rc = dalloc(&g->src_grp, (int64_t)grp.size())) ||
-      (rc = dalloc(&g->src_ptr, n_src + 1)) || (rc = dalloc(&g->pwl_t, npts)) || (rc = dalloc(&g->pwl_i, npts)) ||
-      (rc = dalloc(&g->src_tile, (int64_t)tiles.size())))
-    return rc;
-  if ((rc = upload(g->src_idx, s2)) || (rc = upload(g->src_grp, grp)) || (rc = upload(g->src_ptr, p2)) ||
-      (rc = upload(g->pwl_t, t2)) || (rc = upload(g->pwl_i, i2)) || (rc = upload(g->src_tile, tiles)))
-    return rc;
-  g->nsrc = n_src;
-  g->nsrc_grp = (int64_t)grp.size() - 1;
-  g->npts = npts;
+  // the new store is in place: release the previous one
+  for (int64_t *p : old_i64)
+    if (p) dfree(p);
+  for (double *p : old_d)
+    if (p) dfree(p);
   return PG_OK;
 }
 

@@ -256,8 +256,14 @@ int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, d
                   pg_stats *stats, double t_dc = 0.0, bool cont = false);
 // first group of every RHS tile: tiles[t] = first q with node_of_group[q] >= t * kRhsTile
 std::vector<int64_t> rhs_tile_starts(const std::vector<int64_t> &group_node, int64_t np);
-// upload / download helpers (pg_api.cu)
+// the library's device allocator (pg_api.cu: stream-ordered pool, 256-byte
+// aligned blocks, cudaMalloc / cudaFree semantics)
 int dalloc_bytes(void **p, size_t bytes);
+void dfree_bytes(void *p);
+// device-side store construction (pg_store.cu)
+int build_sources_device(pg_grid *g, int64_t n_src, const int64_t *node, const int64_t *ptr, const double *t,
+                         const double *v, int64_t npts, int32_t *bad_bits, std::string &err);
+cudaError_t mesh_check_async(pg_grid *g, const double *user_array, int which, int32_t *d_err);
 
 // host CSR construction (pg_csr_build.cpp)
 struct CsrHost {

@@ -517,3 +517,26 @@ def test_stopping_record():
         norms.append(dm)
     np.testing.assert_array_equal(np.array(norms[k - 2:k + 4]) if k >= 2 else norms[k - 1:k + 4],
                                   r.dtrace[1] if k >= 2 else r.dtrace[1, 1:])
+
+
+def test_check_every_is_line8_tested_every_f_sweeps():
+    # check_every = F evaluates Algorithm 1 line 8 only after sweeps that are
+    # multiples of F (R13): the first step stops at the first such sweep whose
+    # norm is below tol, read off the paper-semantics run's stopping record
+    g = gridgen.config_grid(0, dims=(2, 14, 16), steps=4)
+    nl = netlist.from_grid(g)
+    o = nodal.NodalOracle(nl)
+    It = pwl.node_currents_table(nl, g.h, 4)
+    order = nodal.red_black_order(g.layers, g.ny, g.nx)
+    r1 = o.transient(g.h, 4, tol=1e-10, omega=1.8, order=order, Itab=It, trace=True)
+    for F in (1, 2, 3):
+        rF = o.transient(g.h, 4, tol=1e-10, omega=1.8, order=order, Itab=It, trace=True, check_every=F)
+        k = int(r1.sweeps[1])
+        norms = {k - 1: r1.dtrace[1, 0], k: r1.dtrace[1, 1]}
+        norms.update({k + 1 + e: r1.dtrace[1, 2 + e] for e in range(4)})
+        j = -(-k // F) * F
+        while not norms[j] < 1e-10:
+            j += F
+        assert rF.sweeps[1] == j and np.all(rF.sweeps[1:] % F == 0)
+        if F == 1:
+            np.testing.assert_array_equal(rF.V, r1.V)
