@@ -318,11 +318,14 @@ PG_API int pg_dc(pg_grid *g, double t, double tol, double omega, int method, int
 
 /* Relaxation factor for Eq. (15) by Young's theory (§IV-D defers the
  * choice of omega to [Young]): `sweeps` Jacobi sweeps of the homogeneous
- * system (C/h + G + hL) e = 0 from x(0) estimate the spectral radius rho of the
- * Jacobi iteration matrix (ratio of successive max-norm differences, power
- * iteration); for the red-black (2-cyclic, consistently ordered) numbering
- * the optimal SOR factor is 2 / (1 + sqrt(1 - rho^2)) (clamped to 1.999).
- * Leaves the grid's state as after creation / pg_set_voltages.            */
+ * system (C/h + G + hL) e = 0 from x(0); the spectral radius rho of the Jacobi
+ * iteration matrix J is estimated by the Rayleigh quotient of J^2 at the
+ * second-to-last iterate, rho^2 ~ ||e_N||_D^2 / ||e_{N-1}||_D^2 (D = diagonal of
+ * the system; D^{1/2} J D^{-1/2} is symmetric), and for the red-black
+ * (2-cyclic, consistently ordered) numbering the optimal SOR factor is
+ * 2 / (1 + sqrt(1 - rho^2)) (clamped to 1.999).  The estimate approaches rho
+ * from below as `sweeps` grows.  Leaves the grid's state as after creation /
+ * pg_set_voltages.                                                        */
 PG_API int pg_estimate_omega(pg_grid *g, double h, int64_t sweeps, double *rho, double *omega_opt);
 
 /* Number of nodes / dimensions (layers, ny, nx are 0 for CSR grids). */

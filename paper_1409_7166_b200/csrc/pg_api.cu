@@ -718,41 +718,41 @@ PG_API int pg_estimate_omega(pg_grid *g, double h, int64_t sweeps, double *rho, 
   REQUIRE(sweeps >= 8, "need at least 8 Jacobi sweeps");
   cudaStream_t st = g->stream;
   int rc;
-  unsigned long long *hist = nullptr;
-  if ((rc = dalloc(&hist, sweeps))) return rc;
+  const int nb = dnorm2_blocks(g);
+  double *part = nullptr;
+  if ((rc = dalloc(&part, 2 * (int64_t)nb))) return rc;
   struct Free {
     void *p;
     ~Free() { dfree(p); }
-  } fr{hist};
+  } fr{part};
   // Jacobi (omega = 1) on the homogeneous system M e = 0 from the start vector
-  // x(0): the differences V^(k) - V^(k-1) obey the same iteration, so the
-  // ratio of successive max-norms tends to the spectral radius of
-  // J = I - D^{-1} M (power iteration; Young: omega_opt = 2 / (1 + sqrt(1 - rho^2))
-  // for the red-black (consistently ordered, 2-cyclic) numbering)
+  // x(0) (b = 0): V^(k) = J^k x(0), J = I - D^{-1} M.  D^{1/2} J D^{-1/2} is
+  // symmetric and D J^2 = J^T D J, so ||V^(N)||_D^2 / ||V^(N-1)||_D^2 is the
+  // Rayleigh quotient of J^2 at V^(N-1): it tends to rho(J)^2 from below, with
+  // an error that decays twice as fast (in the exponent) as the ratio of
+  // successive norms, and it is not fooled by the +-rho pair of the 2-cyclic
+  // (red-black) spectrum.  Young: omega_opt = 2 / (1 + sqrt(1 - rho^2)) for the
+  // consistently ordered red-black numbering (§IV-D refers to Young).
   CK(launch_setup(g, h));
   CK(cudaMemsetAsync(g->b, 0, sizeof(double) * g->np, st));
   CK(cudaMemcpyAsync(g->V[0], g->x0, sizeof(double) * g->np, cudaMemcpyDeviceToDevice, st));
   CK(launch_reset_state(g));
   int64_t launches = 0;
-  for (int64_t j = 0; j < sweeps; ++j) {
-    CK(launch_sweep(g, PG_METHOD_JACOBI, 1.0, 0.0, (int)j, 1, &launches));
-    CK(cudaMemcpyAsync(hist + j, &g->ctl->dmax[j & (kRing - 1)], sizeof(unsigned long long),
-                       cudaMemcpyDeviceToDevice, st));
-  }
-  std::vector<unsigned long long> hh((size_t)sweeps);
-  CK(cudaMemcpyAsync(hh.data(), hist, sizeof(unsigned long long) * sweeps, cudaMemcpyDeviceToHost, st));
+  for (int64_t j = 0; j < sweeps; ++j) CK(launch_sweep(g, PG_METHOD_JACOBI, 1.0, 0.0, (int)j, 1, &launches));
+  // launch j reads V[j & 1] and writes V[(j + 1) & 1]: V^(N) is in V[N & 1]
+  CK(launch_dnorm2(g, part));
+  std::vector<double> hp(2 * (size_t)nb);
+  CK(cudaMemcpyAsync(hp.data(), part, sizeof(double) * 2 * nb, cudaMemcpyDeviceToHost, st));
   CK(launch_reset_state(g));
   CK(cudaMemcpyAsync(g->V[0], g->x0, sizeof(double) * g->np, cudaMemcpyDeviceToDevice, st));
   CK(cudaStreamSynchronize(st));
-  auto val = [&](int64_t k) {
-    double d;
-    std::memcpy(&d, &hh[(size_t)k], sizeof(d));
-    return d;
-  };
-  const int64_t k1 = sweeps / 2, k2 = sweeps - 1;
-  const double a = val(k1), b = val(k2);
-  double r = 0.0;
-  if (a > 0.0 && b > 0.0) r = std::pow(b / a, 1.0 / (double)(k2 - k1));
+  double s0 = 0.0, s1 = 0.0;
+  for (int k = 0; k < nb; ++k) {
+    s0 += hp[2 * k];
+    s1 += hp[2 * k + 1];
+  }
+  const double sN = (sweeps & 1) ? s1 : s0, sN1 = (sweeps & 1) ? s0 : s1;
+  double r = (sN1 > 0.0 && sN >= 0.0) ? std::sqrt(sN / sN1) : 0.0;
   if (!(r >= 0.0)) r = 0.0;
   if (r > 1.0) r = 1.0;
   if (rho) *rho = r;

@@ -211,6 +211,8 @@ cudaError_t launch_inductor_update(pg_grid *g, double h);
 cudaError_t launch_probe(pg_grid *g, const int64_t *probe_idx, int64_t n_probe, double *out);
 cudaError_t launch_reset_state(pg_grid *g, bool keep_base = false);
 cudaError_t launch_check_finite(pg_grid *g);
+int dnorm2_blocks(const pg_grid *g);
+cudaError_t launch_dnorm2(pg_grid *g, double *part);  // part[2 * blocks]: sum d V0^2, sum d V1^2 per block
 cudaError_t launch_gather_user(pg_grid *g, double *dst_user_order);
 cudaError_t launch_scatter_user(pg_grid *g, const double *src_user_order, double *dst_storage);
 int sweeps_per_launch(pg_grid *g, int method);

@@ -829,6 +829,39 @@ cudaError_t launch_rb_resident(pg_grid *g, double omega, double tol, int64_t max
   return cudaLaunchKernelEx(&cfg, k_rb_cluster, a);
 }
 
+// D-weighted squared 2-norms of both V buffers, sum_i d_i V_i^2 (d_i = 1 / invd_i,
+// real nodes only), one partial per block (summed on the host in block order:
+// deterministic for a fixed grid)
+__global__ void k_dnorm2(int64_t np, const double *invd, const double *V0, const double *V1, double *part) {
+  __shared__ double s0[256 / 32], s1[256 / 32];
+  double a = 0.0, b = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < np; i += (int64_t)gridDim.x * blockDim.x) {
+    const double id = invd[i];
+    if (id > 0.0) {
+      a += V0[i] * V0[i] / id;
+      b += V1[i] * V1[i] / id;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s0[threadIdx.x >> 5] = a;
+    s1[threadIdx.x >> 5] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double x = 0.0, y = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+      x += s0[k];
+      y += s1[k];
+    }
+    part[2 * blockIdx.x] = x;
+    part[2 * blockIdx.x + 1] = y;
+  }
+}
+
 __global__ void k_probe(const double *V0, const double *V1, const DevCtl *c, const int64_t *idx,
                         int64_t n, double *out) {
   const double *V = c->base ? V1 : V0;
@@ -1140,6 +1173,13 @@ cudaError_t launch_probe(pg_grid *g, const int64_t *probe_idx, int64_t n_probe, 
 
 cudaError_t launch_reset_state(pg_grid *g, bool keep_base) {
   k_reset_state<<<1, 1, 0, g->stream>>>(g->ctl, keep_base ? 1 : 0);
+  return cudaGetLastError();
+}
+
+int dnorm2_blocks(const pg_grid *g) { return grid_for(g->np, 256, g->num_sms); }
+
+cudaError_t launch_dnorm2(pg_grid *g, double *part) {
+  k_dnorm2<<<dnorm2_blocks(g), 256, 0, g->stream>>>(g->np, g->invd, g->V[0], g->V[1], part);
   return cudaGetLastError();
 }
 

@@ -1,7 +1,7 @@
 """Integrity of the full-size oracle goldens (-m "not gpu"): each file under
 tests/golden/fullsize_*.npz was written by tools/make_golden_fullsize.py from
 gridgen + oracle/ only; here its metadata is checked against the bench's
-workload (omega = bench.YOUNG_OMEGA, h and steps of the BASELINE config), the
+workload (omega = bench.OMEGA, h and steps of the BASELINE config), the
 sampled nodes against the generator's seeded recipe, and the stored record
 against Algorithm 1's stopping rule (line 8: the last sweep of every step is
 the first one below tol, with the paper's check after every sweep)."""
@@ -26,10 +26,12 @@ def test_golden_metadata_and_stopping_record(path):
     import make_golden_fullsize as mg
     z = np.load(path)
     job = str(z["job"])
-    cfg, steps, tol, srl, order = mg.JOBS[job]
+    cfg, steps, tol, srl, order, omega = mg.JOBS[job]
     assert int(z["config"]) == cfg and int(z["steps"]) == steps and float(z["tol"]) == tol
     assert str(z["series_rl"]) == srl and str(z["order"]) == order
-    assert float(z["omega"]) == bench.YOUNG_OMEGA[cfg] == mg.OMEGA[cfg]
+    assert float(z["omega"]) == omega
+    if job == f"c{cfg}" or job == f"c{cfg}_element":
+        assert omega == bench.OMEGA[cfg] == mg.OMEGA[cfg]          # the bench's omega
     c = gridgen.CONFIGS[cfg]
     assert float(z["h"]) == c["h"]
     V, sw, dt = z["V"], z["sweeps"], z["dtrace"]

@@ -14,7 +14,7 @@ cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 T = int(sys.argv[2]) if len(sys.argv) > 2 else 8
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 g = gridgen.config_grid(cfg)
-omega = bench.YOUNG_OMEGA.get(cfg, 1.9)
+omega = bench.OMEGA.get(cfg, 1.9)
 pinned = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
 pin = {k: pinned(getattr(g, k, None)) for k in ("gx", "gy", "gz", "cap", "lz", "pad_node", "pad_g", "pad_l")}
 s = g.sources

@@ -15,8 +15,8 @@ Stored per step: V at the sampled nodes (65 536 seeded random nodes plus the
 all-layer 3 x 3 columns around the 32 earliest-starting loads), the sweep
 count, and the stopping record (dtrace: the norm of the last two sweeps and
 of 4 more sweeps continued on a copy, for the every-F-sweeps stopping test of
-the GPU, R13).  omega is the bench's omega for that config (Young's
-estimate, R15, a literal here); tests read it from the golden.
+the GPU, R13).  omega is a literal of the job (the bench's omega
+for the plain config jobs, R15); tests read it from the golden.
 """
 from __future__ import annotations
 
@@ -33,9 +33,19 @@ sys.path.insert(0, ROOT)
 import gridgen  # noqa: E402
 from oracle import netlist, nodal, pwl  # noqa: E402
 
-# Young's omega of each config as bench.py uses it (pg_estimate_omega with 8000
-# Jacobi sweeps on the config's grid; R15, profiles/r2_probe_omega.log)
+# omega of each config as bench.py uses it (R15): the argmin of the
+# mean sweeps per time step over a grid of omega at / above Young's optimum
+# (tools/omega_scan.py, profiles/r2_omega_scan.log)
 OMEGA = {
+    1: 1.969,
+    2: 1.962,
+    3: 1.957,
+    4: 1.975,
+}
+# round-2 first pass: Young's optimum from the max-norm ratio of 8000 Jacobi
+# sweeps (pg_estimate_omega before the Rayleigh-quotient estimate); these
+# goldens are kept as further parity cases at another omega
+OMEGA_Y8K = {
     1: 1.9639132252348532,
     2: 1.9603462069765296,
     3: 1.9511469274691926,
@@ -43,12 +53,18 @@ OMEGA = {
 }
 
 JOBS = {
-    # name: (config, steps, tol, series_rl, order)
-    "c1": (1, 20, 1e-10, "node", "redblack"),
-    "c2": (2, 6, 1e-10, "node", "redblack"),
-    "c3_element": (3, 20, 1e-10, "element", "redblack"),
-    "c3_node_tight": (3, 20, 1e-13, "node", "natural"),
-    "c4": (4, 3, 1e-10, "node", "redblack"),
+    # name: (config, steps, tol, series_rl, order, omega)
+    "c1": (1, 20, 1e-10, "node", "redblack", OMEGA[1]),
+    "c2": (2, 6, 1e-10, "node", "redblack", OMEGA[2]),
+    "c3_element": (3, 20, 1e-10, "element", "redblack", OMEGA[3]),
+    "c4": (4, 3, 1e-10, "node", "redblack", OMEGA[4]),
+    "c1_young8k": (1, 20, 1e-10, "node", "redblack", OMEGA_Y8K[1]),
+    "c2_young8k": (2, 6, 1e-10, "node", "redblack", OMEGA_Y8K[2]),
+    "c3_element_young8k": (3, 20, 1e-10, "element", "redblack", OMEGA_Y8K[3]),
+    "c4_young8k": (4, 3, 1e-10, "node", "redblack", OMEGA_Y8K[4]),
+    # the paper's internal-node model at a tight tol on both sides (R20): omega
+    # only sets the speed of both iterations here
+    "c3_node_tight": (3, 20, 1e-13, "node", "natural", OMEGA_Y8K[3]),
 }
 
 
@@ -79,8 +95,7 @@ def main():
     ap.add_argument("--resume", action="store_true")
     ap.add_argument("--scratch", default="/tmp/pg_golden")
     a = ap.parse_args()
-    cfg, steps, tol, series_rl, order_name = JOBS[a.job]
-    omega = OMEGA[cfg]
+    cfg, steps, tol, series_rl, order_name, omega = JOBS[a.job]
     os.makedirs(a.scratch, exist_ok=True)
     ck = os.path.join(a.scratch, f"{a.job}.ckpt.npz")
     out = os.path.join(ROOT, "tests", "golden", f"fullsize_{a.job}.npz")
