@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <numeric>
@@ -48,7 +49,7 @@ using namespace pgb;
 namespace {
 
 // Device memory of the grids comes from a library-owned stream-ordered pool
-// per device (release threshold 8 GiB), so creating and destroying grids, the
+// per device (release threshold 48 GiB by default), so creating and destroying grids, the
 // per-call scratch of pg_transient and pg_set_sources do not map and unmap
 // device memory each time (cudaMalloc / cudaFree of large buffers took up to
 // ~200 ms now and then inside the end-to-end call).  Blocks are handed out
@@ -74,7 +75,14 @@ DevPool *pool_of(int dev) {
     pr.handleTypes = cudaMemHandleTypeNone;
     pr.location.type = cudaMemLocationTypeDevice;
     pr.location.id = dev;
-    uint64_t thr = 8ull << 30;
+    // release threshold: freed blocks up to this size stay mapped for the next
+    // grid (PGB200_POOL_GIB, default 48 GiB: a config-4-sized grid is ~11 GB,
+    // and re-mapping it for every end-to-end create cost ~0.4 s); an allocation
+    // the pool cannot serve trims it first (dalloc), so the cache never blocks
+    // this library's own allocations
+    uint64_t gib = 48;
+    if (const char *e = std::getenv("PGB200_POOL_GIB")) gib = std::strtoull(e, nullptr, 10);
+    uint64_t thr = gib << 30;
     if (cudaMemPoolCreate(&d.pool, &pr) != cudaSuccess ||
         cudaMemPoolSetAttribute(d.pool, cudaMemPoolAttrReleaseThreshold, &thr) != cudaSuccess ||
         cudaStreamCreateWithFlags(&d.s, cudaStreamNonBlocking) != cudaSuccess) {

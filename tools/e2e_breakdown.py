@@ -20,6 +20,8 @@ pin = {k: pinned(getattr(g, k, None)) for k in ("gx", "gy", "gz", "cap", "lz", "
 s = g.sources
 src = [pinned(a) for a in (s.node, s.ptr, s.t, s.i)]
 out = torch.empty(g.n, dtype=torch.float64).pin_memory().numpy()
+# as in bench.py: the device-resident grid of the timed region stays alive
+keep = P.Grid.from_mesh_grid(g, device=True) if os.environ.get("E2E_KEEP") else None
 for rep in range(reps):
     torch.cuda.synchronize(); t0 = time.perf_counter()
     H = P.Grid.mesh(g.layers, g.ny, g.nx, pin["gx"], pin["gy"], pin["gz"], pin["cap"], pin["pad_node"], pin["pad_g"],
