@@ -76,6 +76,9 @@ def parse():
     ap.add_argument("--omega", type=float, default=None)
     ap.add_argument("--estimate-omega", action="store_true",
                     help="estimate Young's omega on the grid at run time instead of the recorded value")
+    ap.add_argument("--tune-omega", action="store_true",
+                    help="tune omega on the grid at run time (pg_tune_omega: omega_b and 7 candidates "
+                         "4e-4 apart, first 8 time steps) instead of the recorded value")
     ap.add_argument("--tol", type=float, default=1e-10)
     ap.add_argument("--method", default="rbsor", choices=["rbsor", "jacobi"])
     ap.add_argument("--slabs", type=int, default=1,
@@ -180,6 +183,8 @@ def omega_of(args, cfg):
         return args.omega, "--omega"
     if args.method == "jacobi":
         return FALLBACK_OMEGA, "fixed (Jacobi weight)"
+    if args.tune_omega:
+        return None, "tuned at run time (pg_tune_omega: omega_b + k 4e-4, k < 8, first 8 time steps)"
     if cfg in OMEGA and not args.estimate_omega:
         return OMEGA[cfg], ("recorded: argmin of sweeps per time step over omega >= Young's omega_b "
                             "(pg_estimate_omega, Rayleigh quotient of 8000 Jacobi sweeps) on this grid "
@@ -374,12 +379,14 @@ def run_b200(args):
             q.set_option(k, int(v))
     t_om = time.perf_counter()
     omega, omega_src = omega_of(args, cfg)
-    if omega is None:
+    if omega is None and args.tune_omega and grp is None:
+        omega, _ = G.tune_omega(g.h, steps=8, tol=tol, n=8, d_omega=4e-4)
+    elif omega is None:
         _, omega = G.estimate_omega(g.h, 8000)
-        if world > 1:
-            t = torch.tensor([omega], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            omega = float(t.item())
+    if world > 1:
+        t = torch.tensor([omega], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        omega = float(t.item())
     t_om = time.perf_counter() - t_om
 
     state = {"done": 0}

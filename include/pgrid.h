@@ -328,6 +328,17 @@ PG_API int pg_dc(pg_grid *g, double t, double tol, double omega, int method, int
  * pg_set_voltages.                                                        */
 PG_API int pg_estimate_omega(pg_grid *g, double h, int64_t sweeps, double *rho, double *omega_opt);
 
+/* Relaxation factor tuned on the grid's own transient: omega_b from
+ * pg_estimate_omega (2000 sweeps), then n_cand candidates omega_b + k d_omega
+ * (k = 0 .. n_cand-1, capped at 1.999; Young: overestimating omega_b costs
+ * little, underestimating it a lot) each run for the first `steps` time steps
+ * from x(0) to tol; *omega_out = the candidate with the fewest sweeps
+ * (sweeps_out, nullable host int64[n_cand], receives every candidate's total;
+ * INT64_MAX if it hit 1e6 sweeps in a step).  Leaves the grid at x(0) with
+ * zero inductor currents.  1 <= n_cand <= 64, d_omega >= 0, tol > 0.      */
+PG_API int pg_tune_omega(pg_grid *g, double h, int64_t steps, double tol, int64_t n_cand, double d_omega,
+                         double *omega_out, int64_t *sweeps_out);
+
 /* Number of nodes / dimensions (layers, ny, nx are 0 for CSR grids). */
 PG_API int pg_info(const pg_grid *g, int64_t *n, int32_t *layers, int32_t *ny, int32_t *nx,
                    int32_t *n_colors);

@@ -50,6 +50,7 @@ SIGNATURES = {
                          ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),
     "pg_destroy": (None, [_vp]),
     "pg_estimate_omega": (_c_int, [_vp, _dbl, _i64, ctypes.POINTER(_dbl), ctypes.POINTER(_dbl)]),
+    "pg_tune_omega": (_c_int, [_vp, _dbl, _i64, _dbl, _i64, _dbl, ctypes.POINTER(_dbl), _vp]),
     "pg_dc": (_c_int, [_vp, _dbl, _dbl, _dbl, _c_int, _i64, ctypes.POINTER(PgStats)]),
     "pg_set_slab": (_c_int, [_vp, _i32, _i32, _i32]),
     "pg_nccl_unique_id": (_c_int, [_vp]),

@@ -222,6 +222,15 @@ class Grid:
                                             ctypes.byref(om)))
         return rho.value, om.value
 
+    def tune_omega(self, h, steps=8, tol=1e-10, n=6, d_omega=4e-4):
+        """(omega, sweeps per candidate) from pg_tune_omega: Young's omega_b and
+        n - 1 candidates above it, each run for the first `steps` time steps."""
+        om = ctypes.c_double()
+        sw = np.zeros(int(n), dtype=np.int64)
+        L.check(self._lib.pg_tune_omega(self._h, float(h), int(steps), float(tol), int(n), float(d_omega),
+                                        ctypes.byref(om), sw.ctypes.data))
+        return om.value, sw
+
     def dc(self, t=0.0, tol=1e-10, omega=1.9, method="rbsor", max_sweeps=1000000,
            raise_on_noconv=True):
         """DC operating point G v = G0 Vdd - i(t) (pg_dc); returns the stats.

@@ -768,6 +768,47 @@ PG_API int pg_estimate_omega(pg_grid *g, double h, int64_t sweeps, double *rho, 
   return PG_OK;
 }
 
+PG_API int pg_tune_omega(pg_grid *g, double h, int64_t steps, double tol, int64_t n_cand, double d_omega,
+                         double *omega_out, int64_t *sweeps_out) {
+  REQUIRE(g != nullptr && omega_out != nullptr, "grid / omega_out is NULL");
+  REQUIRE(!g->slab, "slab grids are tuned through their single-grid twin");
+  REQUIRE(h > 0.0 && std::isfinite(h), "h must be finite and > 0");
+  REQUIRE(steps >= 1 && n_cand >= 1 && n_cand <= 64, "steps >= 1 and 1 <= n_cand <= 64");
+  REQUIRE(tol > 0.0 && d_omega >= 0.0 && std::isfinite(d_omega), "tol > 0 and d_omega >= 0");
+  double rho = 0.0, omega_b = 1.0;
+  int rc;
+  if ((rc = pg_estimate_omega(g, h, 2000, &rho, &omega_b))) return rc;
+  // Young: the SOR convergence rate falls steeply below omega_b and only
+  // linearly above it (and omega_b itself has a Jordan block), so candidates
+  // start at omega_b and go up; the first candidate with the fewest sweeps
+  // over the first `steps` time steps from x(0) wins
+  double best = omega_b;
+  int64_t best_sw = -1;
+  for (int64_t k = 0; k < n_cand; ++k) {
+    const double om = std::min(omega_b + (double)k * d_omega, 1.999);
+    pg_stats st;
+    rc = pg_transient(g, h, steps, tol, om, PG_METHOD_RBSOR, 1000000, 0, nullptr, nullptr, PG_MEM_HOST, nullptr,
+                      &st);
+    if (rc != PG_OK && rc != PG_ENOCONV) return rc;
+    const int64_t sw = rc == PG_OK ? st.sweeps_total : INT64_MAX;
+    if (sweeps_out) sweeps_out[k] = sw;
+    if (best_sw < 0 || sw < best_sw) {
+      best_sw = sw;
+      best = om;
+    }
+  }
+  // leave the grid at x(0) (as after creation / pg_set_voltages)
+  CK(cudaMemcpyAsync(g->V[0], g->x0, sizeof(double) * g->np, cudaMemcpyDeviceToDevice, g->stream));
+  CK(launch_reset_state(g));
+  if (g->iz) CK(cudaMemsetAsync(g->iz, 0, sizeof(double) * g->np, g->stream));
+  if (g->pad_i) CK(cudaMemsetAsync(g->pad_i, 0, sizeof(double) * g->npad, g->stream));
+  CK(cudaStreamSynchronize(g->stream));
+  g->traj_steps = 0;
+  g->traj_h = 0.0;
+  *omega_out = best;
+  return PG_OK;
+}
+
 }  // extern "C"
 
 namespace pgb {

@@ -94,3 +94,27 @@ def test_estimate_omega_matches_dense_spectrum(pgb, shape, h):
     r2 = G.transient(h, 3, tol=1e-12, omega=om, max_sweeps=1_000_000)
     G.close()
     assert r2.stats.sweeps_total < r1.stats.sweeps_total
+
+
+def test_tune_omega_picks_fewest_sweeps_and_resets(pgb):
+    # pg_tune_omega: candidate 0 is Young's omega_b, the pick is the candidate
+    # with the fewest sweeps over the first steps, and the grid is left at x(0)
+    g = gridgen.config_grid(1, dims=(2, 96, 128), steps=6)
+    G = pgb.Grid.from_mesh_grid(g, device=True)
+    G.set_option("resident", 0)
+    rho, omb = G.estimate_omega(g.h, 2000)
+    om, sw = G.tune_omega(g.h, steps=4, tol=1e-10, n=5, d_omega=0.002)
+    cands = [min(omb + k * 0.002, 1.999) for k in range(5)]
+    assert min(abs(om - c) for c in cands) < 1e-15
+    assert sw[cands.index(min(cands, key=lambda c: abs(c - om)))] == sw.min()
+    r0 = G.transient(g.h, 4, tol=1e-10, omega=cands[0], max_sweeps=200000)
+    assert int(r0.stats.sweeps_total) == sw[0]
+    # left at x(0): a continuation from here equals a fresh transient
+    G2 = pgb.Grid.from_mesh_grid(g, device=True)
+    G2.set_option("resident", 0)
+    G2.tune_omega(g.h, steps=2, tol=1e-10, n=2, d_omega=0.002)
+    a = G2.transient(g.h, 3, tol=1e-10, omega=om, max_sweeps=200000, cont=True, probes=np.arange(g.n))
+    b = G.transient(g.h, 3, tol=1e-10, omega=om, max_sweeps=200000, probes=np.arange(g.n))
+    np.testing.assert_array_equal(a.probes, b.probes)
+    G.close()
+    G2.close()
