@@ -622,7 +622,7 @@ PG_API int pg_set_sources(pg_grid *g, int64_t n_src, const int64_t *node, const 
       set_error("pg_set_sources: " + err);
       return rc;
     }
-    REQUIRE(!(bad & 1), "ptr[0] must be 0");
+    REQUIRE(!(bad & 1), "ptr[0] must be 0 and every ptr[k] in [0, ptr[n_src]]");
     REQUIRE(!(bad & 2), "every source needs at least one breakpoint");
     REQUIRE(!(bad & 4), "source node index out of range");
     REQUIRE(!(bad & 8), "PWL breakpoint times must be strictly increasing");

@@ -26,7 +26,7 @@ namespace pgb {
 namespace {
 
 enum : int32_t {
-  kBadPtr0 = 1,       // ptr[0] != 0
+  kBadPtr0 = 1,       // ptr[0] != 0 or an offset outside [0, npts]
   kBadCount = 2,      // a source with no breakpoint
   kBadNode = 4,       // node index out of range
   kBadOrder = 8,      // breakpoint times not strictly increasing
@@ -34,6 +34,19 @@ enum : int32_t {
 };
 
 __device__ __forceinline__ bool finite(double x) { return fabs(x) <= 1.7976931348623157e308; }
+
+// the breakpoint offsets alone first (0 = ptr[0] < ptr[1] < ... <= npts), so
+// that the next kernel never reads outside t / v
+__global__ void k_src_ptr_check(int64_t n_src, const int64_t *ptr, int64_t npts, int32_t *err) {
+  int32_t e = 0;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n_src; k += (int64_t)gridDim.x * blockDim.x) {
+    if (k == 0 && ptr[0] != 0) e |= kBadPtr0;
+    const int64_t a = ptr[k], b = ptr[k + 1];
+    if (!(b > a)) e |= kBadCount;
+    if (a < 0 || b > npts) e |= kBadPtr0;
+  }
+  if (e) atomicOr(err, e);
+}
 
 // validation + storage index of every source (key) and its input position (value)
 __global__ void k_src_keys(int64_t n_src, const int64_t *node, const int64_t *ptr, const double *t,
@@ -188,6 +201,17 @@ int build_sources_device(pg_grid *g, int64_t n_src, const int64_t *node, const i
   SCK(cudaMallocAsync(&gidx, nb, st), "alloc");
   SCK(cudaMallocAsync(&d_err, sizeof(int32_t), st), "alloc");
   SCK(cudaMemsetAsync(d_err, 0, sizeof(int32_t), st), "memset");
+  k_src_ptr_check<<<grid, B, 0, st>>>(n_src, ptr, npts, d_err);
+  SCK(cudaGetLastError(), "k_src_ptr_check");
+  int32_t p_err = 0;
+  SCK(cudaMemcpyAsync(&p_err, d_err, sizeof(int32_t), cudaMemcpyDeviceToHost, st), "copy");
+  SCK(cudaStreamSynchronize(st), "sync");
+  if (p_err) {
+    cleanup();
+    cudaStreamSynchronize(st);
+    *bad_bits = p_err;
+    return PG_OK;
+  }
   k_src_keys<<<grid, B, 0, st>>>(n_src, node, ptr, t, v, g->n, g->kind == 0, g->md, g->iperm, key, pos, len, d_err);
   SCK(cudaGetLastError(), "k_src_keys");
   int32_t h_err = 0;

@@ -168,6 +168,7 @@ def test_bad_sources_rejected_and_store_kept(pgb):
         (np.array([3, 4]), np.array([0, 1, 1]), np.array([0.0]), np.array([1e-3])),     # empty source
         (np.array([g.n]), np.array([0, 1]), np.array([0.0]), np.array([1e-3])),         # node out of range
         (np.array([3]), np.array([0, 2]), np.array([1.0, 1.0]), np.array([0.0, 1.0])),  # not increasing
+        (np.array([3, 4]), np.array([0, 10**6, 3]), np.zeros(3), np.zeros(3)),         # offset past the end
     ]
     for args in bad:
         with pytest.raises(pgb.PgError):
