@@ -74,7 +74,9 @@ enum {
  *   pad_node[n_pads], pad_g[n_pads]: pad branches from node to the Vdd source
  *          node, conductance 1/R (> 0); pad_l[n_pads] series inductance or NULL.
  *          A node may carry several pads.
- *   n = layers * ny * nx.  layers, ny, nx >= 1.
+ *   n = layers * ny * nx.  1 <= layers <= 256, ny, nx >= 1.  Meshes of up to
+ *   8 layers are swept by the streaming strip kernels; taller stacks by the
+ *   per-colour sweep (option "colour"; no slab groups).
  * Every node must have a path to a pad (Lemma 1 / topological assumption 3);
  * this is not checked here (an isolated node without capacitance makes the
  * diagonal zero and is reported as PG_EINVAL by pg_transient).            */
@@ -153,6 +155,11 @@ PG_API int pg_set_stream(pg_grid *g, void *stream);
  *   "stages" shared-memory ring stages S of the mesh sweep (0: auto =
  *            D (F-1) + 6); a (F, S, D) variant that is not compiled falls
  *            back to the default S, then to smaller F
+ *   "colour" 1: mesh sweeps run colour by colour, two launches of
+ *            k_rb_colour_mesh per sweep (one thread per node of the colour;
+ *            same iterates as the streaming sweep bit for bit,
+ *            pg_stats.sweeps_per_launch = 1); 0 (default): only meshes taller
+ *            than 8 layers use it
  *   "timing" 1: time every sweep launch with CUDA events (stats.sweep_ms);
  *            adds one host synchronisation per time step                  */
 PG_API int pg_set_option(pg_grid *g, const char *key, int64_t value);

@@ -347,7 +347,8 @@ PG_API int pg_create_mesh(int32_t layers, int32_t ny, int32_t nx, const double *
   if (out) *out = nullptr;
   REQUIRE(out != nullptr, "out is NULL");
   REQUIRE(layers >= 1 && ny >= 1 && nx >= 1, "layers, ny, nx must be >= 1");
-  REQUIRE(layers <= kMaxLayers, "at most 8 layers per mesh grid (split taller stacks)");
+  REQUIRE(layers <= kMaxMeshLayers, "at most 256 layers per mesh grid");
+  REQUIRE((int64_t)layers * ny < (int64_t)1 << 31, "layers * ny must be < 2^31");
   REQUIRE(mem == PG_MEM_HOST || mem == PG_MEM_DEVICE, "mem must be PG_MEM_HOST or PG_MEM_DEVICE");
   REQUIRE(gx && gy && gz && cap, "gx, gy, gz, cap are required");
   REQUIRE(n_pads >= 0 && (n_pads == 0 || (pad_node && pad_g)), "bad pad arrays");
@@ -532,6 +533,8 @@ PG_API int pg_set_option(pg_grid *g, const char *key, int64_t value) {
       set_error("re-encoding the slab halo tensor maps failed");
       return PG_ECUDA;
     }
+  } else if (k == "colour") {
+    g->colour = value != 0;
   } else if (k == "csr_stage") {
     g->csr_stage = value != 0;
   } else if (k == "graph") {

@@ -469,6 +469,10 @@ PG_API int pg_set_slab(pg_grid *g, int32_t y_begin, int32_t y_end, int32_t y0_pa
     return PG_ESTATE;
   }
   REQ(0 <= y_begin && y_begin < y_end && y_end <= g->md.NY, "need 0 <= y_begin < y_end <= ny");
+  if (g->md.L > kMaxLayers) {
+    set_error("slab grids need the streaming sweep: at most 8 layers");
+    return PG_ESTATE;
+  }
   g->slab = true;
   g->y_begin = y_begin;
   g->y_end = y_end;

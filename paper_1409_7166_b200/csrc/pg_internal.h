@@ -49,6 +49,8 @@ constexpr int kRhsTile = 2048;  // storage elements per tile of the fused RHS ke
 constexpr int kCsrR = 512;
 constexpr int kCsrE = 3072;
 constexpr int kMaxLayers = 8;   // CTA of the mesh sweep = 32 lanes x L warps
+// taller meshes (up to kMaxMeshLayers) use the per-colour sweep k_rb_colour_mesh
+constexpr int kMaxMeshLayers = 256;
 
 // Mesh storage layout ("parity-split rows"), DESIGN.md §7.  Layer-major
 // [L][NY][NXP] with row pitch NXP (a multiple of 64); inside a row the even
@@ -186,6 +188,8 @@ struct pg_grid {
   int l2promo = 256;                   // option "l2promo": TMA L2 promotion bytes (0, 64, 128, 256)
   int pdl = 1;                         // option "pdl": programmatic dependent launch of consecutive sweeps
   int csr_stage = 1;                   // option "csr_stage": bulk-copy staged CSR sweep (k_csr_sweep_staged)
+  int colour = 0;                      // option "colour": per-colour mesh sweep (k_rb_colour_mesh) for every
+                                       // layer count (default: only meshes taller than kMaxLayers)
   bool pdl_ok = false;                 // set by run_transient: single grid, no exchange between launches
   bool group_active = false;           // inside pg_group_transient (peer exchange armed)
   cudaGraphExec_t batch_exec = nullptr;  // captured batch of `batch` full sweep launches
@@ -216,6 +220,9 @@ cudaError_t launch_dnorm2(pg_grid *g, double *part);  // part[2 * blocks]: sum d
 cudaError_t launch_gather_user(pg_grid *g, double *dst_user_order);
 cudaError_t launch_scatter_user(pg_grid *g, const double *src_user_order, double *dst_storage);
 int sweeps_per_launch(pg_grid *g, int method);
+// mesh grids swept colour by colour (two launches per sweep): taller than
+// kMaxLayers or option "colour"
+bool colour_sweep(const pg_grid *g);
 // temporally blocked red-black sweep (pg_sweep_fused.cu)
 bool tma_available(pg_grid *g);
 bool encode_halo_maps(pg_grid *g);

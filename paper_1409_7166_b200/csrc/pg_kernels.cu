@@ -7,6 +7,7 @@
 //                      pass (Eq. (13) in red-black numbering + Eq. (15)), fused
 //                      warp-shuffle max|dV| reduction                  (line 7-8)
 //   k_jacobi_mesh      weighted Jacobi sweep (comparison)
+//   k_rb_colour_mesh   red-black SOR one colour per launch (meshes of any layer count)
 //   k_csr_sweep        multi-colour Gauss-Seidel/SOR on the CSR store (irregular grids)
 //   k_ind_update_*     companion inductor currents i(t+h) = g_e v + alpha i(t)  (Eq. (10))
 //   k_step_end         device-side bookkeeping of the step (sweep count, buffer parity)
@@ -54,6 +55,15 @@ __device__ __forceinline__ bool sweep_skip(DevCtl *c, int j, double tol, bool fi
     }
   }
   return false;
+}
+
+// max-reduce a CTA's |dV| into the launch's norm slot (bit pattern of a
+// non-negative double orders like its value).  The slot only grows, so a CTA
+// whose maximum does not exceed the value it reads skips the atomic: the
+// same-address atomics of thousands of CTAs serialise in L2.
+__device__ __forceinline__ void norm_max(unsigned long long *slot, double m) {
+  const unsigned long long v = d2u(m);
+  if (v > *(volatile unsigned long long *)slot) atomicMax(slot, v);
 }
 
 __device__ __forceinline__ void zero_next_slot(DevCtl *c, int j, bool first_of_sweep) {
@@ -130,7 +140,107 @@ __global__ void __launch_bounds__(256) k_jacobi_mesh(JacobiArgs a) {
   if (threadIdx.x == 0) {
     double m = 0.0;
     for (int k = 0; k < (int)(blockDim.x >> 5); ++k) m = fmax(m, wmax[k]);
-    atomicMax(&a.ctl->dmax[a.launch_idx & (kRing - 1)], d2u(m));
+    norm_max(&a.ctl->dmax[a.launch_idx & (kRing - 1)], m);
+  }
+}
+
+// ------------------------------------------- red-black SOR, one colour per launch
+// Mesh sweep for any layer count (meshes taller than the strip kernels'
+// kMaxLayers, or option "colour"): one sweep of Eq. (13) + (15) in the
+// red-black numbering (R12) is two launches, colour 0 (red,
+// (l + y + x) even) then colour 1.  In the parity-split layout the nodes of one
+// colour in a row are one half row, x parity (colour + l + y) & 1, so thread p
+// of a row updates storage element xpar * HP + p: coalesced, no idle lanes.
+// Ping-pong like the streaming sweep: colour 0 reads iterate k - 1 from V[par]
+// and writes its nodes to V[!par]; colour 1 reads its own old value from V[par]
+// and its neighbours (all red: the mesh is bipartite) from V[!par].  Same
+// operand order as upd_c, absent neighbours with g = 0 and V = 0 (what the
+// TMA zero fill gives the streaming kernels), so the iterates equal theirs bit
+// for bit.  max|dV| of both colours goes to the launch's norm slot.
+struct ColourArgs {
+  MeshDims d;
+  const double *gx, *gy, *gz, *b, *invd;
+  double *V0, *V1;
+  double omega, tol;
+  int32_t launch_idx, colour;
+  DevCtl *ctl;
+};
+
+__global__ void __launch_bounds__(128) k_rb_colour_mesh(ColourArgs a) {
+  __shared__ double wmax[4];
+  a.launch_idx += *(volatile int32_t *)&a.ctl->jbase;
+  const bool first = a.colour == 0;
+  if (sweep_skip(a.ctl, a.launch_idx, a.tol, first)) return;
+  zero_next_slot(a.ctl, a.launch_idx, first);
+  const MeshDims d = a.d;
+  const int par = (*(volatile int32_t *)&a.ctl->base + a.launch_idx) & 1;
+  const double *Vold = par ? a.V1 : a.V0;
+  double *Vnew = par ? a.V0 : a.V1;
+  const double *Vnb = first ? Vold : Vnew;  // the other colour's latest values
+  const double w = a.omega;
+  double dmax = 0.0;
+  // two column pairs per thread, p0 = 2t and p0 + 1: 16-byte loads of every
+  // array at the node's own positions (HP is even, so p0 + 1 < HP and every
+  // pair of positions is 16-byte aligned).  Padding nodes (x >= NX) have
+  // g = 0, 1/d = 0, b = 0 and V = 0 and stay 0, so they need no mask.
+  const int p0 = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+  if (p0 < d.HP) {
+    for (int r = blockIdx.y; r < d.L * d.NY; r += gridDim.y) {
+      const int l = r / d.NY, y = r - l * d.NY;
+      const int xpar = (a.colour + l + y) & 1;
+      const int64_t base = (int64_t)l * d.layer_stride + (int64_t)y * d.NXP;
+      const int64_t i = base + xpar * d.HP + p0;
+      // own pair = columns (2p, 2p + 1); "other" = the x neighbour outside it:
+      // odd nodes (xpar 1): own = even column p, other = even column p + 1;
+      // even nodes: own = odd column p, other = odd column p - 1
+      const int64_t iown = xpar ? base + p0 : base + d.HP + p0;
+      const double2 gxo = ld2(a.gx + base + p0);      // link of pair p (gxOwn)
+      const double2 vo = ld2(Vnb + iown);
+      double2 gxt, vt;                               // gxOth, Voth of the two nodes
+      if (xpar) {
+        gxt = ld2(a.gx + base + d.HP + p0);
+        vt.x = vo.y;
+        vt.y = p0 + 2 < d.HP ? __ldg(Vnb + base + p0 + 2) : 0.0;
+      } else {
+        const double2 g2 = ld2(a.gx + base + d.HP + p0);
+        gxt.x = p0 > 0 ? __ldg(a.gx + base + d.HP + p0 - 1) : 0.0;
+        gxt.y = g2.x;
+        vt.x = p0 > 0 ? __ldg(Vnb + base + d.HP + p0 - 1) : 0.0;
+        vt.y = vo.x;
+      }
+      const bool hN = y > 0, hS = y + 1 < d.NY, hU = l + 1 < d.L, hD = l > 0;
+      const double2 z2 = make_double2(0.0, 0.0);
+      const double2 gyN = hN ? ld2(a.gy + i - d.NXP) : z2, VN = hN ? ld2(Vnb + i - d.NXP) : z2;
+      const double2 gyS = ld2(a.gy + i), VS = hS ? ld2(Vnb + i + d.NXP) : z2;
+      const double2 gzU = ld2(a.gz + i), VU = hU ? ld2(Vnb + i + d.layer_stride) : z2;
+      const double2 gzD = hD ? ld2(a.gz + i - d.layer_stride) : z2;
+      const double2 VD = hD ? ld2(Vnb + i - d.layer_stride) : z2;
+      const double2 Vc = ld2(Vold + i), bb = ld2(a.b + i), id = ld2(a.invd + i);
+      auto upd = [&](double gxOwn, double Vown, double gxOth, double Voth, double gn, double vn_, double gs,
+                     double vs, double gu, double vu, double gd, double vd, double b, double idd, double vc) {
+        double s1 = fma(gxOwn, Vown, b);
+        s1 = fma(gxOth, Voth, s1);
+        s1 = fma(gn, vn_, s1);
+        double s2 = gs * vs;
+        s2 = fma(gu, vu, s2);
+        s2 = fma(gd, vd, s2);
+        return fma(w, (s1 + s2) * idd - vc, vc);
+      };
+      const double n0 = upd(gxo.x, vo.x, gxt.x, vt.x, gyN.x, VN.x, gyS.x, VS.x, gzU.x, VU.x, gzD.x, VD.x, bb.x,
+                            id.x, Vc.x);
+      const double n1 = upd(gxo.y, vo.y, gxt.y, vt.y, gyN.y, VN.y, gyS.y, VS.y, gzU.y, VU.y, gzD.y, VD.y, bb.y,
+                            id.y, Vc.y);
+      st2(Vnew + i, n0, n1);
+      dmax = fmax(dmax, fmax(fabs(n0 - Vc.x), fabs(n1 - Vc.y)));  // NaN / Inf: the RHS kernel's check of V(t)
+    }
+  }
+  dmax = warp_max(dmax);
+  if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = dmax;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) m = fmax(m, wmax[k]);
+    norm_max(&a.ctl->dmax[a.launch_idx & (kRing - 1)], m);
   }
 }
 
@@ -191,7 +301,7 @@ __global__ void __launch_bounds__(256) k_csr_sweep(CsrArgs a) {
   if (threadIdx.x == 0) {
     double m = 0.0;
     for (int k = 0; k < (int)(blockDim.x >> 5); ++k) m = fmax(m, wmax[k]);
-    atomicMax(&a.ctl->dmax[a.launch_idx & (kRing - 1)], d2u(m));
+    norm_max(&a.ctl->dmax[a.launch_idx & (kRing - 1)], m);
   }
 }
 
@@ -220,7 +330,7 @@ __global__ void __launch_bounds__(256) k_csr_jacobi(CsrArgs a) {
   if (threadIdx.x == 0) {
     double m = 0.0;
     for (int k = 0; k < (int)(blockDim.x >> 5); ++k) m = fmax(m, wmax[k]);
-    atomicMax(&a.ctl->dmax[a.launch_idx & (kRing - 1)], d2u(m));
+    norm_max(&a.ctl->dmax[a.launch_idx & (kRing - 1)], m);
   }
 }
 
@@ -366,7 +476,7 @@ __global__ void __launch_bounds__(kCsrT, 2) k_csr_sweep_staged(CsrArgs a) {
   if (tid == 0) {
     double m = 0.0;
     for (int k = 0; k < kCsrT / 32; ++k) m = fmax(m, wmax[k]);
-    atomicMax(&a.ctl->dmax[a.launch_idx & (kRing - 1)], d2u(m));
+    norm_max(&a.ctl->dmax[a.launch_idx & (kRing - 1)], m);
   }
 }
 
@@ -967,8 +1077,11 @@ static FusedCfg fused_cfg_for(const pg_grid *g, int fuse) {
   return {1, 6, 3, 32};
 }
 
+bool colour_sweep(const pg_grid *g) { return g->kind == 0 && !g->slab && (g->colour || g->md.L > kMaxLayers); }
+
 int sweeps_per_launch(pg_grid *g, int method) {
   if (resident_ok(g, method)) return 1;  // convergence tested after every sweep
+  if (colour_sweep(g)) return 1;
   return (g->kind == 0 && method == PG_METHOD_RBSOR) ? fused_cfg(g).F : 1;
 }
 
@@ -1070,6 +1183,23 @@ std::vector<int64_t> rhs_tile_starts(const std::vector<int64_t> &group_node, int
 cudaError_t launch_sweep(pg_grid *g, int method, double omega, double tol, int j, int nsweeps,
                          int64_t *launches) {
   if (g->kind == 0) {
+    if (method == PG_METHOD_RBSOR && colour_sweep(g)) {
+      ColourArgs a;
+      a.d = g->md;
+      a.gx = g->gx; a.gy = g->gy; a.gz = g->gze; a.b = g->b; a.invd = g->invd;
+      a.V0 = g->V[0];
+      a.V1 = g->V[1];
+      a.omega = omega; a.tol = tol; a.ctl = g->ctl; a.launch_idx = j;
+      const int bx = (g->md.HP / 2 + 127) / 128;
+      const int64_t rows = (int64_t)g->md.L * g->md.NY;
+      const int by = (int)std::min<int64_t>(rows, std::max<int64_t>(1, (int64_t)g->num_sms * 16 / bx));
+      for (int c = 0; c < 2; ++c) {
+        a.colour = c;
+        k_rb_colour_mesh<<<dim3(bx, by), 128, 0, g->stream>>>(a);
+      }
+      ++*launches;
+      return cudaGetLastError();
+    }
     if (method == PG_METHOD_RBSOR) {
       if (!tma_available(g)) return cudaErrorNotSupported;
       const FusedCfg c = fused_cfg(g);
