@@ -147,7 +147,8 @@ PG_API int pg_set_stream(pg_grid *g, void *stream);
  *   "l2promo" L2 promotion of the sweep's TMA loads in bytes: 0, 64, 128,
  *            256 (default 256)
  *   "graph"  1 (default): replay full batches of sweep launches from a captured
- *            CUDA graph (single grids, option "timing" off); 0: plain launches
+ *            CUDA graph (single grids, and slab groups whose exchange is
+ *            capturable or fused into the sweep); 0: plain launches
  *   "rows"   rows per CTA of the mesh sweep (0: auto)
  *   "width"  column pairs per strip of the mesh sweep: 32 (one warp per layer
  *            row) or 64 (two warps; halves the x-halo share, needs 2x shared
@@ -160,8 +161,9 @@ PG_API int pg_set_stream(pg_grid *g, void *stream);
  *            same iterates as the streaming sweep bit for bit,
  *            pg_stats.sweeps_per_launch = 1); 0 (default): only meshes taller
  *            than 8 layers use it
- *   "timing" 1: time every sweep launch with CUDA events (stats.sweep_ms);
- *            adds one host synchronisation per time step                  */
+ *   "timing" 1: an event pair around every time step's sweep launches
+ *            (stats.sweep_ms, stats.sweep_launches), read after the call: no
+ *            extra synchronisation, graphs and PDL stay on                  */
 PG_API int pg_set_option(pg_grid *g, const char *key, int64_t value);
 
 typedef struct {
