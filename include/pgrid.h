@@ -145,7 +145,8 @@ PG_API int pg_set_stream(pg_grid *g, void *stream);
  *            l2first = 63 (stream the reads, keep the freshly written V for
  *            the next launch), larger meshes 0 / 0
  *   "l2promo" L2 promotion of the sweep's TMA loads in bytes: 0, 64, 128,
- *            256 (default 256)
+ *            256 (default 128: +0.6-1.3 % over 256 on configs 1, 3, 4,
+ *            profiles/r2_l2promo_ab.txt)
  *   "graph"  1 (default): replay full batches of sweep launches from a captured
  *            CUDA graph (single grids, and slab groups whose exchange is
  *            capturable or fused into the sweep); 0: plain launches

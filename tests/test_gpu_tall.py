@@ -114,3 +114,20 @@ def test_tall_mesh_limits(pgb):
     g = mk(257, 1, 2, seed=1)
     with pytest.raises(pgb.PgError):
         pgb.Grid.from_mesh_grid(g)
+
+
+def test_tall_mesh_dc_matches_dense_solve(pgb):
+    # DC (A = G, §II-A) on a 12-layer mesh through the per-colour sweep
+    from oracle import dense, netlist, pwl
+    g = gridgen.mesh_grid(12, 5, 6, seed=9, pad_pitch=3, src_frac=0.5, h=10e-12, src_start=5e-12,
+                          src_width=40e-12)
+    t = 20e-12
+    G = pgb.Grid.from_mesh_grid(g)
+    G.set_option("resident", 0)
+    G.dc(t=t, tol=1e-15, omega=1.7, max_sweeps=2_000_000)
+    V = G.voltages()
+    G.close()
+    nl = netlist.from_mesh(g)
+    Vd = dense.dc_solve(nl, pwl.node_currents(nl, t))
+    assert np.abs(Vd - 1.0).max() > 1e-6
+    np.testing.assert_allclose(V, Vd, rtol=0, atol=1e-9)
