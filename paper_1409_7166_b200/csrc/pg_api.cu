@@ -744,6 +744,7 @@ PG_API int pg_estimate_omega(pg_grid *g, double h, int64_t sweeps, double *rho, 
   // successive norms, and it is not fooled by the +-rho pair of the 2-cyclic
   // (red-black) spectrum.  Young: omega_opt = 2 / (1 + sqrt(1 - rho^2)) for the
   // consistently ordered red-black numbering (§IV-D refers to Young).
+  g->setup_ok = false;
   CK(launch_setup(g, h));
   CK(cudaMemsetAsync(g->b, 0, sizeof(double) * g->np, st));
   CK(cudaMemcpyAsync(g->V[0], g->x0, sizeof(double) * g->np, cudaMemcpyDeviceToDevice, st));
@@ -973,8 +974,12 @@ int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, d
     if (!cont && q->iz) CK(cudaMemsetAsync(q->iz, 0, sizeof(double) * q->np, st));
     if (!cont && q->pad_i) CK(cudaMemsetAsync(q->pad_i, 0, sizeof(double) * q->npad, st));
     CK(launch_reset_state(q, cont));
-    CK(launch_setup(q, h));
-    launches += 4;
+    if (!(q->setup_ok && q->setup_h == h)) {  // h = +inf (DC) is a setup of its own
+      q->setup_ok = false;
+      CK(launch_setup(q, h));
+      launches += 3;
+    }
+    launches += 1;
   }
   if (ex) CK(ex->begin());
   if (n_probe > 0) {
@@ -1118,6 +1123,10 @@ int run_transient(pg_grid **gs, int ng, Exchange *ex, double h, int64_t steps, d
       set_error("a node has a non-positive diagonal d_i (no capacitance and no conductive path; Lemma 1)");
       return PG_EINVAL;
     }
+  }
+  for (int k = 0; k < ng; ++k) {  // the setup for h is valid (diagonal checked)
+    gs[k]->setup_ok = true;
+    gs[k]->setup_h = h;
   }
   for (int k = 0; k < ng; ++k) {
     if (gs[k]->ctl_host->nonfinite) {

@@ -152,6 +152,10 @@ struct pg_grid {
   // state pg_transient_continue resumes from); 0 after create / set_voltages / dc
   int64_t traj_steps = 0;
   double traj_h = 0.0;
+  // step-size-dependent setup (companion conductances, 1/d) valid for setup_h:
+  // a call with the same h (e.g. the next pg_transient_continue window) skips it
+  bool setup_ok = false;
+  double setup_h = 0.0;
 
   // ---- control
   pgb::DevCtl *ctl = nullptr;
