@@ -219,6 +219,17 @@ __device__ __forceinline__ NodeC load_c(const double *Ry, const double *Rn, int 
 // VU / VD via neighbours in layers l+1 / l-1 (gzD = 0 in layer 0 cancels VD).
 __device__ __forceinline__ double upd_c(const NodeC &c, double w, double Vc, double Vown, double Voth,
                                         double VN, double VS, double VU, double VD) {
+#ifdef PG_DIAG_NOFP
+  // diagnostic build only (tools/power_trace.py experiments): every operand is
+  // still loaded, but the update is integer bit mixing masked to zero by a
+  // runtime condition the compiler cannot fold (omega is never > 100), so the
+  // kernel moves the same data without its fp64 arithmetic
+  const unsigned long long m = w > 100.0 ? ~0ull : 0ull;
+  auto u = [](double x) { return (unsigned long long)__double_as_longlong(x); };
+  const unsigned long long x = u(c.gxOwn) ^ u(Vown) ^ u(c.gxOth) ^ u(Voth) ^ u(c.gyN) ^ u(VN) ^ u(c.gyS) ^
+                               u(VS) ^ u(c.gzU) ^ u(VU) ^ u(c.gzD) ^ u(VD) ^ u(c.b) ^ u(c.id);
+  return __longlong_as_double((long long)(u(Vc) ^ (x & m)));
+#endif
   double s1 = fma(c.gxOwn, Vown, c.b);
   s1 = fma(c.gxOth, Voth, s1);
   s1 = fma(c.gyN, VN, s1);
