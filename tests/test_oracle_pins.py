@@ -540,3 +540,58 @@ def test_check_every_is_line8_tested_every_f_sweeps():
         assert rF.sweeps[1] == j and np.all(rF.sweeps[1:] % F == 0)
         if F == 1:
             np.testing.assert_array_equal(rF.V, r1.V)
+
+
+@pytest.mark.parametrize("rlc", [False, True])
+def test_netlist_from_mesh_brute_force(rlc):
+    # the oracle's branch list of a mesh (gridgen.mesh_to_edges + netlist.from_mesh)
+    # against the PAPER.md §II-A element list written out node by node: an R
+    # branch for every in-layer segment (l,y,x)-(l,y,x+1) / (l,y,x)-(l,y+1,x)
+    # and every via (l,y,x)-(l+1,y,x) (R6, R16), a G0 branch from every pad
+    # node to the Vdd source node, a capacitor to ground at every node and a
+    # current source per load; RLC (R7, "node" model): a via or pad with
+    # inductance is R to a new internal node, then L onward
+    g = gridgen.mesh_grid(3, 4, 5, seed=4, pad_pitch=2, src_frac=0.5, h=2e-12, rlc=rlc)
+    L, NY, NX = g.layers, g.ny, g.nx
+    nid = lambda l, y, x: (l * NY + y) * NX + x                   # noqa: E731
+    R, Lb = [], []
+    nxt = g.n
+    for l in range(L):
+        for y in range(NY):
+            for x in range(NX):
+                if x + 1 < NX:
+                    R.append((nid(l, y, x), nid(l, y, x + 1), float(g.gx[l, y, x])))
+                if y + 1 < NY:
+                    R.append((nid(l, y, x), nid(l, y + 1, x), float(g.gy[l, y, x])))
+    for l in range(L - 1):
+        for y in range(NY):
+            for x in range(NX):
+                a, b, gz = nid(l, y, x), nid(l + 1, y, x), float(g.gz[l, y, x])
+                lz = 0.0 if g.lz is None else float(g.lz[l, y, x])
+                if lz > 0:
+                    R.append((a, nxt, gz))
+                    Lb.append((nxt, b, lz))
+                    nxt += 1
+                else:
+                    R.append((a, b, gz))
+    for k in range(len(g.pad_node)):
+        p, gp = int(g.pad_node[k]), float(g.pad_g[k])
+        if g.pad_l is not None:
+            R.append((p, nxt, gp))
+            Lb.append((nxt, src(0), float(g.pad_l[k])))
+            nxt += 1
+        else:
+            R.append((p, src(0), gp))
+    nl = netlist.from_mesh(g)
+    assert nl.n == nxt and nl.n_mesh == g.n
+    got_r = sorted(zip(nl.ra.tolist(), nl.rb.tolist(), nl.rg.tolist()))
+    assert got_r == sorted(R)
+    got_l = sorted(zip(nl.la.tolist(), nl.lb.tolist(), nl.lv.tolist()))
+    assert got_l == sorted(Lb)
+    assert len(Lb) > 0 if rlc else len(Lb) == 0
+    np.testing.assert_array_equal(nl.ca, np.arange(g.n))
+    assert np.all(nl.cb == GROUND)
+    np.testing.assert_array_equal(nl.cv, g.cap.reshape(-1))
+    assert float(nl.vd[0]) == g.vdd
+    np.testing.assert_array_equal(nl.ia, g.sources.node)
+    assert np.all(nl.ib == GROUND)
