@@ -2,7 +2,7 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
                     [--workload C] [--tsteps T] [--omega w] [--method rbsor|jacobi]
-                    [--scaling strong|weak] [--transport nccl|p2p] [--opt key=value ...]
+                    [--scaling strong|weak] [--transport auto|nccl|p2p] [--opt key=value ...]
 
 Workload: BASELINE.json config C (default 4: the 8 x 4096 x 4096 RC mesh,
 134M nodes, h = 5 ps, 200 steps -- the largest single-GPU configuration,
@@ -85,8 +85,9 @@ def parse():
                     help="N = 1 only: split the mesh into this many row slabs advanced by the "
                          "single-process group (pg_group_local): the multi-GPU protocol's "
                          "exchange cost measured on one GPU")
-    ap.add_argument("--transport", default=None, choices=["nccl", "copy", "p2p"],
-                    help="slab exchange: nccl (N > 1 default), copy (--slabs default), or p2p: "
+    ap.add_argument("--transport", default=None, choices=["auto", "nccl", "copy", "p2p"],
+                    help="slab exchange: auto (N > 1 default: p2p, checked once against nccl on the "
+                         "first window, nccl if they differ), nccl, copy (--slabs default), or p2p: "
                          "fused into the sweep kernel over peer memory (CUDA IPC for N > 1)")
     ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
                     help="N > 1: strong = the config split over the GPUs (default), weak = config rows x N")
@@ -196,8 +197,11 @@ def config_dict(cfg, g, T, tol, omega, omega_src, method, opts, world, scaling, 
     """The workload description both arms print (identical for the same args)."""
     if world > 1:
         par = (f"slab{world}: rows split over {world} GPUs ({scaling} scaling), "
-               + ("ghost rows and norm exchanged by the sweep kernel over peer memory (CUDA IPC)"
-                  if transport == "p2p" else "NCCL ghost-row exchange + norm allreduce per sweep launch"))
+               + {"p2p": "ghost rows and norm exchanged by the sweep kernel over peer memory (CUDA IPC)",
+                  "auto": ("ghost rows and norm exchanged by the sweep kernel over peer memory (CUDA IPC), "
+                           "checked bit for bit against the NCCL transport on the first window "
+                           "(NCCL if they differ; detail.transport says which ran)")}.get(
+                   transport, "NCCL ghost-row exchange + norm allreduce per sweep launch"))
     elif slabs > 1:
         par = (f"1 GPU, {slabs} row slabs exchanged in one process ("
                + ("pg_group_local_p2p: peer-memory exchange in the sweep kernel" if transport == "p2p"
@@ -328,6 +332,38 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------- b200 arm
+def verify_p2p(P, g, rank, world, make_group, T, tol, omega):
+    """First window (T time steps from x(0)) with the NCCL transport and with
+    the peer-memory exchange fused into the sweep: owned voltages and per-step
+    sweep counts must be identical on every rank.  Returns (ok, reason), the
+    same on every rank."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    res, why = {}, ""
+    for p2p in (False, True):
+        try:
+            grp = make_group(p2p=p2p)
+            try:
+                r = grp.transient(g.h, T, tol=tol, omega=omega, max_sweeps=200000)
+                V = np.concatenate([v.reshape(-1) for _, v in grp.owned_voltages(g)])
+                res[p2p] = (V, np.asarray(r.sweeps).copy())
+            finally:
+                grp.close()
+        except Exception as e:  # noqa: BLE001 -- any failure selects NCCL
+            why = f"{'p2p' if p2p else 'nccl'} raised {type(e).__name__}: {e}"[:200]
+            break
+    ok = len(res) == 2 and all(np.array_equal(a, b) for a, b in zip(res[False], res[True]))
+    if len(res) == 2 and not ok:
+        why = "owned voltages or sweep counts differ from the nccl transport"
+    flag = torch.tensor([1 if ok else 0], dtype=torch.int32,
+                        device="cuda" if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    if int(flag.item()) == 0 and ok:
+        why = "another rank's check failed"
+    return bool(flag.item()), why
+
+
 def run_b200(args):
     import numpy as np
     import torch
@@ -346,26 +382,26 @@ def run_b200(args):
     stream = torch.cuda.current_stream()
     opts = dict(kv.split("=", 1) for kv in args.opt)
     fuse = int(opts.get("fuse", 2))
-    transport = args.transport or ("nccl" if world > 1 else "copy")
-    p2p = transport == "p2p"
+    transport = args.transport or ("auto" if world > 1 else "copy")
     iopts = {k: int(v) for k, v in opts.items()}
+    tr = {"p2p": transport in ("p2p", "auto"), "note": None}
 
-    def make_group(device=True):
+    def make_group(device=True, p2p=None):
         # slab partition over the ranks, exchange after every sweep launch
         # inside the library (pg_group_transient): NCCL halo send/recv + norm
         # allreduce, or the peer-memory exchange fused into the sweep kernel
-        if p2p:
+        if tr["p2p"] if p2p is None else p2p:
             return P.SlabGroup.p2p(g, rank, world, fuse=fuse, stream=stream, device=device, options=iopts)
         return P.SlabGroup.nccl(g, rank, world, fuse=fuse, stream=stream, device=device)
 
     if world > 1:
-        grp = make_group()
+        grp = make_group(p2p=False if transport == "auto" else None)
         G = grp.grids[0]
         sp = grp.specs[0]
         my_nodes = g.layers * (sp.y1 - sp.y0) * g.nx
     elif args.slabs > 1:
-        grp = P.SlabGroup.local(g, args.slabs, fuse=fuse, stream=stream, transport="p2p" if p2p else "copy",
-                                options=iopts if p2p else None)
+        grp = P.SlabGroup.local(g, args.slabs, fuse=fuse, stream=stream,
+                                transport="p2p" if tr["p2p"] else "copy", options=iopts if tr["p2p"] else None)
         G = grp.grids[0]
         my_nodes = g.n
     else:
@@ -388,6 +424,21 @@ def run_b200(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         omega = float(t.item())
     t_om = time.perf_counter() - t_om
+    if world > 1 and transport == "auto":
+        # the fused peer-memory exchange is the product path; before it is
+        # timed, its first window is compared bit for bit with the NCCL
+        # transport's (both equal the single grid, tests/test_gpu_slab.py,
+        # test_gpu_p2p.py) and every rank falls back to NCCL unless all agree
+        grp.close()
+        ok, why = verify_p2p(P, g, rank, world, make_group, T, tol, omega)
+        tr["p2p"] = ok
+        tr["note"] = "p2p (equal to nccl on the first window)" if ok else f"nccl (p2p check failed: {why})"
+        grp = make_group()
+        G = grp.grids[0]
+        for k, v in opts.items():
+            G.set_option(k, int(v))
+    elif world > 1:
+        tr["note"] = transport
 
     state = {"done": 0}
 
@@ -525,7 +576,7 @@ def run_b200(args):
         h2d = d2h = 0
         for _ in range(nrep):
             H = make_group(device=False)
-            if not p2p:
+            if not tr["p2p"]:
                 for k, v in opts.items():
                     H.grids[0].set_option(k, int(v))
             rr = H.transient(g.h, T, tol=tol, omega=omega, max_sweeps=200000)
@@ -616,7 +667,8 @@ def run_b200(args):
                                                f"included) / {TOT}") if full is not None else None,
                        "sweeps_per_time_step_mean": float(spt.mean()),
                        "sweeps_per_time_step_max": int(spt.max()),
-                       "omega_time_s": round(t_om, 3)},
+                       "omega_time_s": round(t_om, 3),
+                       "transport": tr["note"]},
             "clocks": ck, "e2e": e2e, "gpu_launches": launches, "roofline": roof,
             "cpu_baseline": cpu,
         }
