@@ -4,7 +4,9 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -48,6 +50,29 @@ using namespace pgb;
 
 namespace {
 
+// PGB200_TRACE=1: phase times of the host-buffer calls (create, set_sources,
+// get_voltages) on stderr, each phase closed by a device synchronisation
+// (diagnostics of the end-to-end path; off by default, no synchronisation)
+struct PhaseTrace {
+  bool on;
+  const char *call;
+  std::chrono::steady_clock::time_point t;
+  explicit PhaseTrace(const char *c) : on(std::getenv("PGB200_TRACE") != nullptr), call(c) {
+    if (on) {
+      cudaDeviceSynchronize();
+      t = std::chrono::steady_clock::now();
+    }
+  }
+  void mark(const char *what) {
+    if (!on) return;
+    cudaDeviceSynchronize();
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[pgb200 trace] %s %s %.2f ms\n", call, what,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 // Device memory of the grids comes from a library-owned stream-ordered pool
 // per device (release threshold 48 GiB by default), so creating and destroying grids, the
 // per-call scratch of pg_transient and pg_set_sources do not map and unmap
@@ -56,9 +81,16 @@ namespace {
 // after the pool's stream reached the allocation and returned after a device
 // synchronisation, so they are usable from any stream like cudaMalloc memory.
 // DevCtl stays plain cudaMalloc memory: it is exported over CUDA IPC.
+// Two pools per device: blocks of >= kLargeBlock bytes (the per-node arrays)
+// and smaller ones (pads, load store, scratch).  A pool splits its cached free
+// blocks to serve smaller requests, so with one pool a 256-byte flag or a
+// 40 MB sort buffer carved out of a freed 1 GB array made the next grid's 1 GB
+// arrays map fresh memory (10-140 ms per call on config 4, PGB200_TRACE).
+constexpr size_t kLargeBlock = (size_t)32 << 20;
 struct DevPool {
   bool init = false;
-  cudaMemPool_t pool = nullptr;
+  cudaMemPool_t pool = nullptr;   // blocks >= kLargeBlock
+  cudaMemPool_t small = nullptr;  // blocks < kLargeBlock
   cudaStream_t s = nullptr;
 };
 std::mutex g_pool_mu;
@@ -83,8 +115,11 @@ DevPool *pool_of(int dev) {
     uint64_t gib = 48;
     if (const char *e = std::getenv("PGB200_POOL_GIB")) gib = std::strtoull(e, nullptr, 10);
     uint64_t thr = gib << 30;
+    uint64_t thr_small = (uint64_t)1 << 30;
     if (cudaMemPoolCreate(&d.pool, &pr) != cudaSuccess ||
         cudaMemPoolSetAttribute(d.pool, cudaMemPoolAttrReleaseThreshold, &thr) != cudaSuccess ||
+        cudaMemPoolCreate(&d.small, &pr) != cudaSuccess ||
+        cudaMemPoolSetAttribute(d.small, cudaMemPoolAttrReleaseThreshold, &thr_small) != cudaSuccess ||
         cudaStreamCreateWithFlags(&d.s, cudaStreamNonBlocking) != cudaSuccess) {
       cudaGetLastError();
       d.pool = nullptr;
@@ -139,15 +174,18 @@ int dalloc(T **p, int64_t count, bool plain = false) {
   if (d) {
     // sizes rounded to 256 B so that every block keeps cudaMalloc's alignment
     // (TMA tensor maps and vector loads rely on it); checked below
-    e = cudaMallocFromPoolAsync((void **)p, (bytes + 255) & ~(size_t)255, d->pool, d->s);
+    const size_t rb = (bytes + 255) & ~(size_t)255;
+    cudaMemPool_t mp = rb >= kLargeBlock ? d->pool : d->small;
+    e = cudaMallocFromPoolAsync((void **)p, rb, mp, d->s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(d->s);
     if (e != cudaSuccess) {
-      // the pool's cached free blocks may be what is missing: release them to
+      // the pools' cached free blocks may be what is missing: release them to
       // the device and retry once before falling back to cudaMalloc
       cudaGetLastError();
       cudaStreamSynchronize(d->s);
       cudaMemPoolTrimTo(d->pool, 0);
-      e = cudaMallocFromPoolAsync((void **)p, (bytes + 255) & ~(size_t)255, d->pool, d->s);
+      cudaMemPoolTrimTo(d->small, 0);
+      e = cudaMallocFromPoolAsync((void **)p, rb, mp, d->s);
       if (e == cudaSuccess) e = cudaStreamSynchronize(d->s);
     }
     if (e == cudaSuccess && ((uintptr_t)*p & 255)) {
@@ -368,28 +406,33 @@ PG_API int pg_create_mesh(int32_t layers, int32_t ny, int32_t nx, const double *
   g->md.np = (int64_t)layers * g->md.layer_stride;
   g->np = g->md.np;
   int rc;
+  PhaseTrace tr("pg_create_mesh");
   if ((rc = common_init(g))) return rc;
+  tr.mark("common_init");
   const cudaMemcpyKind kind = mem == PG_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
   double *stage = nullptr;  // user-order staging buffer, scattered into the storage layout
   int32_t *d_bad = nullptr;  // value-check flags of the inputs (checked on the device)
-  if ((rc = dalloc(&stage, n)) || (rc = dalloc(&d_bad, 1))) return rc;
-  struct StageGuard {
-    double *p;
+  // the staging buffer stays with the grid as its user-order buffer
+  // (pg_get_voltages / pg_set_voltages), so reading the result back allocates nothing
+  if ((rc = dalloc(&stage, n))) return rc;
+  g->user_buf = stage;
+  if ((rc = dalloc(&d_bad, 1))) return rc;
+  struct FlagGuard {
     int32_t *q;
-    ~StageGuard() {
-      dfree(p);
-      dfree(q);
-    }
-  } stage_guard{stage, d_bad};
+    ~FlagGuard() { dfree(q); }
+  } flag_guard{d_bad};
   CK(cudaMemset(d_bad, 0, sizeof(int32_t)));
   // which: 0 gx, 1 gy, 2 gz (>= 0, finite, zero on the open boundary), 3 cap, 4 lz (>= 0, finite)
   auto put = [&](double **dst, const double *src, int which) -> int {
     int r = dalloc(dst, g->np);
     if (r) return r;
     CK(cudaMemset(*dst, 0, sizeof(double) * g->np));
+    tr.mark("alloc+memset");
     CK(cudaMemcpy(stage, src, sizeof(double) * n, kind));
+    tr.mark("copy");
     CK(mesh_check_async(g, stage, which, d_bad));
     CK(launch_scatter_user(g, stage, *dst));
+    tr.mark("check+scatter");
     return PG_OK;
   };
   if ((rc = put(&g->gx, gx, 0)) || (rc = put(&g->gy, gy, 1)) || (rc = put(&g->gz, gz, 2)) ||
@@ -409,8 +452,10 @@ PG_API int pg_create_mesh(int32_t layers, int32_t ny, int32_t nx, const double *
   REQUIRE(!(bad & (1 << 2)), "gz must be finite, >= 0 and 0 in the top layer");
   REQUIRE(!(bad & (1 << 3)), "cap must be finite and >= 0");
   REQUIRE(!(bad & (1 << 4)), "lz must be finite and >= 0");
+  tr.mark("gze+lz+flags");
   if ((rc = set_pads(g, n_pads, pad_node, pad_g, pad_l, mem, nullptr))) return rc;
   CK(cudaDeviceSynchronize());
+  tr.mark("set_pads");
   guard.g = nullptr;
   *out = g;
   return PG_OK;
@@ -600,6 +645,7 @@ PG_API int pg_set_sources(pg_grid *g, int64_t n_src, const int64_t *node, const 
     }
   } tg{tmp};
   int rc;
+  PhaseTrace tr("pg_set_sources");
   if (n_src > 0 && mem == PG_MEM_HOST) {
     int64_t *a = nullptr, *b = nullptr;
     double *c = nullptr, *d = nullptr;
@@ -615,6 +661,7 @@ PG_API int pg_set_sources(pg_grid *g, int64_t n_src, const int64_t *node, const 
     CK(cudaMemcpyAsync(c, t, sizeof(double) * npts, cudaMemcpyHostToDevice, g->stream));
     CK(cudaMemcpyAsync(d, i, sizeof(double) * npts, cudaMemcpyHostToDevice, g->stream));
     d_node = a, d_ptr = b, d_t = c, d_i = d;
+    tr.mark("alloc+copy");
   }
   int64_t *old_i64[4] = {g->src_idx, g->src_grp, g->src_ptr, g->src_tile};
   double *old_d[2] = {g->pwl_t, g->pwl_i};
@@ -630,6 +677,7 @@ PG_API int pg_set_sources(pg_grid *g, int64_t n_src, const int64_t *node, const 
     REQUIRE(!(bad & 4), "source node index out of range");
     REQUIRE(!(bad & 8), "PWL breakpoint times must be strictly increasing");
     REQUIRE(!(bad & 16), "PWL breakpoints and values must be finite");
+    tr.mark("build");
   } else {
     g->src_idx = g->src_grp = g->src_ptr = g->src_tile = nullptr;
     g->pwl_t = g->pwl_i = nullptr;
@@ -680,11 +728,14 @@ PG_API int pg_get_voltages(pg_grid *g, double *v, int mem) {
   // staged through a per-grid buffer kept until pg_destroy: no cudaMalloc /
   // cudaFree (a device-wide synchronisation) per read-back
   int rc;
+  PhaseTrace tr("pg_get_voltages");
   if (!g->user_buf && (rc = dalloc(&g->user_buf, g->n))) return rc;
   double *tmp = g->user_buf;
   cudaError_t e = launch_gather_user(g, tmp);
+  tr.mark("alloc+gather");
   if (e == cudaSuccess) e = cudaMemcpyAsync(v, tmp, sizeof(double) * g->n, cudaMemcpyDeviceToHost, g->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
+  tr.mark("copy");
   if (e != cudaSuccess) return cuda_fail(e, "pg_get_voltages");
   return PG_OK;
 }

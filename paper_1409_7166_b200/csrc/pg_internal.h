@@ -163,7 +163,7 @@ struct pg_grid {
   int32_t *done_host = nullptr;        // pinned ring of polled `done` flags
   int64_t *dev_sweeps = nullptr;       // per-step sweep counts (device)
   int64_t dev_sweeps_cap = 0;
-  double *user_buf = nullptr;          // n doubles: user-order staging of pg_get/set_voltages (lazy)
+  double *user_buf = nullptr;          // n doubles: user-order staging of pg_get/set_voltages (mesh: the create staging buffer; CSR: lazy)
 
   // ---- slab of a partitioned mesh (pg_set_slab): rows [y_begin, y_end) are
   // owned, the others are ghost rows refreshed by the group exchange

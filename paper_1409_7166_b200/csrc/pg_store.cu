@@ -173,14 +173,19 @@ int build_sources_device(pg_grid *g, int64_t n_src, const int64_t *node, const i
   auto out_alloc = [&](void **p, size_t bytes) -> cudaError_t {
     return dalloc_bytes(p, bytes) == PG_OK ? cudaSuccess : cudaErrorMemoryAllocation;
   };
+  // scratch from the library's pool too (pg_api.cu): cudaMallocAsync on the
+  // device's default pool returned its ~300 MB (config 4) to the device at
+  // every synchronisation and re-mapped it on the next call (5-260 ms per
+  // pg_set_sources, PGB200_TRACE)
+  auto scratch = [&](void **p, size_t bytes) -> cudaError_t { return out_alloc(p, bytes); };
   auto cleanup = [&]() {
+    cudaStreamSynchronize(st);
     for (void *p : {(void *)key, (void *)pos, (void *)skey, (void *)spos, (void *)len, (void *)head, (void *)gidx,
                     (void *)d_err, tmp})
-      if (p) cudaFreeAsync(p, st);
+      if (p) dfree_bytes(p);
   };
   auto fail = [&](cudaError_t e, const char *what) {
     cleanup();
-    cudaStreamSynchronize(st);
     for (void *p : {(void *)o_ptr, (void *)o_grp, (void *)o_tiles, (void *)o_t, (void *)o_v, (void *)o_idx})
       if (p) dfree_bytes(p);
     err = std::string(what) + ": " + cudaGetErrorString(e);
@@ -192,14 +197,14 @@ int build_sources_device(pg_grid *g, int64_t n_src, const int64_t *node, const i
     if (_e != cudaSuccess) return fail(_e, what); \
   } while (0)
   const size_t nb = sizeof(int64_t) * (size_t)n_src;
-  SCK(cudaMallocAsync(&key, nb, st), "alloc");
-  SCK(cudaMallocAsync(&pos, nb, st), "alloc");
-  SCK(cudaMallocAsync(&skey, nb, st), "alloc");
-  SCK(cudaMallocAsync(&spos, nb, st), "alloc");
-  SCK(cudaMallocAsync(&len, nb, st), "alloc");
-  SCK(cudaMallocAsync(&head, nb, st), "alloc");
-  SCK(cudaMallocAsync(&gidx, nb, st), "alloc");
-  SCK(cudaMallocAsync(&d_err, sizeof(int32_t), st), "alloc");
+  SCK(scratch((void **)&key, nb), "alloc");
+  SCK(scratch((void **)&pos, nb), "alloc");
+  SCK(scratch((void **)&skey, nb), "alloc");
+  SCK(scratch((void **)&spos, nb), "alloc");
+  SCK(scratch((void **)&len, nb), "alloc");
+  SCK(scratch((void **)&head, nb), "alloc");
+  SCK(scratch((void **)&gidx, nb), "alloc");
+  SCK(scratch((void **)&d_err, sizeof(int32_t)), "alloc");
   SCK(cudaMemsetAsync(d_err, 0, sizeof(int32_t), st), "memset");
   k_src_ptr_check<<<grid, B, 0, st>>>(n_src, ptr, npts, d_err);
   SCK(cudaGetLastError(), "k_src_ptr_check");
@@ -208,7 +213,6 @@ int build_sources_device(pg_grid *g, int64_t n_src, const int64_t *node, const i
   SCK(cudaStreamSynchronize(st), "sync");
   if (p_err) {
     cleanup();
-    cudaStreamSynchronize(st);
     *bad_bits = p_err;
     return PG_OK;
   }
@@ -219,7 +223,6 @@ int build_sources_device(pg_grid *g, int64_t n_src, const int64_t *node, const i
   SCK(cudaStreamSynchronize(st), "sync");
   if (h_err) {
     cleanup();
-    cudaStreamSynchronize(st);
     *bad_bits = h_err;
     return PG_OK;
   }
@@ -230,7 +233,7 @@ int build_sources_device(pg_grid *g, int64_t n_src, const int64_t *node, const i
   cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, key, skey, pos, spos, n_src, 0, end_bit, st);
   cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, len, len, n_src, st);
   tmp_bytes = std::max(sort_bytes, scan_bytes);
-  SCK(cudaMallocAsync(&tmp, tmp_bytes, st), "alloc");
+  SCK(scratch(&tmp, tmp_bytes), "alloc");
   SCK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key, skey, pos, spos, n_src, 0, end_bit, st), "sort");
   // breakpoint offsets in sorted order: the sorted sources' lengths (key is
   // free after the sort), exclusively scanned, the total in o_ptr[n_src]
@@ -261,7 +264,6 @@ int build_sources_device(pg_grid *g, int64_t n_src, const int64_t *node, const i
   SCK(cudaStreamSynchronize(st), "sync");
 #undef SCK
   cleanup();
-  cudaStreamSynchronize(st);
   g->src_idx = o_idx;
   g->src_grp = o_grp;
   g->src_ptr = o_ptr;

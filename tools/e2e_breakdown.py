@@ -38,3 +38,12 @@ for rep in range(reps):
     print(f"config{cfg} rep {rep}: create {1e3*(t1-t0):.1f} ms, set_sources {1e3*(t2-t1):.1f} ms, "
           f"transient({T}) {1e3*(t3-t2):.1f} ms (device {r.stats.device_ms:.1f}), voltages {1e3*(t4-t3):.1f} ms, "
           f"close {1e3*(t5-t4):.1f} ms", flush=True)
+# raw PCIe rates for comparison: torch copies of one pinned 1 GiB array
+hb = torch.empty(1 << 27, dtype=torch.float64).pin_memory()
+db = torch.empty(1 << 27, dtype=torch.float64, device="cuda")
+for rep in range(3):
+    torch.cuda.synchronize(); t0 = time.perf_counter()
+    db.copy_(hb, non_blocking=True); torch.cuda.synchronize(); t1 = time.perf_counter()
+    hb.copy_(db, non_blocking=True); torch.cuda.synchronize(); t2 = time.perf_counter()
+    print(f"raw 1 GiB pinned: H2D {1e3*(t1-t0):.1f} ms ({(1<<30)/(t1-t0)/1e9:.1f} GB/s), "
+          f"D2H {1e3*(t2-t1):.1f} ms ({(1<<30)/(t2-t1)/1e9:.1f} GB/s)", flush=True)
