@@ -353,8 +353,19 @@ PG_API int pg_tune_omega(pg_grid *g, double h, int64_t steps, double tol, int64_
 PG_API int pg_info(const pg_grid *g, int64_t *n, int32_t *layers, int32_t *ny, int32_t *nx,
                    int32_t *n_colors);
 
-/* Free all device memory of the grid.  NULL is a no-op. */
+/* Free all device memory of the grid.  NULL is a no-op.  The grid's blocks
+ * return to the library's per-device memory pools, which keep up to
+ * PGB200_POOL_GIB (default 48) GiB of freed per-node arrays and 1 GiB of
+ * smaller blocks mapped for the next grid (re-mapping a config-4-sized grid
+ * costs ~0.4-1 s per create); pg_release_memory hands them back. */
 PG_API void pg_destroy(pg_grid *g);
+
+/* Return the freed blocks the library's memory pools hold on `device`
+ * (-1: every device the library has used) to the CUDA driver, so that other
+ * allocators of the process (cudaMalloc, PyTorch) can use that memory.  Live
+ * grids keep their memory.  Synchronises the device(s).  Returns PG_OK, or
+ * PG_EINVAL for a device index outside [-1, 63]. */
+PG_API int pg_release_memory(int32_t device);
 
 /* Description of the last error on this thread ("" if none). */
 PG_API const char *pg_last_error(void);

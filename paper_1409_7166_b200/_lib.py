@@ -49,6 +49,7 @@ SIGNATURES = {
     "pg_info": (_c_int, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i32), ctypes.POINTER(_i32),
                          ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),
     "pg_destroy": (None, [_vp]),
+    "pg_release_memory": (_c_int, [_i32]),
     "pg_estimate_omega": (_c_int, [_vp, _dbl, _i64, ctypes.POINTER(_dbl), ctypes.POINTER(_dbl)]),
     "pg_tune_omega": (_c_int, [_vp, _dbl, _i64, _dbl, _i64, _dbl, ctypes.POINTER(_dbl), _vp]),
     "pg_dc": (_c_int, [_vp, _dbl, _dbl, _dbl, _c_int, _i64, ctypes.POINTER(PgStats)]),

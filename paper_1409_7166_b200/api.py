@@ -262,6 +262,12 @@ class Grid:
         self.close()
 
 
+def release_memory(device: int = -1) -> None:
+    """pg_release_memory: return the freed blocks the library's device memory
+    pools keep cached (for the next grid) to the CUDA driver; -1 = all devices."""
+    L.check(L.load().pg_release_memory(int(device)))
+
+
 def _ptr_of(x):
     if _is_torch(x):
         if not x.is_contiguous() or x.dtype.__str__() != "torch.float64":

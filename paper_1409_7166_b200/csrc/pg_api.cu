@@ -233,8 +233,6 @@ int upload(T *dst, const std::vector<T> &v) {
   return PG_OK;
 }
 
-std::atomic<int> g_live_grids[64];  // grids alive per device (the pool is trimmed when none is)
-
 void free_grid(pg_grid *g) {
   if (!g) return;
   int cur = 0;
@@ -254,10 +252,10 @@ void free_grid(pg_grid *g) {
   if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
   if (g->ctl_host) cudaFreeHost(g->ctl_host);
   if (g->done_host) cudaFreeHost(g->done_host);
-  if (g->counted && g->dev >= 0 && g->dev < 64) g_live_grids[g->dev].fetch_sub(1);
-  // the pool keeps up to its release threshold of freed memory cached for the
-  // next grid (re-mapping ~10 GB for a config-4-sized grid costs ~1 s); an
-  // allocation the pool cannot serve trims it before falling back to cudaMalloc
+  // the pools keep up to their release thresholds of freed memory cached for
+  // the next grid (re-mapping ~10 GB for a config-4-sized grid costs ~1 s); an
+  // allocation the pools cannot serve trims them before falling back to
+  // cudaMalloc, and pg_release_memory hands the cache back explicitly
   if (other) cudaSetDevice(cur);
   delete g;
 }
@@ -288,10 +286,6 @@ std::vector<int64_t> groups_of(const std::vector<int64_t> &sidx) {
 
 int common_init(pg_grid *g) {
   CK(cudaGetDevice(&g->dev));
-  if (g->dev >= 0 && g->dev < 64) {
-    g_live_grids[g->dev].fetch_add(1);
-    g->counted = true;
-  }
   CK(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, g->dev));
   g->ntile = (g->np + kRhsTile - 1) / kRhsTile;
   int rc;
@@ -532,6 +526,26 @@ PG_API int pg_create_csr(int64_t n, int64_t m, const int64_t *bu, const int64_t 
 }
 
 PG_API void pg_destroy(pg_grid *g) { free_grid(g); }
+
+PG_API int pg_release_memory(int32_t device) {
+  REQUIRE(device >= -1 && device < 64, "device must be -1 (all) or a device index < 64");
+  int cur = 0;
+  CK(cudaGetDevice(&cur));
+  for (int dv = device < 0 ? 0 : device; dv < (device < 0 ? 64 : device + 1); ++dv) {
+    DevPool *d = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(g_pool_mu);
+      if (g_pools[dv].init && g_pools[dv].pool) d = &g_pools[dv];
+    }
+    if (!d) continue;
+    CK(cudaSetDevice(dv));
+    CK(cudaDeviceSynchronize());  // blocks freed stream-ordered on the pool stream are returned
+    CK(cudaMemPoolTrimTo(d->pool, 0));
+    CK(cudaMemPoolTrimTo(d->small, 0));
+  }
+  CK(cudaSetDevice(cur));
+  return PG_OK;
+}
 
 PG_API int pg_set_stream(pg_grid *g, void *stream) {
   REQUIRE(g != nullptr, "grid is NULL");

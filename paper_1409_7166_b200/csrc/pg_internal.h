@@ -110,7 +110,6 @@ struct pg_grid {
   cudaStream_t stream = nullptr;
   int dev = -1;               // set by creation (common_init)
   int num_sms = 148;
-  bool counted = false;      // counted in the per-device live-grid count (pool trimming)
 
   // ---- mesh store (padded natural layout, SoA)
   pgb::MeshDims md{};

@@ -94,3 +94,12 @@ def test_binding_refuses_mismatched_buffer_sizes(libpath):
         g.set_sources(np.array([1]), np.array([0, 3]), np.zeros(2), np.zeros(3))
     with pytest.raises(ValueError):
         g.transient(1e-12, 3, probes=np.array([0, 1]), probe_out=np.empty((3, 2)))
+
+
+def test_release_memory_rejects_bad_device_without_gpu(libpath):
+    # argument check before any CUDA call
+    from paper_1409_7166_b200 import _lib
+    lib = _lib.load()
+    assert lib.pg_release_memory(64) == _lib.PG_EINVAL
+    assert b"device" in lib.pg_last_error()
+    assert lib.pg_release_memory(-2) == _lib.PG_EINVAL
