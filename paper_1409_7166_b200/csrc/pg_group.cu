@@ -28,6 +28,7 @@
 #include <algorithm>
 #include <cstddef>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -67,16 +68,12 @@ struct NcclApi {
   const char *(*GetErrorString)(ncclResult_t) = nullptr;
 };
 
-const NcclApi &nccl() {
-  static NcclApi api;
-  static bool tried = false;
-  if (tried) return api;
-  tried = true;
+void load_nccl(NcclApi &api) {
   // an NCCL already loaded into the process (e.g. by torch) is reused
   void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
   if (!h) {
     api.why = std::string("dlopen(libnccl.so.2) failed: ") + dlerror();
-    return api;
+    return;
   }
   auto sym = [&](const char *name) -> void * { return dlsym(h, name); };
   api.GetUniqueId = (decltype(api.GetUniqueId))sym("ncclGetUniqueId");
@@ -91,6 +88,12 @@ const NcclApi &nccl() {
   api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.Send &&
            api.Recv && api.GroupStart && api.GroupEnd && api.GetErrorString;
   if (!api.ok) api.why = "libnccl.so.2 lacks a required symbol";
+}
+
+const NcclApi &nccl() {  // loaded once per process (thread-safe)
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] { load_nccl(api); });
   return api;
 }
 
