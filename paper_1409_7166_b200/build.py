@@ -16,7 +16,7 @@ LIB = os.path.join(LIBDIR, "libpgb200.so")
 PROF_LIB = os.path.join(LIBDIR, "libpgb200_prof.so")
 SOURCES = ["pg_sweep_fused_i1.cu", "pg_sweep_fused_i2.cu", "pg_sweep_fused_i3.cu", "pg_sweep_fused_i4.cu",
            "pg_sweep_fused_i5.cu", "pg_sweep2.cu", "pg_kernels.cu", "pg_sweep_fused.cu", "pg_api.cu", "pg_group.cu", "pg_store.cu",
-           "pg_csr_build.cpp"]
+           "pg_csr_build.cpp", "pg_csr_device.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden",

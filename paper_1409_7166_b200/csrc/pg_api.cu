@@ -466,60 +466,111 @@ PG_API int pg_create_csr(int64_t n, int64_t m, const int64_t *bu, const int64_t 
   REQUIRE(cap != nullptr, "cap is required");
   REQUIRE(mem == PG_MEM_HOST || mem == PG_MEM_DEVICE, "mem must be PG_MEM_HOST or PG_MEM_DEVICE");
   REQUIRE(n_pads >= 0 && (n_pads == 0 || (pad_node && pad_g)), "bad pad arrays");
-  std::vector<int64_t> u, v;
-  std::vector<double> gg, c;
   int rc;
-  if ((rc = to_host(bu, m, mem, u)) || (rc = to_host(bv, m, mem, v)) || (rc = to_host(bg, m, mem, gg)) ||
-      (rc = to_host(cap, n, mem, c)))
-    return rc;
-  for (int64_t k = 0; k < n; ++k) REQUIRE(c[k] >= 0 && std::isfinite(c[k]), "cap must be finite and >= 0");
-  CsrHost H;
-  std::string err;
-  if (build_csr(n, m, u.data(), v.data(), gg.data(), H, err) != 0) {
-    set_error(err);
-    return PG_EINVAL;
-  }
+  PhaseTrace tr("pg_create_csr");
   pg_grid *g = new pg_grid();
   GridGuard guard{g};
   g->kind = 1;
   g->n = n;
   g->np = n;
   g->vdd = vdd;
-  g->ncolor = (int32_t)H.color_ptr.size() - 1;
-  g->color_ptr = H.color_ptr;
   if ((rc = common_init(g))) return rc;
-  std::vector<double> cp((size_t)n);
-  for (int64_t k = 0; k < n; ++k) cp[H.iperm[k]] = c[k];
-  const int64_t nnz = (int64_t)H.col.size();
-  REQUIRE(nnz < (int64_t)INT32_MAX - 64, "CSR grids are limited to 2^31 - 64 stored entries");
-  // int32 row pointers (4 B per row) and 8 elements of zero slack after
-  // rowptr / col / val: the staged sweep bulk-copies 16-byte-rounded ranges
-  std::vector<int32_t> rp32((size_t)n + 1 + 8, (int32_t)nnz);
-  for (int64_t k = 0; k <= n; ++k) rp32[k] = (int32_t)H.rowptr[k];
-  std::vector<int32_t> col_p(H.col);
-  col_p.resize((size_t)nnz + 8, 0);
-  std::vector<double> val_p(H.val);
-  val_p.resize((size_t)nnz + 8, 0.0);
-  // every kCsrR-row tile of every colour must fit the staged sweep's entry buffer
-  bool fits = true;
-  for (int32_t c = 0; c + 1 < (int32_t)H.color_ptr.size() && fits; ++c)
-    for (int64_t r0 = H.color_ptr[c]; r0 < H.color_ptr[c + 1]; r0 += kCsrR) {
-      const int64_t r1 = std::min<int64_t>(H.color_ptr[c + 1], r0 + kCsrR);
-      if (H.rowptr[r1] - H.rowptr[r0] > kCsrE) {
-        fits = false;
-        break;
+  tr.mark("init");
+  // The colour-permuted store is built on the device (pg_csr_device.cu) when
+  // the graph is connected and bipartite, else -- or with PGB200_CSR_HOST set
+  // -- by the host builder (pg_csr_build.cpp); both give the same store.
+  std::vector<int64_t> iperm_h;
+  bool done = false;
+  if (!std::getenv("PGB200_CSR_HOST")) {
+    const int64_t *du = bu, *dv = bv;
+    const double *dg = bg, *dc = cap;
+    void *tmp[4] = {nullptr, nullptr, nullptr, nullptr};
+    struct TmpGuard {
+      void **p;
+      ~TmpGuard() {
+        for (int k = 0; k < 4; ++k)
+          if (p[k]) dfree(p[k]);
       }
+    } tg{tmp};
+    if (mem == PG_MEM_HOST) {
+      int64_t *a = nullptr, *b = nullptr;
+      double *c = nullptr, *d = nullptr;
+      if ((rc = dalloc(&a, m)) || (rc = dalloc(&b, m)) || (rc = dalloc(&c, m)) || (rc = dalloc(&d, n))) {
+        for (void *q : {(void *)a, (void *)b, (void *)c, (void *)d})
+          if (q) dfree(q);
+        return rc;
+      }
+      tmp[0] = a, tmp[1] = b, tmp[2] = c, tmp[3] = d;
+      if (m > 0) {
+        CK(cudaMemcpyAsync(a, bu, sizeof(int64_t) * m, cudaMemcpyHostToDevice, g->stream));
+        CK(cudaMemcpyAsync(b, bv, sizeof(int64_t) * m, cudaMemcpyHostToDevice, g->stream));
+        CK(cudaMemcpyAsync(c, bg, sizeof(double) * m, cudaMemcpyHostToDevice, g->stream));
+      }
+      CK(cudaMemcpyAsync(d, cap, sizeof(double) * n, cudaMemcpyHostToDevice, g->stream));
+      du = a, dv = b, dg = c, dc = d;
     }
-  g->csr_staged_ok = fits;
-  if ((rc = dalloc(&g->rowptr, (int64_t)rp32.size())) || (rc = dalloc(&g->col, (int64_t)col_p.size())) ||
-      (rc = dalloc(&g->val, (int64_t)val_p.size())) || (rc = dalloc(&g->perm, n)) ||
-      (rc = dalloc(&g->iperm, n)) || (rc = dalloc(&g->cap, n)))
-    return rc;
-  if ((rc = upload(g->rowptr, rp32)) || (rc = upload(g->col, col_p)) || (rc = upload(g->val, val_p)) ||
-      (rc = upload(g->perm, H.perm)) || (rc = upload(g->iperm, H.iperm)) || (rc = upload(g->cap, cp)))
-    return rc;
-  if ((rc = set_pads(g, n_pads, pad_node, pad_g, nullptr, mem, &H.iperm))) return rc;
+    std::string err;
+    if ((rc = build_csr_device(g, n, m, du, dv, dg, dc, &done, err))) {
+      set_error(err);
+      return rc;
+    }
+    if (done) {
+      iperm_h.resize((size_t)n);
+      CK(cudaMemcpy(iperm_h.data(), g->iperm, sizeof(int64_t) * n, cudaMemcpyDeviceToHost));
+    }
+    tr.mark(done ? "build (device)" : "device build declined (not connected and bipartite)");
+  }
+  if (!done) {
+    std::vector<int64_t> u, v;
+    std::vector<double> gg, c;
+    if ((rc = to_host(bu, m, mem, u)) || (rc = to_host(bv, m, mem, v)) || (rc = to_host(bg, m, mem, gg)) ||
+        (rc = to_host(cap, n, mem, c)))
+      return rc;
+    for (int64_t k = 0; k < n; ++k) REQUIRE(c[k] >= 0 && std::isfinite(c[k]), "cap must be finite and >= 0");
+    CsrHost H;
+    std::string err;
+    if (build_csr(n, m, u.data(), v.data(), gg.data(), H, err) != 0) {
+      set_error(err);
+      return PG_EINVAL;
+    }
+    g->ncolor = (int32_t)H.color_ptr.size() - 1;
+    g->color_ptr = H.color_ptr;
+    std::vector<double> cp((size_t)n);
+    for (int64_t k = 0; k < n; ++k) cp[H.iperm[k]] = c[k];
+    const int64_t nnz = (int64_t)H.col.size();
+    REQUIRE(nnz < (int64_t)INT32_MAX - 64, "CSR grids are limited to 2^31 - 64 stored entries");
+    // int32 row pointers (4 B per row) and 8 elements of zero slack after
+    // rowptr / col / val: the staged sweep bulk-copies 16-byte-rounded ranges
+    std::vector<int32_t> rp32((size_t)n + 1 + 8, (int32_t)nnz);
+    for (int64_t k = 0; k <= n; ++k) rp32[k] = (int32_t)H.rowptr[k];
+    std::vector<int32_t> col_p(H.col);
+    col_p.resize((size_t)nnz + 8, 0);
+    std::vector<double> val_p(H.val);
+    val_p.resize((size_t)nnz + 8, 0.0);
+    // every kCsrR-row tile of every colour must fit the staged sweep's entry buffer
+    bool fits = true;
+    for (int32_t c = 0; c + 1 < (int32_t)H.color_ptr.size() && fits; ++c)
+      for (int64_t r0 = H.color_ptr[c]; r0 < H.color_ptr[c + 1]; r0 += kCsrR) {
+        const int64_t r1 = std::min<int64_t>(H.color_ptr[c + 1], r0 + kCsrR);
+        if (H.rowptr[r1] - H.rowptr[r0] > kCsrE) {
+          fits = false;
+          break;
+        }
+      }
+    g->csr_staged_ok = fits;
+    if ((rc = dalloc(&g->rowptr, (int64_t)rp32.size())) || (rc = dalloc(&g->col, (int64_t)col_p.size())) ||
+        (rc = dalloc(&g->val, (int64_t)val_p.size())) || (rc = dalloc(&g->perm, n)) ||
+        (rc = dalloc(&g->iperm, n)) || (rc = dalloc(&g->cap, n)))
+      return rc;
+    if ((rc = upload(g->rowptr, rp32)) || (rc = upload(g->col, col_p)) || (rc = upload(g->val, val_p)) ||
+        (rc = upload(g->perm, H.perm)) || (rc = upload(g->iperm, H.iperm)) || (rc = upload(g->cap, cp)))
+      return rc;
+    iperm_h = std::move(H.iperm);
+    tr.mark("build (host) + uploads");
+  }
+  if ((rc = set_pads(g, n_pads, pad_node, pad_g, nullptr, mem, &iperm_h))) return rc;
   CK(cudaDeviceSynchronize());
+  tr.mark("set_pads");
   guard.g = nullptr;
   *out = g;
   return PG_OK;

@@ -11,7 +11,10 @@
   2048-element tile boundaries of the storage layout: fixed-sweep iterates
   equal to the oracle's (1e-12 V);
 * the device-side load store: sources given in any order (unsorted, repeated
-  nodes) give the same store as sorted input (bit-identical iterates).
+  nodes) give the same store as sorted input (bit-identical iterates);
+* the device CSR builder (connected bipartite graphs) against the host builder
+  (PGB200_CSR_HOST=1), which also serves non-bipartite and disconnected graphs:
+  bit-identical iterates, host and device inputs.
 """
 import numpy as np
 import pytest
@@ -89,6 +92,60 @@ def test_staged_csr_equals_row_kernel_and_oracle(pgb, n, extra, star):
     rc, _ = run(pgb, g, 6, 1e-13, 1.5, 200000)
     assert ro.status == 0 and rc.status == 0
     np.testing.assert_allclose(rc.probes, ro.V, rtol=0, atol=1e-9)
+
+
+def _two_components(n, seed):
+    """Two disjoint random bipartite pieces (a path plus even-offset chords):
+    connected within each piece, so the device builder declines (one BFS from
+    node 0 does not reach the second piece) and the host builds the store."""
+    rng = np.random.default_rng(seed)
+    h = n // 2
+    us, vs = [], []
+    for off, m in ((0, h), (h, n - h)):
+        us.append(np.arange(off, off + m - 1)); vs.append(np.arange(off + 1, off + m))
+        a = rng.integers(off, off + m - 3, m // 2)
+        us.append(a); vs.append(a + 3)                     # odd distance: keeps the piece bipartite
+    u, v = np.concatenate(us).astype(np.int64), np.concatenate(vs).astype(np.int64)
+    g = rng.lognormal(0.0, 0.5, u.size)
+    pads = np.array([0, h], np.int64)
+    nodes = np.arange(1, n, 7, dtype=np.int64)
+    src = gridgen._triangle_sources(rng, nodes, 1e-3, 40e-12, 60e-12)
+    return gridgen.EdgeGrid(n=n, eu=u, ev=v, eg=g, cap=rng.uniform(1e-15, 1e-14, n), pad_node=pads,
+                            pad_g=np.full(2, 10.0), vdd=1.0, sources=src, h=5e-12, steps=8)
+
+
+@pytest.mark.parametrize("case", ["config2_small", "config2_ragged", "non_bipartite", "two_components"])
+def test_device_csr_builder_equals_host_builder(pgb, case, monkeypatch):
+    # pg_create_csr builds the colour-permuted store on the device for connected
+    # bipartite graphs (pg_csr_device.cu) and on the host otherwise or with
+    # PGB200_CSR_HOST set: same colours, permutation, rows, so bit-identical
+    # iterates; both memories of the inputs
+    if case == "config2_small":
+        g = gridgen.config_grid(2, dims=(2, 64, 96), steps=4)
+    elif case == "config2_ragged":
+        g = gridgen.config_grid(2, dims=(3, 37, 53), steps=4)
+    elif case == "non_bipartite":
+        g = random_graph(3001, 2500, seed=7)
+    else:
+        g = _two_components(4001, seed=5)
+    runs = {}
+    for host in (False, True):
+        if host:
+            monkeypatch.setenv("PGB200_CSR_HOST", "1")
+        else:
+            monkeypatch.delenv("PGB200_CSR_HOST", raising=False)
+        for device in (False, True):
+            G = pgb.Grid.from_edge_grid(g, device=device)
+            nc = G.info()["n_colors"]
+            r = G.transient(g.h, 4, tol=0.0, omega=1.7, max_sweeps=9, probes=np.arange(g.n),
+                            raise_on_noconv=False)
+            G.close()
+            runs[(host, device)] = (nc, r.probes)
+    ref_nc, ref = runs[(True, False)]
+    for key, (nc, pr) in runs.items():
+        assert nc == ref_nc, key
+        np.testing.assert_array_equal(pr, ref, err_msg=str(key))
+    assert np.abs(ref[-1] - 1.0).max() > 1e-9
 
 
 def test_rhs_tiles_multi_pads_and_loads(pgb):

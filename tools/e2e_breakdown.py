@@ -16,16 +16,21 @@ reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 g = gridgen.config_grid(cfg)
 omega = bench.OMEGA.get(cfg, 1.9)
 pinned = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
-pin = {k: pinned(getattr(g, k, None)) for k in ("gx", "gy", "gz", "cap", "lz", "pad_node", "pad_g", "pad_l")}
+pin = {k: pinned(getattr(g, k, None)) for k in ("gx", "gy", "gz", "cap", "lz", "pad_node", "pad_g", "pad_l",
+                                                "eu", "ev", "eg")}
 s = g.sources
 src = [pinned(a) for a in (s.node, s.ptr, s.t, s.i)]
 out = torch.empty(g.n, dtype=torch.float64).pin_memory().numpy()
 # as in bench.py: the device-resident grid of the timed region stays alive
-keep = P.Grid.from_mesh_grid(g, device=True) if os.environ.get("E2E_KEEP") else None
+keep = ((P.Grid.from_mesh_grid if hasattr(g, "gx") else P.Grid.from_edge_grid)(g, device=True)
+        if os.environ.get("E2E_KEEP") else None)
 for rep in range(reps):
     torch.cuda.synchronize(); t0 = time.perf_counter()
-    H = P.Grid.mesh(g.layers, g.ny, g.nx, pin["gx"], pin["gy"], pin["gz"], pin["cap"], pin["pad_node"], pin["pad_g"],
-                    g.vdd, pin["lz"], pin["pad_l"])
+    if hasattr(g, "gx"):
+        H = P.Grid.mesh(g.layers, g.ny, g.nx, pin["gx"], pin["gy"], pin["gz"], pin["cap"], pin["pad_node"],
+                        pin["pad_g"], g.vdd, pin["lz"], pin["pad_l"])
+    else:
+        H = P.Grid.csr(g.n, pin["eu"], pin["ev"], pin["eg"], pin["cap"], pin["pad_node"], pin["pad_g"], g.vdd)
     torch.cuda.synchronize(); t1 = time.perf_counter()
     H.set_sources(*src)
     torch.cuda.synchronize(); t2 = time.perf_counter()
