@@ -87,9 +87,15 @@ PG_API int pg_create_mesh(int32_t layers, int32_t ny, int32_t nx,
                           const double *pad_l, double vdd, int mem, pg_grid **out);
 
 /* Irregular RC grid given as a branch list (CSR store built natively:
- * parallel branches kept, self-loops dropped, nodes 2-coloured by BFS when the
- * graph is bipartite, greedily multi-coloured otherwise; the sweep visits the
- * colours in order -- Eq. (13) under that numbering).
+ * parallel branches kept, self-loops and zero-conductance branches dropped,
+ * nodes 2-coloured by BFS parity when the graph is bipartite, greedily
+ * multi-coloured otherwise; the sweep visits the colours in order -- Eq. (13)
+ * under that numbering).  Connected bipartite graphs are built on the device;
+ * other graphs (and every graph when the environment variable
+ * PGB200_CSR_HOST is set) by the host builder, which gives the same store.
+ * Invalid branches (endpoint outside [0, n), conductance negative or not
+ * finite) or capacitances return PG_EINVAL with the first offending index
+ * in pg_last_error().
  *   bu[m], bv[m]: branch end nodes in [0, n); bg[m]: conductance (>= 0).
  *   cap[n], pads as in pg_create_mesh (RC pads only).  n >= 1.          */
 PG_API int pg_create_csr(int64_t n, int64_t m, const int64_t *bu, const int64_t *bv,
