@@ -94,8 +94,8 @@ PG_API int pg_create_mesh(int32_t layers, int32_t ny, int32_t nx,
  * other graphs (and every graph when the environment variable
  * PGB200_CSR_HOST is set) by the host builder, which gives the same store.
  * Invalid branches (endpoint outside [0, n), conductance negative or not
- * finite) or capacitances return PG_EINVAL with the first offending index
- * in pg_last_error().
+ * finite; pg_last_error() names the first such branch) or capacitances
+ * (negative or not finite) return PG_EINVAL.
  *   bu[m], bv[m]: branch end nodes in [0, n); bg[m]: conductance (>= 0).
  *   cap[n], pads as in pg_create_mesh (RC pads only).  n >= 1.          */
 PG_API int pg_create_csr(int64_t n, int64_t m, const int64_t *bu, const int64_t *bv,
