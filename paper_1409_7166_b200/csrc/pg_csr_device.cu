@@ -81,9 +81,13 @@ __global__ void k_adj(int64_t nent, const int64_t *sval, const int64_t *bu, cons
   }
 }
 
-// one BFS level: frontier nodes (distance lvl) claim their unvisited neighbours
-__global__ void k_bfs_level(int64_t nf, const int64_t *front, const int64_t *ptr, const int64_t *adj, int32_t lvl,
-                            int32_t *dist, int64_t *next, unsigned long long *nnext) {
+// one BFS level: frontier nodes (distance lvl) claim their unvisited neighbours;
+// the frontier size is read on the device (levels are launched in batches
+// without a host round trip)
+__global__ void k_bfs_level(const unsigned long long *nfp, const int64_t *front, const int64_t *ptr,
+                            const int64_t *adj, int32_t lvl, int32_t *dist, int64_t *next,
+                            unsigned long long *nnext) {
+  const int64_t nf = (int64_t)*nfp;
   GSTRIDE(q, nf) {
     const int64_t i = front[q];
     for (int64_t k = ptr[i]; k < ptr[i + 1]; ++k) {
@@ -99,10 +103,13 @@ __global__ void k_first_unvisited(int64_t n, const int32_t *dist, unsigned long 
   }
 }
 
-__global__ void k_seed(int64_t s, int32_t *dist, int64_t *front) {  // source s, level 0
+__global__ void k_seed(int64_t s, int32_t *dist, int64_t *front, unsigned long long *nf) {  // source s, level 0
   dist[s] = 0;
   front[0] = s;
+  *nf = 1ull;
 }
+
+__global__ void k_carry(unsigned long long *lc, int b) { lc[0] = lc[b]; }
 
 // colour = distance parity; an edge inside one colour class: not bipartite
 __global__ void k_colour_check(int64_t n, const int64_t *ptr, const int64_t *adj, const int32_t *dist,
@@ -264,17 +271,25 @@ int build_csr_device(pg_grid *g, int64_t n, int64_t m, const int64_t *bu, const 
   DAL(fa, sizeof(int64_t) * (size_t)n);
   DAL(fb, sizeof(int64_t) * (size_t)n);
   DCK(cudaMemsetAsync(dist, 0xff, sizeof(int32_t) * (size_t)n, st), "memset");
-  unsigned long long *cnt = bad;  // reused: cnt[0] next-frontier size, cnt[1] first unvisited node
-  k_seed<<<1, 1, 0, st>>>(0, dist, fa);
-  int64_t nf = 1;
-  for (int32_t lvl = 0; nf > 0; ++lvl) {
-    DCK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), st), "memset");
-    k_bfs_level<<<gridn(nf, nsm), 256, 0, st>>>(nf, fa, ptr, adj, lvl, dist, fb, cnt);
+  unsigned long long *cnt = bad;  // reused: cnt[1] first unvisited node
+  // levels in batches of kB launches; lc[t] = frontier size of the batch's level t
+  constexpr int kB = 32;
+  unsigned long long *lc = nullptr;
+  DAL(lc, sizeof(unsigned long long) * (kB + 1));
+  int64_t *buf[2] = {fa, fb};  // level l's frontier in buf[l & 1] (kB even)
+  k_seed<<<1, 1, 0, st>>>(0, dist, fa, lc);
+  const int bfs_grid = nsm * 8;
+  for (int32_t lvl = 0;; lvl += kB) {
+    DCK(cudaMemsetAsync(lc + 1, 0, sizeof(unsigned long long) * kB, st), "memset");
+    for (int t = 0; t < kB; ++t)
+      k_bfs_level<<<bfs_grid, 256, 0, st>>>(lc + t, buf[t & 1], ptr, adj, lvl + t, dist, buf[(t + 1) & 1],
+                                            lc + t + 1);
+    DCK(cudaGetLastError(), "k_bfs_level");
     unsigned long long hn = 0;
-    DCK(cudaMemcpyAsync(&hn, cnt, sizeof(hn), cudaMemcpyDeviceToHost, st), "copy");
+    DCK(cudaMemcpyAsync(&hn, lc + kB, sizeof(hn), cudaMemcpyDeviceToHost, st), "copy");
     DCK(cudaStreamSynchronize(st), "sync");
-    nf = (int64_t)hn;
-    std::swap(fa, fb);
+    if (hn == 0) break;
+    k_carry<<<1, 1, 0, st>>>(lc, kB);
   }
   // several components: their sources are the host's (smallest node of each),
   // which one level-synchronous BFS does not give -- leave them to the host
