@@ -115,7 +115,9 @@ PG_API int pg_set_sources(pg_grid *g, int64_t n_src, const int64_t *node,
 /* Initial condition x(0) (n values; Algorithm 1 input "initial capacitor
  * voltages").  Default after create: every node at vdd, inductor currents 0
  * (the exact DC operating point of an unloaded grid).  Inductor currents are
- * reset to 0 by this call.                                                  */
+ * reset to 0 by this call.  The values (host or device memory) are checked on
+ * the device first: a NaN or infinite value returns PG_EINVAL and leaves the
+ * grid's state unchanged.                                                   */
 PG_API int pg_set_voltages(pg_grid *g, const double *v, int mem);
 
 /* Voltages after the last completed pg_transient step (or x(0)); n values. */

@@ -759,18 +759,26 @@ PG_API int pg_set_sources(pg_grid *g, int64_t n_src, const int64_t *node, const 
 PG_API int pg_set_voltages(pg_grid *g, const double *v, int mem) {
   REQUIRE(g != nullptr && v != nullptr, "grid/v is NULL");
   REQUIRE(mem == PG_MEM_HOST || mem == PG_MEM_DEVICE, "bad mem");
-  if (mem == PG_MEM_HOST) {
-    bool ok = true;
-    for (int64_t k = 0; k < g->n; ++k) ok &= std::isfinite(v[k]);
-    REQUIRE(ok, "voltages must be finite");
-  }
   int rc;
   if (!g->user_buf && (rc = dalloc(&g->user_buf, g->n))) return rc;
   double *tmp = g->user_buf;
-  cudaError_t e = cudaMemcpyAsync(tmp, v, sizeof(double) * g->n,
-                                  mem == PG_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
-                                  g->stream);
-  if (e == cudaSuccess) e = launch_scatter_user(g, tmp, g->x0);
+  // the values are checked on the device (host or device input) before the
+  // grid's state changes
+  int32_t *d_bad = nullptr;
+  if ((rc = dalloc(&d_bad, 1))) return rc;
+  struct FlagGuard {
+    int32_t *q;
+    ~FlagGuard() { dfree(q); }
+  } flag_guard{d_bad};
+  int32_t bad = 0;
+  CK(cudaMemsetAsync(d_bad, 0, sizeof(int32_t), g->stream));
+  CK(cudaMemcpyAsync(tmp, v, sizeof(double) * g->n,
+                     mem == PG_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, g->stream));
+  CK(finite_check_async(g, tmp, g->n, d_bad));
+  CK(cudaMemcpyAsync(&bad, d_bad, sizeof(int32_t), cudaMemcpyDeviceToHost, g->stream));
+  CK(cudaStreamSynchronize(g->stream));
+  REQUIRE(!bad, "voltages must be finite");
+  cudaError_t e = launch_scatter_user(g, tmp, g->x0);
   if (e == cudaSuccess) e = cudaMemcpyAsync(g->V[0], g->x0, sizeof(double) * g->np, cudaMemcpyDeviceToDevice, g->stream);
   if (e == cudaSuccess) e = launch_reset_state(g);
   if (e == cudaSuccess && g->iz) e = cudaMemsetAsync(g->iz, 0, sizeof(double) * g->np, g->stream);

@@ -276,6 +276,8 @@ void dfree_bytes(void *p);
 int build_sources_device(pg_grid *g, int64_t n_src, const int64_t *node, const int64_t *ptr, const double *t,
                          const double *v, int64_t npts, int32_t *bad_bits, std::string &err);
 cudaError_t mesh_check_async(pg_grid *g, const double *user_array, int which, int32_t *d_err);
+// *d_err |= 1 if any of a[0..n) is NaN or infinite (on g->stream)
+cudaError_t finite_check_async(pg_grid *g, const double *a, int64_t n, int32_t *d_err);
 
 // host CSR construction (pg_csr_build.cpp)
 struct CsrHost {

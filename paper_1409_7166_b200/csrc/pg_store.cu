@@ -142,6 +142,13 @@ __global__ void k_mesh_check(int64_t n, int32_t L, int32_t NY, int32_t NX, const
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(err, 1 << which);
 }
 
+__global__ void k_finite_check(int64_t n, const double *a, int32_t *err) {
+  bool bad = false;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+    bad |= !finite(a[k]);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(err, 1);
+}
+
 int grid_of(int64_t work, int num_sms) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, (int64_t)num_sms * 8));
 }
@@ -150,6 +157,11 @@ int grid_of(int64_t work, int num_sms) {
 
 cudaError_t mesh_check_async(pg_grid *g, const double *user_array, int which, int32_t *d_err) {
   k_mesh_check<<<grid_of(g->n, g->num_sms), 256>>>(g->n, g->md.L, g->md.NY, g->md.NX, user_array, which, d_err);
+  return cudaGetLastError();
+}
+
+cudaError_t finite_check_async(pg_grid *g, const double *a, int64_t n, int32_t *d_err) {
+  k_finite_check<<<grid_of(n, g->num_sms), 256, 0, g->stream>>>(n, a, d_err);
   return cudaGetLastError();
 }
 

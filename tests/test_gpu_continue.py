@@ -121,17 +121,32 @@ def test_group_continue_equals_one_call(pgb, transport):
 
 
 def test_rhs_kernel_flags_nonfinite_iterates(pgb):
-    import torch
+    # two finite loads of 1.7e308 A on one node overflow the right-hand side
+    # to -inf: the fused RHS kernel's check of V(t) reports PG_ENONFINITE
     g = mk(2, 16, 20, 10)
     G = grid_of(pgb, g, {"resident": 0})
-    v = torch.ones(g.n, dtype=torch.float64, device="cuda")
-    v[37] = float("nan")                       # device inputs are not value-checked
-    G.set_voltages(v)
+    G.set_sources(np.array([37, 37]), np.array([0, 1, 2]), np.array([0.0, 0.0]), np.array([1.7e308, 1.7e308]))
     with pytest.raises(pgb.PgError) as e:
-        G.transient(g.h, 3, tol=1e-10, omega=1.5, max_sweeps=50, cont=True)
+        G.transient(g.h, 3, tol=1e-10, omega=1.5, max_sweeps=50)
     assert e.value.code == -6
-    with pytest.raises(pgb.PgError):           # host inputs are
-        G.set_voltages(np.full(g.n, np.inf))
+    G.close()
+
+
+@pytest.mark.parametrize("device", [False, True])
+def test_set_voltages_must_be_finite(pgb, device):
+    # host and device inputs are value-checked on the device before the grid's
+    # state changes: a rejected call leaves V where it was
+    import torch
+    g = mk(2, 16, 20, 12)
+    G = grid_of(pgb, g, {"resident": 0})
+    v0 = np.linspace(0.9, 1.0, g.n)
+    G.set_voltages(v0)
+    bad = v0.copy()
+    bad[37] = np.nan if device else np.inf
+    with pytest.raises(pgb.PgError) as e:
+        G.set_voltages(torch.from_numpy(bad).cuda() if device else bad)
+    assert e.value.code == -1 and "finite" in str(e.value)
+    np.testing.assert_array_equal(G.voltages(), v0)
     G.close()
 
 
