@@ -90,7 +90,7 @@ PG_API int pg_create_mesh(int32_t layers, int32_t ny, int32_t nx,
  * parallel branches kept, self-loops and zero-conductance branches dropped,
  * nodes 2-coloured by BFS parity when the graph is bipartite, greedily
  * multi-coloured otherwise; the sweep visits the colours in order -- Eq. (13)
- * under that numbering).  Connected bipartite graphs are built on the device;
+ * under that numbering).  Bipartite graphs are built on the device;
  * other graphs (and every graph when the environment variable
  * PGB200_CSR_HOST is set) by the host builder, which gives the same store.
  * Invalid branches (endpoint outside [0, n), conductance negative or not

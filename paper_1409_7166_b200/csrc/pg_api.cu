@@ -477,7 +477,7 @@ PG_API int pg_create_csr(int64_t n, int64_t m, const int64_t *bu, const int64_t 
   if ((rc = common_init(g))) return rc;
   tr.mark("init");
   // The colour-permuted store is built on the device (pg_csr_device.cu) when
-  // the graph is connected and bipartite, else -- or with PGB200_CSR_HOST set
+  // the graph is bipartite, else -- or with PGB200_CSR_HOST set
   // -- by the host builder (pg_csr_build.cpp); both give the same store.
   std::vector<int64_t> iperm_h;
   bool done = false;
@@ -518,7 +518,7 @@ PG_API int pg_create_csr(int64_t n, int64_t m, const int64_t *bu, const int64_t 
       iperm_h.resize((size_t)n);
       CK(cudaMemcpy(iperm_h.data(), g->iperm, sizeof(int64_t) * n, cudaMemcpyDeviceToHost));
     }
-    tr.mark(done ? "build (device)" : "device build declined (not connected and bipartite)");
+    tr.mark(done ? "build (device)" : "device build declined (not bipartite)");
   }
   if (!done) {
     std::vector<int64_t> u, v;

@@ -13,11 +13,12 @@
 //   2. adjacency rows: the 2 m (row, branch) entries stable-sorted by row, so a
 //      row lists its branches in branch order (the host's fill order);
 //   3. 2-colouring by BFS parity: a level-synchronous BFS from node 0, colour =
-//      distance parity; the 2-colouring of a connected bipartite graph is unique
-//      once node 0's colour is fixed, so it equals the host's;
-//   4. an edge with equal colours on both ends (not bipartite) or a node the
-//      BFS did not reach (several components): *done = false and the caller
-//      builds the store on the host (greedy colouring / one BFS per component);
+//      distance parity (the 2-colouring of a connected bipartite graph is unique
+//      once one node's colour is fixed, so it equals the host's) --
+//      with several components, every component from its smallest node (found
+//      by minimum-label propagation), as the host's sequential BFS seeds them;
+//   4. an edge with equal colours on both ends (not bipartite): *done = false
+//      and the caller builds the store on the host (greedy colouring);
 //   5. permutation (colour-major, stable), permuted row pointers, columns,
 //      values and capacitances.
 #include <cuda_runtime.h>
@@ -111,6 +112,36 @@ __global__ void k_seed(int64_t s, int32_t *dist, int64_t *front, unsigned long l
 
 __global__ void k_carry(unsigned long long *lc, int b) { lc[0] = lc[b]; }
 
+// connected components by minimum-label propagation (labels only decrease; at
+// the fixed point every node carries the smallest index of its component)
+__global__ void k_lab_init(int64_t n, int64_t *lab) {
+  GSTRIDE(i, n) lab[i] = i;
+}
+__global__ void k_lab_hook(int64_t n, const int64_t *ptr, const int64_t *adj, int64_t *lab, int32_t *changed) {
+  GSTRIDE(i, n) {
+    int64_t m = lab[i];
+    for (int64_t k = ptr[i]; k < ptr[i + 1]; ++k) m = min(m, lab[adj[k]]);
+    if (m < lab[i]) {
+      atomicMin((unsigned long long *)&lab[i], (unsigned long long)m);
+      *changed = 1;
+    }
+  }
+}
+__global__ void k_lab_jump(int64_t n, int64_t *lab) {
+  GSTRIDE(i, n) lab[i] = lab[lab[i]];
+}
+// every component's smallest node starts the BFS at level 0
+__global__ void k_seed_all(int64_t n, const int64_t *lab, int32_t *dist, int64_t *front, unsigned long long *nf) {
+  GSTRIDE(i, n) {
+    if (lab[i] == i) {
+      dist[i] = 0;
+      front[atomicAdd(nf, 1ull)] = i;
+    } else {
+      dist[i] = -1;
+    }
+  }
+}
+
 // colour = distance parity; an edge inside one colour class: not bipartite
 __global__ void k_colour_check(int64_t n, const int64_t *ptr, const int64_t *adj, const int32_t *dist,
                                int64_t *black, int32_t *conflict) {
@@ -172,6 +203,7 @@ __global__ void k_tile_fit(int64_t c0, int64_t c1, const int32_t *rp32, int32_t 
 int build_csr_device(pg_grid *g, int64_t n, int64_t m, const int64_t *bu, const int64_t *bv, const double *bg,
                      const double *cap, bool *done, std::string &err) {
   *done = false;
+  int rc = PG_OK;
   cudaStream_t st = g->stream;
   const int nsm = g->num_sms;
   std::vector<void *> tmp;
@@ -277,28 +309,49 @@ int build_csr_device(pg_grid *g, int64_t n, int64_t m, const int64_t *bu, const 
   unsigned long long *lc = nullptr;
   DAL(lc, sizeof(unsigned long long) * (kB + 1));
   int64_t *buf[2] = {fa, fb};  // level l's frontier in buf[l & 1] (kB even)
-  k_seed<<<1, 1, 0, st>>>(0, dist, fa, lc);
   const int bfs_grid = nsm * 8;
-  for (int32_t lvl = 0;; lvl += kB) {
-    DCK(cudaMemsetAsync(lc + 1, 0, sizeof(unsigned long long) * kB, st), "memset");
-    for (int t = 0; t < kB; ++t)
-      k_bfs_level<<<bfs_grid, 256, 0, st>>>(lc + t, buf[t & 1], ptr, adj, lvl + t, dist, buf[(t + 1) & 1],
-                                            lc + t + 1);
-    DCK(cudaGetLastError(), "k_bfs_level");
-    unsigned long long hn = 0;
-    DCK(cudaMemcpyAsync(&hn, lc + kB, sizeof(hn), cudaMemcpyDeviceToHost, st), "copy");
-    DCK(cudaStreamSynchronize(st), "sync");
-    if (hn == 0) break;
-    k_carry<<<1, 1, 0, st>>>(lc, kB);
-  }
-  // several components: their sources are the host's (smallest node of each),
-  // which one level-synchronous BFS does not give -- leave them to the host
+  auto bfs = [&]() -> int {  // from the level-0 frontier in fa (size lc[0])
+    for (int32_t lvl = 0;; lvl += kB) {
+      DCK(cudaMemsetAsync(lc + 1, 0, sizeof(unsigned long long) * kB, st), "memset");
+      for (int t = 0; t < kB; ++t)
+        k_bfs_level<<<bfs_grid, 256, 0, st>>>(lc + t, buf[t & 1], ptr, adj, lvl + t, dist, buf[(t + 1) & 1],
+                                              lc + t + 1);
+      DCK(cudaGetLastError(), "k_bfs_level");
+      unsigned long long hn = 0;
+      DCK(cudaMemcpyAsync(&hn, lc + kB, sizeof(hn), cudaMemcpyDeviceToHost, st), "copy");
+      DCK(cudaStreamSynchronize(st), "sync");
+      if (hn == 0) return PG_OK;
+      k_carry<<<1, 1, 0, st>>>(lc, kB);
+    }
+  };
+  k_seed<<<1, 1, 0, st>>>(0, dist, fa, lc);
+  if ((rc = bfs())) return rc;
   DCK(cudaMemsetAsync(cnt + 1, 0xff, sizeof(unsigned long long), st), "memset");
   k_first_unvisited<<<gridn(n, nsm), 256, 0, st>>>(n, dist, cnt + 1);
   unsigned long long first = 0;
   DCK(cudaMemcpyAsync(&first, cnt + 1, sizeof(first), cudaMemcpyDeviceToHost, st), "copy");
   DCK(cudaStreamSynchronize(st), "sync");
-  if (first != ~0ull) return PG_OK;
+  if (first != ~0ull) {
+    // several components: the host seeds each at its smallest node (colour 0);
+    // find those by minimum-label propagation, then one multi-source BFS
+    int64_t *lab = nullptr;
+    int32_t *changed = nullptr;
+    DAL(lab, sizeof(int64_t) * (size_t)n);
+    DAL(changed, sizeof(int32_t));
+    k_lab_init<<<gridn(n, nsm), 256, 0, st>>>(n, lab);
+    for (int32_t hc = 1; hc;) {
+      DCK(cudaMemsetAsync(changed, 0, sizeof(int32_t), st), "memset");
+      k_lab_hook<<<gridn(n, nsm), 256, 0, st>>>(n, ptr, adj, lab, changed);
+      for (int k = 0; k < 4; ++k) k_lab_jump<<<gridn(n, nsm), 256, 0, st>>>(n, lab);
+      DCK(cudaGetLastError(), "labels");
+      DCK(cudaMemcpyAsync(&hc, changed, sizeof(int32_t), cudaMemcpyDeviceToHost, st), "copy");
+      DCK(cudaStreamSynchronize(st), "sync");
+    }
+    DCK(cudaMemsetAsync(lc, 0, sizeof(unsigned long long), st), "memset");
+    k_seed_all<<<gridn(n, nsm), 256, 0, st>>>(n, lab, dist, fa, lc);
+    DCK(cudaGetLastError(), "k_seed_all");
+    if ((rc = bfs())) return rc;
+  }
   int64_t *black = deg, *sblack = nullptr;  // deg is free now
   int32_t *conflict = nullptr;
   DAL(sblack, sizeof(int64_t) * (size_t)(n + 1));
@@ -317,7 +370,6 @@ int build_csr_device(pg_grid *g, int64_t n, int64_t m, const int64_t *bu, const 
   if (hconf) return PG_OK;  // not bipartite: the host's greedy colouring
   const int64_t n_red = n - n_black;
   // the store (library allocations, kept by the grid)
-  int rc;
   if ((rc = dalloc_bytes((void **)&g->rowptr, sizeof(int32_t) * (size_t)(n + 1 + 8))) ||
       (rc = dalloc_bytes((void **)&g->col, sizeof(int32_t) * (size_t)(nnz + 8))) ||
       (rc = dalloc_bytes((void **)&g->val, sizeof(double) * (size_t)(nnz + 8))) ||

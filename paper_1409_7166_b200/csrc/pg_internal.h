@@ -290,8 +290,8 @@ struct CsrHost {
 int build_csr(int64_t n, int64_t m, const int64_t *bu, const int64_t *bv, const double *bg,
               CsrHost &out, std::string &err);
 // the same store built on the device into g (pg_csr_device.cu; device input
-// arrays); *done = false (and g untouched) when the graph is not connected and
-// bipartite -- the caller then uses build_csr
+// arrays); *done = false (and g untouched) when the graph is not bipartite --
+// the caller then uses build_csr
 int build_csr_device(pg_grid *g, int64_t n, int64_t m, const int64_t *bu, const int64_t *bv, const double *bg,
                      const double *cap, bool *done, std::string &err);
 }  // namespace pgb

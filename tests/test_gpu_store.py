@@ -12,8 +12,9 @@
   equal to the oracle's (1e-12 V);
 * the device-side load store: sources given in any order (unsorted, repeated
   nodes) give the same store as sorted input (bit-identical iterates);
-* the device CSR builder (connected bipartite graphs) against the host builder
-  (PGB200_CSR_HOST=1), which also serves non-bipartite and disconnected graphs:
+* the device CSR builder (bipartite graphs, one or several components)
+  against the host builder (PGB200_CSR_HOST=1), which also serves
+  non-bipartite graphs:
   bit-identical iterates, host and device inputs.
 """
 import numpy as np
@@ -95,9 +96,9 @@ def test_staged_csr_equals_row_kernel_and_oracle(pgb, n, extra, star):
 
 
 def _two_components(n, seed):
-    """Two disjoint random bipartite pieces (a path plus even-offset chords):
-    connected within each piece, so the device builder declines (one BFS from
-    node 0 does not reach the second piece) and the host builds the store."""
+    """Two disjoint random bipartite pieces (a path plus odd-offset chords):
+    the device builder seeds each piece at its smallest node (minimum-label
+    propagation), as the host's BFS per component does."""
     rng = np.random.default_rng(seed)
     h = n // 2
     us, vs = [], []
@@ -116,7 +117,7 @@ def _two_components(n, seed):
 
 @pytest.mark.parametrize("case", ["config2_small", "config2_ragged", "non_bipartite", "two_components"])
 def test_device_csr_builder_equals_host_builder(pgb, case, monkeypatch):
-    # pg_create_csr builds the colour-permuted store on the device for connected
+    # pg_create_csr builds the colour-permuted store on the device for
     # bipartite graphs (pg_csr_device.cu) and on the host otherwise or with
     # PGB200_CSR_HOST set: same colours, permutation, rows, so bit-identical
     # iterates; both memories of the inputs
