@@ -1,8 +1,9 @@
 """Randomised cross-check of the device CSR builder (pg_csr_device.cu) against
 the host builder (PGB200_CSR_HOST=1) on the GPU (not part of the suite):
 config-2-recipe grids of random shape (connected, bipartite: the device path)
-and random graphs (trees plus chords, sometimes with triangles or split into
-pieces: the host fallback).  Both stores must give bit-identical iterates.
+and random graphs (trees plus chords -- half of them between the tree's two
+colours, so bipartite: the device path; the others mostly not: the host
+fallback -- some split into pieces, with open branches or self loops).  Both stores must give bit-identical iterates.
 usage: python tools/fuzz_csr_builder.py N_CASES SEED"""
 import os
 import sys
@@ -20,6 +21,12 @@ def random_graph(rng, n):
     v = [perm[rng.integers(0, k)] for k in range(1, n)]
     extra = int(rng.integers(0, n))
     a, b = rng.integers(0, n, extra), rng.integers(0, n, extra)
+    if rng.random() < 0.5:           # bipartite: chords between the two colours of the tree
+        depth = np.zeros(n, np.int64)
+        for k in range(1, n):        # the tree's parent of perm[k] is perm[j], j < k
+            depth[perm[k]] = depth[v[k - 1]] + 1
+        b = np.where((depth[a] ^ depth[b]) & 1, b, -1)
+        a, b = a[b >= 0], b[b >= 0]
     u = np.concatenate([np.array(u, np.int64), a])
     v = np.concatenate([np.array(v, np.int64), b])
     if rng.random() < 0.3:           # cut into two pieces
