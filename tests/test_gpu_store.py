@@ -254,3 +254,30 @@ def test_release_memory_returns_the_pool_cache(pgb):
     r = G.transient(g.h, 1, tol=1e-10, omega=1.96, max_sweeps=100000)
     G.close()
     assert r.status == 0
+
+
+@pytest.mark.parametrize("host_builder", [False, True])
+@pytest.mark.parametrize("device", [False, True])
+def test_csr_input_errors(pgb, host_builder, device, monkeypatch):
+    # bad branch lists and capacitances are rejected (PG_EINVAL) by the device
+    # builder and the host builder alike, host and device inputs
+    import torch
+    if host_builder:
+        monkeypatch.setenv("PGB200_CSR_HOST", "1")
+    else:
+        monkeypatch.delenv("PGB200_CSR_HOST", raising=False)
+    put = (lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()) if device else (lambda a: a)
+    n = 6
+    u, v = np.array([0, 1, 2, 3, 4], np.int64), np.array([1, 2, 3, 4, 5], np.int64)
+    g, cap = np.ones(5), np.full(n, 1e-15)
+    pads, pg = np.array([0], np.int64), np.array([10.0])
+    G = pgb.Grid.csr(n, put(u), put(v), put(g), put(cap), put(pads), put(pg))   # valid
+    G.close()
+    for bu, bv, bg, c, what in [(np.array([0, 1, 2, 3, 9]), v, g, cap, "branch 4"),
+                                (u, np.array([1, -2, 3, 4, 5]), g, cap, "branch 1"),
+                                (u, v, np.array([1.0, 1.0, -1.0, 1.0, 1.0]), cap, "branch 2"),
+                                (u, v, np.array([1.0, np.nan, 1.0, 1.0, 1.0]), cap, "branch 1"),
+                                (u, v, g, np.array([1e-15, 1e-15, np.inf, 1e-15, 1e-15, 1e-15]), "cap")]:
+        with pytest.raises(pgb.PgError) as e:
+            pgb.Grid.csr(n, put(bu.astype(np.int64)), put(bv.astype(np.int64)), put(bg), put(c), put(pads), put(pg))
+        assert e.value.code == -1 and what in str(e.value), str(e.value)
