@@ -360,6 +360,12 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
     const double Voth = vring[vY + ot];
     const double VN = fWn[f1];
     NodeC c0;
+#ifdef PG_DIAG_NOLDSC
+    // diagnostic build only (power experiments): the staged constants are
+    // loaded by TMA as usual but not read (fixed register values, no LDS)
+    c0 = NodeC{0.5, 0.5, 0.5, 0.5, 0.5, 0.5, 0.0, 0.3};
+    (void)cYm;
+#else
     c0.gxOwn = cring[cY + CGX + pe];
     c0.gxOth = cring[cY + CGX + gxo];
     c0.gyN = cring[cYm + CGY + me];
@@ -368,6 +374,7 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
     c0.gzD = cring[cY + CGZ + me - RW];
     c0.b = cring[cY + CB + me];
     c0.id = cring[cY + CID + me];
+#endif
     const double r0 = upd_c(c0, w, Vc, Vown, Voth, VN, vring[vY1 + me], vring[vY + me + RW], vring[vY + me - RW]);
     // red_1(y - 3): column class k ^ 1 (= mo); own value red_0(y - 3), x
     // neighbour black_0(y - 3), north / south black_0(y - 4) / black_0(y - 2)
@@ -398,6 +405,9 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
     (void)mo;
     // black_0(y - 1): column class k (its old value is red_0(y)'s north operand)
     NodeC cb;
+#ifdef PG_DIAG_NOLDSC
+    cb = NodeC{0.5, 0.5, cR[f2].gyS, aGyN, 0.5, 0.5, 0.0, 0.3};
+#else
     cb.gxOwn = cring[cYm + CGX + pe];
     cb.gxOth = cring[cYm + CGX + gxo];
     cb.gyN = cR[f2].gyS;  // gy of row y - 2 in this column: red_0(y - 2)'s own south link
@@ -406,6 +416,7 @@ __global__ void __launch_bounds__(W * L, 1) k_rb_sweep2(const __grid_constant__ 
     cb.gzD = cring[cYm + CGZ + me - RW];
     cb.b = cring[cYm + CB + me];
     cb.id = cring[cYm + CID + me];
+#endif
     const double b0 = upd_c(cb, w, aVN, fR0[f1], vring[vYm + ot], fR0[f2], aR0, vring[vYm + me + RW],
                             vring[vYm + me - RW]);
     // black_1(y - 4): column class k ^ 1; own value black_0(y - 4), x neighbour
