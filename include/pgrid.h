@@ -141,9 +141,10 @@ PG_API int pg_set_stream(pg_grid *g, void *stream);
  *   "pipe"   1 (default): full launches of F = 2 mesh sweeps run the
  *            warp-specialised two-level pipeline kernel (k_rb_sweep2); 0: the
  *            generic temporally blocked kernel for every F (same results)
- *   "pdl"    1 (default): consecutive sweep launches of a single grid use
- *            programmatic dependent launch (the next launch's prologue and
- *            constant-row loads overlap the previous launch's tail); 0: off
+ *   "pdl"    0 (default): off; 1: consecutive sweep launches of a single
+ *            grid use programmatic dependent launch (the next launch's
+ *            prologue and constant-row loads overlap the previous launch's
+ *            tail) -- measured slower on configs 1 and 4
  *   "l2keep" / "l2first" L2 eviction policy of the pipeline kernel, 6-bit
  *            masks over (gx, gy, gz_eff, b, 1/d, V): l2keep bits 0-4 read that
  *            constant array with evict_last, bit 5 writes V with evict_last;

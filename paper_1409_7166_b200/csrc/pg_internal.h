@@ -189,7 +189,8 @@ struct pg_grid {
   int l2first = -1;                    // option "l2first": arrays read with evict_first (bit mask, -1: auto)
   int l2keep = -1;                     // option "l2keep": arrays kept in L2 across launches (bit mask, -1: auto)
   int l2promo = 128;                   // option "l2promo": TMA L2 promotion bytes (0, 64, 128, 256)
-  int pdl = 1;                         // option "pdl": programmatic dependent launch of consecutive sweeps
+  int pdl = 0;                         // option "pdl": programmatic dependent launch of consecutive sweeps
+                                       // (off by default: 1.5-3 % slower on configs 1 and 4)
   int csr_stage = 1;                   // option "csr_stage": bulk-copy staged CSR sweep (k_csr_sweep_staged)
   int colour = 0;                      // option "colour": per-colour mesh sweep (k_rb_colour_mesh) for every
                                        // layer count (default: only meshes taller than kMaxLayers)

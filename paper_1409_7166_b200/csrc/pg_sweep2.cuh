@@ -39,9 +39,10 @@
 //   operands and an explicit L2 policy (auto: stream the reads, keep the
 //   written V for the next launch), and the proxy fence that orders the
 //   ring's generic accesses before its TMA refills runs every second step.
-// * Programmatic dependent launch (constant rows requested before
-//   griddepcontrol.wait) and, in a peer-memory slab group, the halo exchange
-//   and the global norm fused into the kernel's tail.
+// * Programmatic dependent launch as an option ("pdl", off by default:
+//   measured slower; constant rows requested before griddepcontrol.wait)
+//   and, in a peer-memory slab group, the halo exchange and the global norm
+//   fused into the kernel's tail.
 //
 // Streaming step y (u = y - r_first - 1, compile-time modulo 12):
 //   phase A: red_0(y), red_1(y - 3)          | (fence.proxy.async); barrier

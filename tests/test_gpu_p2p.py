@@ -107,14 +107,16 @@ def test_p2p_rejects_unsupported(pgb):
     grp.close()
 
 
-def test_p2p_single_slab_uses_graphs_and_pdl(pgb):
+@pytest.mark.parametrize("pdl", [0, 1])
+def test_p2p_single_slab_uses_graphs_and_pdl(pgb, pdl):
     # one slab per process (the multi-GPU shape): the exchange lives in the
-    # sweep kernels, so the driver replays graph batches with PDL between
-    # launches; the result equals the single grid bit for bit
+    # sweep kernels, so the driver replays graph batches (with PDL between
+    # launches when the option is on); the result equals the single grid bit
+    # for bit
     g = gridgen.config_grid(0, dims=(4, 80, 96), steps=10)
     steps, omega = 10, 1.9
     r1, V1 = single(pgb, g, steps, 1e-10, omega, 200000)
-    rn, Vn = grouped(pgb, g, 1, steps, 1e-10, omega, 200000, repeat=2)
+    rn, Vn = grouped(pgb, g, 1, steps, 1e-10, omega, 200000, options={"pdl": pdl}, repeat=2)
     np.testing.assert_array_equal(rn.sweeps, r1.sweeps)
     np.testing.assert_array_equal(Vn, V1)
 

@@ -130,6 +130,7 @@ def main():
                     help="idle seconds after every call (bursts: the board power stays low, so the "
                          "SM clock stays high); with --duty, calls alternate between --sweeps and "
                          "3 x --sweeps and the launch time is the difference (no per-call overhead)")
+    ap.add_argument("--opt", action="append", default=[], help="library option key=value (pg_set_option)")
     a = ap.parse_args()
     if a.copy:
         return copy_trace(a)
@@ -141,6 +142,9 @@ def main():
     g = gridgen.config_grid(a.workload)
     omega = bench.OMEGA.get(a.workload, bench.FALLBACK_OMEGA)
     G = P.Grid.from_mesh_grid(g, device=True)
+    for kv in a.opt:
+        k, v = kv.split("=", 1)
+        G.set_option(k, int(v))
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6550.4)
     nbytes = 56.0 * g.n
     launches = a.sweeps // 2
