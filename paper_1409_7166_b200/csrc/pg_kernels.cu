@@ -367,9 +367,12 @@ __device__ __forceinline__ void csr_bulk(void *dst, const void *src, uint32_t by
 }
 __device__ __forceinline__ uint32_t r16(int64_t bytes) { return (uint32_t)((bytes + 15) & ~(int64_t)15); }
 
-__device__ void csr_issue(const CsrArgs &a, CsrStage *st, uint64_t *bar, int64_t t, uint64_t pol) {
+// tile t's entry range [k0, k1) = [rowptr[r0], rowptr[r1]) is passed in: the
+// caller loads it one tile ahead, so the refill after a barrier does not wait
+// on a global load (warp 0 would otherwise start every tile a round trip late)
+__device__ void csr_issue(const CsrArgs &a, CsrStage *st, uint64_t *bar, int64_t t, int64_t k0, int64_t k1,
+                          uint64_t pol) {
   const int64_t r0 = a.r0 + t * kCsrR, r1 = min(a.r1, r0 + kCsrR);
-  const int64_t k0 = a.rowptr[r0], k1 = a.rowptr[r1];
   const int64_t ra = r0 & ~3ll, rb = r0 & ~1ll, ca = k0 & ~3ll, va = k0 & ~1ll;
   const uint32_t n_rp = r16(4 * (r1 + 1 - ra)), n_b = r16(8 * (r1 - rb)), n_c = r16(4 * (k1 - ca)),
                  n_v = r16(8 * (k1 - va));
@@ -402,14 +405,27 @@ __global__ void __launch_bounds__(kCsrT, 2) k_csr_sweep_staged(CsrArgs a) {
   }
   __syncthreads();
   if (tid == 0) {
-    if (blockIdx.x < ntiles) csr_issue(a, &st[0], &bar[0], blockIdx.x, pf);
-    if (blockIdx.x + gridDim.x < ntiles) csr_issue(a, &st[1], &bar[1], blockIdx.x + gridDim.x, pf);
+    for (int k = 0; k < 2; ++k) {
+      const int64_t t = blockIdx.x + (int64_t)k * gridDim.x;
+      if (t < ntiles) {
+        const int64_t r0 = a.r0 + t * kCsrR;
+        csr_issue(a, &st[k], &bar[k], t, a.rowptr[r0], a.rowptr[min(a.r1, r0 + kCsrR)], pf);
+      }
+    }
   }
   double dmax = 0.0;
   int it = 0;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
     const int sg = it & 1;
     CsrStage &S = st[sg];
+    // entry range of the tile this stage is refilled with after the barrier
+    const int64_t tn = t + 2 * (int64_t)gridDim.x;
+    int32_t nk0 = 0, nk1 = 0;
+    if (tid == 0 && tn < ntiles) {
+      const int64_t nr0 = a.r0 + tn * kCsrR;
+      nk0 = a.rowptr[nr0];
+      nk1 = a.rowptr[min(a.r1, nr0 + kCsrR)];
+    }
     {
       const uint32_t par = (uint32_t)((it >> 1) & 1);
       uint32_t done = 0;
@@ -468,7 +484,7 @@ __global__ void __launch_bounds__(kCsrT, 2) k_csr_sweep_staged(CsrArgs a) {
     // ordered before the async-proxy writes)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
-    if (tid == 0 && t + 2 * (int64_t)gridDim.x < ntiles) csr_issue(a, &S, &bar[sg], t + 2 * gridDim.x, pf);
+    if (tid == 0 && tn < ntiles) csr_issue(a, &S, &bar[sg], tn, nk0, nk1, pf);
   }
   dmax = warp_max(dmax);
   if ((tid & 31) == 0) wmax[tid >> 5] = dmax;
