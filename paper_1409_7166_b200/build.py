@@ -33,13 +33,18 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, prof: bool = False) -> str:
-    lib = PROF_LIB if prof else LIB
-    if not force and not prof and not _stale():
+def build(force: bool = False, verbose: bool = False, prof: bool = False, variant: str = "",
+          defs: tuple = ()) -> str:
+    """prof: the cycle-instrumented library; variant: an experiment library
+    lib/libpgb200_<variant>.so compiled with the extra -D flags `defs` (A/B
+    runs select it with PGB200_LIB); the default library takes neither."""
+    lib = PROF_LIB if prof else (os.path.join(LIBDIR, f"libpgb200_{variant}.so") if variant else LIB)
+    if not force and not prof and not variant and not _stale():
         return LIB
     # experiments: extra -D flags for the instrumented build only
     extra = (["-DPG_PROF"] + os.environ.get("PG_EXTRA_DEFS", "").split()) if prof else []
-    tag = "_prof" if prof else ""
+    extra += [f"-D{d}" for d in defs]
+    tag = "_prof" if prof else (f"_{variant}" if variant else "")
     os.makedirs(LIBDIR, exist_ok=True)
 
     def compile_one(src):

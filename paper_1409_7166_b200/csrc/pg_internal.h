@@ -46,8 +46,11 @@ struct DevCtl {
 constexpr int kRing = 4;
 constexpr int kRhsTile = 2048;  // storage elements per tile of the fused RHS kernel
 // staged CSR sweep: rows per tile and entry capacity per tile (6 per row)
-constexpr int kCsrR = 512;
-constexpr int kCsrE = 3072;
+#ifndef PG_CSR_R
+#define PG_CSR_R 512
+#endif
+constexpr int kCsrR = PG_CSR_R;
+constexpr int kCsrE = 6 * kCsrR;
 constexpr int kMaxLayers = 8;   // CTA of the mesh sweep = 32 lanes x L warps
 // taller meshes (up to kMaxMeshLayers) use the per-colour sweep k_rb_colour_mesh
 constexpr int kMaxMeshLayers = 256;

@@ -353,7 +353,15 @@ struct __align__(16) CsrStage {
   int32_t col[kCsrE + 8];
   double val[kCsrE + 4];
 };
-constexpr int kCsrT = 256;       // threads per CTA: two rows each
+#ifndef PG_CSR_T
+#define PG_CSR_T 256
+#endif
+#ifndef PG_CSR_B
+#define PG_CSR_B 2
+#endif
+constexpr int kCsrT = PG_CSR_T;  // threads per CTA: kCsrR / kCsrT (1 or 2) rows each
+constexpr int kCsrB = PG_CSR_B;  // resident CTAs per SM
+static_assert(kCsrR == kCsrT || kCsrR == 2 * kCsrT, "one or two rows per thread");
 constexpr int kCsrU = 6;         // gathers per row issued together (mesh-like degrees <= 6)
 
 __device__ __forceinline__ uint32_t csr_su32(const void *p) {
@@ -386,7 +394,7 @@ __device__ void csr_issue(const CsrArgs &a, CsrStage *st, uint64_t *bar, int64_t
   if (n_v) csr_bulk(st->val, a.val + va, n_v, bar, pol);
 }
 
-__global__ void __launch_bounds__(kCsrT, 2) k_csr_sweep_staged(CsrArgs a) {
+__global__ void __launch_bounds__(kCsrT, kCsrB) k_csr_sweep_staged(CsrArgs a) {
   extern __shared__ __align__(16) unsigned char csr_smem[];
   CsrStage *st = reinterpret_cast<CsrStage *>(csr_smem);
   __shared__ __align__(8) uint64_t bar[2];
@@ -444,7 +452,7 @@ __global__ void __launch_bounds__(kCsrT, 2) k_csr_sweep_staged(CsrArgs a) {
     const int32_t ca = k0 & ~3, va = k0 & ~1;
     // two rows per thread, their gathers issued together
     const int q0 = tid, q1 = tid + kCsrT;
-    const bool h0 = q0 < nr, h1 = q1 < nr;
+    const bool h0 = q0 < nr, h1 = kCsrR > kCsrT && q1 < nr;
     int32_t e0 = h0 ? S.rp[oa + q0] : 0, f0 = h0 ? S.rp[oa + q0 + 1] : 0;
     int32_t e1 = h1 ? S.rp[oa + q1] : 0, f1 = h1 ? S.rp[oa + q1 + 1] : 0;
     double s0 = h0 ? S.b[ob + q0] : 0.0, s1 = h1 ? S.b[ob + q1] : 0.0;
@@ -1267,7 +1275,7 @@ cudaError_t launch_sweep(pg_grid *g, int method, double omega, double tol, int j
         const int64_t rows = a.r1 - a.r0;
         if (staged) {
           const int64_t tiles = (rows + kCsrR - 1) / kCsrR;
-          const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 2 * (int64_t)g->num_sms));
+          const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, kCsrB * (int64_t)g->num_sms));
           k_csr_sweep_staged<<<grid, kCsrT, 2 * sizeof(CsrStage), g->stream>>>(a);
         } else {
           k_csr_sweep<<<grid_for(rows, 256, g->num_sms), 256, 0, g->stream>>>(a);
