@@ -359,8 +359,13 @@ struct __align__(16) CsrStage {
 #ifndef PG_CSR_B
 #define PG_CSR_B 2
 #endif
+#ifndef PG_CSR_S
+#define PG_CSR_S 2
+#endif
 constexpr int kCsrT = PG_CSR_T;  // threads per CTA: kCsrR / kCsrT (1 or 2) rows each
 constexpr int kCsrB = PG_CSR_B;  // resident CTAs per SM
+constexpr int kCsrS = PG_CSR_S;  // stages per CTA: kCsrS - 1 tiles in flight ahead of the compute
+static_assert(kCsrS >= 2 && kCsrS <= 8, "stage count");
 static_assert(kCsrR == kCsrT || kCsrR == 2 * kCsrT, "one or two rows per thread");
 constexpr int kCsrU = 6;         // gathers per row issued together (mesh-like degrees <= 6)
 
@@ -397,7 +402,7 @@ __device__ void csr_issue(const CsrArgs &a, CsrStage *st, uint64_t *bar, int64_t
 __global__ void __launch_bounds__(kCsrT, kCsrB) k_csr_sweep_staged(CsrArgs a) {
   extern __shared__ __align__(16) unsigned char csr_smem[];
   CsrStage *st = reinterpret_cast<CsrStage *>(csr_smem);
-  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ __align__(8) uint64_t bar[kCsrS];
   __shared__ double wmax[kCsrT / 32];
   a.launch_idx += *(volatile int32_t *)&a.ctl->jbase;
   if (sweep_skip(a.ctl, a.launch_idx, a.tol, a.first != 0)) return;
@@ -407,13 +412,13 @@ __global__ void __launch_bounds__(kCsrT, kCsrB) k_csr_sweep_staged(CsrArgs a) {
   const int tid = threadIdx.x;
   const uint64_t pf = pol_first();
   if (tid == 0) {
-    for (int k = 0; k < 2; ++k)
+    for (int k = 0; k < kCsrS; ++k)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(csr_su32(&bar[k])) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   if (tid == 0) {
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < kCsrS; ++k) {
       const int64_t t = blockIdx.x + (int64_t)k * gridDim.x;
       if (t < ntiles) {
         const int64_t r0 = a.r0 + t * kCsrR;
@@ -422,12 +427,12 @@ __global__ void __launch_bounds__(kCsrT, kCsrB) k_csr_sweep_staged(CsrArgs a) {
     }
   }
   double dmax = 0.0;
-  int it = 0;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-    const int sg = it & 1;
+  int sg = 0;          // stage of tile t
+  uint32_t par = 0;    // its mbarrier phase parity (flips every kCsrS tiles)
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     CsrStage &S = st[sg];
     // entry range of the tile this stage is refilled with after the barrier
-    const int64_t tn = t + 2 * (int64_t)gridDim.x;
+    const int64_t tn = t + kCsrS * (int64_t)gridDim.x;
     int32_t nk0 = 0, nk1 = 0;
     if (tid == 0 && tn < ntiles) {
       const int64_t nr0 = a.r0 + tn * kCsrR;
@@ -435,7 +440,6 @@ __global__ void __launch_bounds__(kCsrT, kCsrB) k_csr_sweep_staged(CsrArgs a) {
       nk1 = a.rowptr[min(a.r1, nr0 + kCsrR)];
     }
     {
-      const uint32_t par = (uint32_t)((it >> 1) & 1);
       uint32_t done = 0;
       while (!done)
         asm volatile(
@@ -493,6 +497,10 @@ __global__ void __launch_bounds__(kCsrT, kCsrB) k_csr_sweep_staged(CsrArgs a) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     if (tid == 0 && tn < ntiles) csr_issue(a, &S, &bar[sg], tn, nk0, nk1, pf);
+    if (++sg == kCsrS) {
+      sg = 0;
+      par ^= 1u;
+    }
   }
   dmax = warp_max(dmax);
   if ((tid & 31) == 0) wmax[tid >> 5] = dmax;
@@ -1263,7 +1271,7 @@ cudaError_t launch_sweep(pg_grid *g, int method, double omega, double tol, int j
         if (g->dev < 0 || g->dev >= 64) return cudaErrorInvalidDevice;
         if (!attr_set[g->dev].load(std::memory_order_acquire)) {
           cudaError_t e = cudaFuncSetAttribute(k_csr_sweep_staged, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)(2 * sizeof(CsrStage)));
+                                               (int)(kCsrS * sizeof(CsrStage)));
           if (e != cudaSuccess) return e;
           attr_set[g->dev].store(true, std::memory_order_release);
         }
@@ -1276,7 +1284,7 @@ cudaError_t launch_sweep(pg_grid *g, int method, double omega, double tol, int j
         if (staged) {
           const int64_t tiles = (rows + kCsrR - 1) / kCsrR;
           const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, kCsrB * (int64_t)g->num_sms));
-          k_csr_sweep_staged<<<grid, kCsrT, 2 * sizeof(CsrStage), g->stream>>>(a);
+          k_csr_sweep_staged<<<grid, kCsrT, kCsrS * sizeof(CsrStage), g->stream>>>(a);
         } else {
           k_csr_sweep<<<grid_for(rows, 256, g->num_sms), 256, 0, g->stream>>>(a);
         }
