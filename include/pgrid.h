@@ -144,7 +144,10 @@ PG_API int pg_set_stream(pg_grid *g, void *stream);
  *   "pdl"    0 (default): off; 1: consecutive sweep launches of a single
  *            grid use programmatic dependent launch (the next launch's
  *            prologue and constant-row loads overlap the previous launch's
- *            tail) -- measured slower on configs 1 and 4
+ *            tail; mesh pipeline kernel and the staged CSR colour launches,
+ *            whose first tiles' bulk copies are then requested before the
+ *            dependency wait) -- same results, measured slower on configs
+ *            1, 2 and 4
  *   "l2keep" / "l2first" L2 eviction policy of the pipeline kernel, 6-bit
  *            masks over (gx, gy, gz_eff, b, 1/d, V): l2keep bits 0-4 read that
  *            constant array with evict_last, bit 5 writes V with evict_last;

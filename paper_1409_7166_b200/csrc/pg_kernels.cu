@@ -254,6 +254,7 @@ struct CsrArgs {
   double omega, tol;
   int32_t launch_idx;
   int32_t first;    // first colour of the sweep
+  int32_t pre;      // staged sweep launched with programmatic stream serialisation after a sweep launch
   DevCtl *ctl;
 };
 
@@ -404,13 +405,21 @@ __global__ void __launch_bounds__(kCsrT, kCsrB) k_csr_sweep_staged(CsrArgs a) {
   CsrStage *st = reinterpret_cast<CsrStage *>(csr_smem);
   __shared__ __align__(8) uint64_t bar[kCsrS];
   __shared__ double wmax[kCsrT / 32];
-  a.launch_idx += *(volatile int32_t *)&a.ctl->jbase;
-  if (sweep_skip(a.ctl, a.launch_idx, a.tol, a.first != 0)) return;
-  zero_next_slot(a.ctl, a.launch_idx, a.first != 0);
-  double *V = (*(volatile int32_t *)&a.ctl->base) ? a.V1 : a.V0;
   const int64_t ntiles = (a.r1 - a.r0 + kCsrR - 1) / kCsrR;
   const int tid = threadIdx.x;
   const uint64_t pf = pol_first();
+  // Programmatic dependent launch (a.pre: the previous launch in the stream is
+  // a sweep launch, whose outputs are V and the control block only): the
+  // first tiles' row data -- constants of the transient's step -- are
+  // requested while that launch drains; V and the control block are read
+  // after griddepcontrol.wait.  Otherwise the skip test comes first and a
+  // converged step's queued launches cost no memory traffic.
+  if (a.pre) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  } else {
+    a.launch_idx += *(volatile int32_t *)&a.ctl->jbase;
+    if (sweep_skip(a.ctl, a.launch_idx, a.tol, a.first != 0)) return;
+  }
   if (tid == 0) {
     for (int k = 0; k < kCsrS; ++k)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(csr_su32(&bar[k])) : "memory");
@@ -426,6 +435,30 @@ __global__ void __launch_bounds__(kCsrT, kCsrB) k_csr_sweep_staged(CsrArgs a) {
       }
     }
   }
+  if (a.pre) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    a.launch_idx += *(volatile int32_t *)&a.ctl->jbase;
+    if (sweep_skip(a.ctl, a.launch_idx, a.tol, a.first != 0)) {
+      // the copies in flight target this CTA's shared memory: let them land
+      if (tid == 0) {
+        for (int k = 0; k < kCsrS; ++k) {
+          if (blockIdx.x + (int64_t)k * gridDim.x >= ntiles) break;
+          uint32_t done = 0;
+          while (!done)
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                "selp.u32 %0, 1, 0, p;\n\t}"
+                : "=r"(done)
+                : "r"(csr_su32(&bar[k])), "r"(0u)
+                : "memory");
+        }
+      }
+      __syncthreads();
+      return;
+    }
+  }
+  zero_next_slot(a.ctl, a.launch_idx, a.first != 0);
+  double *V = (*(volatile int32_t *)&a.ctl->base) ? a.V1 : a.V0;
   double dmax = 0.0;
   int sg = 0;          // stage of tile t
   uint32_t par = 0;    // its mbarrier phase parity (flips every kCsrS tiles)
@@ -1276,6 +1309,8 @@ cudaError_t launch_sweep(pg_grid *g, int method, double omega, double tol, int j
           attr_set[g->dev].store(true, std::memory_order_release);
         }
       }
+      bool prev_staged = staged;  // launch j - 1 (same grid, same kernel choice)
+      a.pre = 0;
       for (int c = 0; c < g->ncolor; ++c) {
         a.r0 = g->color_ptr[c];
         a.r1 = g->color_ptr[c + 1];
@@ -1284,7 +1319,22 @@ cudaError_t launch_sweep(pg_grid *g, int method, double omega, double tol, int j
         if (staged) {
           const int64_t tiles = (rows + kCsrR - 1) / kCsrR;
           const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, kCsrB * (int64_t)g->num_sms));
-          k_csr_sweep_staged<<<grid, kCsrT, kCsrS * sizeof(CsrStage), g->stream>>>(a);
+          // option "pdl": overlap this launch's first bulk copies with the
+          // previous sweep launch (never with the RHS kernel, which writes b)
+          a.pre = g->pdl_ok && (j > 0 || c > 0) && prev_staged ? 1 : 0;
+          cudaLaunchConfig_t cfg = {};
+          cfg.gridDim = dim3(grid);
+          cfg.blockDim = dim3(kCsrT);
+          cfg.dynamicSmemBytes = kCsrS * sizeof(CsrStage);
+          cfg.stream = g->stream;
+          cudaLaunchAttribute attr[1];
+          attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+          attr[0].val.programmaticStreamSerializationAllowed = 1;
+          cfg.attrs = attr;
+          cfg.numAttrs = a.pre ? 1 : 0;
+          cudaError_t e = cudaLaunchKernelEx(&cfg, k_csr_sweep_staged, a);
+          if (e != cudaSuccess) return e;
+          prev_staged = true;
         } else {
           k_csr_sweep<<<grid_for(rows, 256, g->num_sms), 256, 0, g->stream>>>(a);
         }

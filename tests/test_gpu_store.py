@@ -95,6 +95,24 @@ def test_staged_csr_equals_row_kernel_and_oracle(pgb, n, extra, star):
     np.testing.assert_allclose(rc.probes, ro.V, rtol=0, atol=1e-9)
 
 
+@pytest.mark.parametrize("n,extra,star,graph", [(1001, 700, 0, 1), (20011, 15000, 0, 1), (20011, 15000, 0, 0),
+                                                (5003, 3000, 4000, 1)])
+def test_staged_csr_pdl_is_bit_identical(pgb, n, extra, star, graph):
+    """Option pdl on the CSR path (programmatic dependent launch of the staged
+    colour launches: the first tiles' row data requested before
+    griddepcontrol.wait): same iterates, same converged results and sweep
+    counts (a converged step's queued launches drain their copies and exit)."""
+    g = random_graph(n, extra, seed=n + star, star=star)
+    ra, _ = run(pgb, g, 6, 0.0, 1.5, 7, {"pdl": 1, "graph": graph})
+    rb, _ = run(pgb, g, 6, 0.0, 1.5, 7, {"pdl": 0, "graph": graph})
+    np.testing.assert_array_equal(ra.probes, rb.probes)
+    ca, _ = run(pgb, g, 6, 1e-11, 1.5, 200000, {"pdl": 1, "graph": graph})
+    cb, _ = run(pgb, g, 6, 1e-11, 1.5, 200000, {"pdl": 0, "graph": graph})
+    assert ca.status == 0 and cb.status == 0
+    np.testing.assert_array_equal(ca.probes, cb.probes)
+    np.testing.assert_array_equal(np.asarray(ca.sweeps), np.asarray(cb.sweeps))
+
+
 def _two_components(n, seed):
     """Two disjoint random bipartite pieces (a path plus odd-offset chords):
     the device builder seeds each piece at its smallest node (minimum-label
