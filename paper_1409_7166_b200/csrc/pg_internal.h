@@ -47,7 +47,7 @@ constexpr int kRing = 4;
 constexpr int kRhsTile = 2048;  // storage elements per tile of the fused RHS kernel
 // staged CSR sweep: rows per tile and entry capacity per tile (6 per row)
 #ifndef PG_CSR_R
-#define PG_CSR_R 512
+#define PG_CSR_R 256
 #endif
 constexpr int kCsrR = PG_CSR_R;
 constexpr int kCsrE = 6 * kCsrR;

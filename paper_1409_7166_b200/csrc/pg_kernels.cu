@@ -340,13 +340,20 @@ __global__ void __launch_bounds__(256) k_csr_jacobi(CsrArgs a) {
 // arbitrary graph, colour-permuted rows, §IV), with the row data of
 // every tile of kCsrR rows -- row pointers, b, 1/d, column indices, values: all
 // contiguous in the colour-permuted store -- moved into shared memory by 1-D
-// bulk copies (cp.async.bulk, mbarrier completion, L2 evict_first) one tile
-// ahead of the compute (two stages per CTA, persistent CTAs).  The only
+// bulk copies (cp.async.bulk, mbarrier completion, L2 evict_first).  The only
 // dependent global loads left are the gathers V[col] (the other colours' rows,
 // L2-resident for these grid sizes); each thread keeps the gathers of its two
-// rows in flight together.  Per-row arithmetic and summation order are those
-// of k_csr_sweep (bit-identical results).  Ranges are copied from 16-byte
-// aligned starts and rounded up to 16 bytes (the arrays carry zero slack).
+// rows in flight together.  What bounds the sweep is the number of rows whose
+// gathers are outstanding per SM, capped by the rows staged in shared memory
+// and by the register file (measured), so the default is ONE
+// stage per CTA and many small persistent CTAs per SM (256-row tiles, 128
+// threads, 8 CTAs per SM, 64 registers): a CTA's bulk copies are covered by
+// the other resident CTAs' compute, and about two thirds of the staged rows
+// are computing at any time instead of the half of a two-stage ring
+// (-DPG_CSR_S=2 and the other geometries stay as experiment builds).
+// Per-row arithmetic and summation order are those of k_csr_sweep
+// (bit-identical results).  Ranges are copied from 16-byte aligned starts and
+// rounded up to 16 bytes (the arrays carry zero slack).
 struct __align__(16) CsrStage {
   int32_t rp[kCsrR + 8];
   double b[kCsrR + 2];
@@ -355,18 +362,19 @@ struct __align__(16) CsrStage {
   double val[kCsrE + 4];
 };
 #ifndef PG_CSR_T
-#define PG_CSR_T 256
+#define PG_CSR_T 128
 #endif
 #ifndef PG_CSR_B
-#define PG_CSR_B 2
+#define PG_CSR_B 8
 #endif
 #ifndef PG_CSR_S
-#define PG_CSR_S 2
+#define PG_CSR_S 1
 #endif
 constexpr int kCsrT = PG_CSR_T;  // threads per CTA: kCsrR / kCsrT (1 or 2) rows each
 constexpr int kCsrB = PG_CSR_B;  // resident CTAs per SM
-constexpr int kCsrS = PG_CSR_S;  // stages per CTA: kCsrS - 1 tiles in flight ahead of the compute
-static_assert(kCsrS >= 2 && kCsrS <= 8, "stage count");
+constexpr int kCsrS = PG_CSR_S;  // stages per CTA: kCsrS - 1 tiles in flight ahead of the compute (1: the
+                                 // other resident CTAs cover a CTA's load)
+static_assert(kCsrS >= 1 && kCsrS <= 8, "stage count");
 static_assert(kCsrR == kCsrT || kCsrR == 2 * kCsrT, "one or two rows per thread");
 constexpr int kCsrU = 6;         // gathers per row issued together (mesh-like degrees <= 6)
 
@@ -494,19 +502,19 @@ __global__ void __launch_bounds__(kCsrT, kCsrB) k_csr_sweep_staged(CsrArgs a) {
     int32_t e1 = h1 ? S.rp[oa + q1] : 0, f1 = h1 ? S.rp[oa + q1 + 1] : 0;
     double s0 = h0 ? S.b[ob + q0] : 0.0, s1 = h1 ? S.b[ob + q1] : 0.0;
     while (e0 < f0 || e1 < f1) {
-      double v0[kCsrU], w0[kCsrU], v1[kCsrU], w1[kCsrU];
+      // the gathers of both rows in flight together; the branch values are
+      // read from the stage when they have landed (not held in registers
+      // beside them: 64 registers, 1024 resident threads per SM)
+      double v0[kCsrU], v1[kCsrU];
 #pragma unroll
       for (int u = 0; u < kCsrU; ++u) {
-        const bool p0 = e0 + u < f0, p1 = e1 + u < f1;
-        v0[u] = p0 ? __ldg(V + S.col[e0 + u - ca]) : 0.0;
-        w0[u] = p0 ? S.val[e0 + u - va] : 0.0;
-        v1[u] = p1 ? __ldg(V + S.col[e1 + u - ca]) : 0.0;
-        w1[u] = p1 ? S.val[e1 + u - va] : 0.0;
+        v0[u] = e0 + u < f0 ? __ldg(V + S.col[e0 + u - ca]) : 0.0;
+        v1[u] = e1 + u < f1 ? __ldg(V + S.col[e1 + u - ca]) : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < kCsrU; ++u) {
-        if (e0 + u < f0) s0 = fma(w0[u], v0[u], s0);
-        if (e1 + u < f1) s1 = fma(w1[u], v1[u], s1);
+        if (e0 + u < f0) s0 = fma(S.val[e0 + u - va], v0[u], s0);
+        if (e1 + u < f1) s1 = fma(S.val[e1 + u - va], v1[u], s1);
       }
       e0 += kCsrU;
       e1 += kCsrU;
@@ -1306,6 +1314,12 @@ cudaError_t launch_sweep(pg_grid *g, int method, double omega, double tol, int j
           cudaError_t e = cudaFuncSetAttribute(k_csr_sweep_staged, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)(kCsrS * sizeof(CsrStage)));
           if (e != cudaSuccess) return e;
+          // kCsrB CTAs per SM need nearly all of the SM's shared memory
+#ifndef PG_CSR_NOCARVE
+          e = cudaFuncSetAttribute(k_csr_sweep_staged, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                   (int)cudaSharedmemCarveoutMaxShared);
+          if (e != cudaSuccess) return e;
+#endif
           attr_set[g->dev].store(true, std::memory_order_release);
         }
       }

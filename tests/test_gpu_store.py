@@ -1,6 +1,6 @@
 """Store-construction and kernel edge cases (-m gpu):
 
-* the staged CSR sweep (bulk-copied 512-row tiles) on irregular graphs whose
+* the staged CSR sweep (bulk-copied 256-row tiles) on irregular graphs whose
   colour classes start at unaligned rows, with several colours (greedy
   colouring of non-bipartite graphs), tiles of varying entry counts and a
   star node too large for the stage (whole-grid fallback): bit-identical to the

@@ -43,13 +43,15 @@ def random_graph(rng, n):
                             pad_g=np.full(pads.size, 10.0), vdd=1.0, sources=src, h=5e-12, steps=4)
 
 
-def run(g, host):
+def run(g, host, pdl=0):
     if host:
         os.environ["PGB200_CSR_HOST"] = "1"
     else:
         os.environ.pop("PGB200_CSR_HOST", None)
     G = P.Grid.from_edge_grid(g, device=bool(host is False))
     nc = G.info()["n_colors"]
+    if pdl:
+        G.set_option("pdl", 1)
     r = G.transient(g.h, 3, tol=0.0, omega=1.6, max_sweeps=7, probes=np.arange(g.n), raise_on_noconv=False)
     G.close()
     return nc, r.probes
@@ -69,7 +71,8 @@ for case in range(n_cases):
         kind = f"random n={n} m={g.eu.size}"
     nd, pd = run(g, False)
     nh, ph = run(g, True)
-    ok = nd == nh and np.array_equal(pd, ph)
+    _, pp = run(g, False, pdl=1)     # programmatic dependent launch of the staged colour launches
+    ok = nd == nh and np.array_equal(pd, ph) and np.array_equal(pd, pp)
     fails += not ok
     print(f"case {case}: {kind} colours {nd}/{nh} {'OK' if ok else 'MISMATCH'}", flush=True)
 print(f"{n_cases - fails}/{n_cases} passed")

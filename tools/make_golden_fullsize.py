@@ -55,7 +55,7 @@ OMEGA_Y8K = {
 JOBS = {
     # name: (config, steps, tol, series_rl, order, omega)
     "c1": (1, 20, 1e-10, "node", "redblack", OMEGA[1]),
-    "c2": (2, 6, 1e-10, "node", "redblack", OMEGA[2]),
+    "c2": (2, 20, 1e-10, "node", "redblack", OMEGA[2]),
     "c3_element": (3, 20, 1e-10, "element", "redblack", OMEGA[3]),
     "c4": (4, 3, 1e-10, "node", "redblack", OMEGA[4]),
     "c1_young8k": (1, 20, 1e-10, "node", "redblack", OMEGA_Y8K[1]),
