@@ -1314,12 +1314,9 @@ cudaError_t launch_sweep(pg_grid *g, int method, double omega, double tol, int j
           cudaError_t e = cudaFuncSetAttribute(k_csr_sweep_staged, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)(kCsrS * sizeof(CsrStage)));
           if (e != cudaSuccess) return e;
-          // kCsrB CTAs per SM need nearly all of the SM's shared memory
-#ifndef PG_CSR_NOCARVE
-          e = cudaFuncSetAttribute(k_csr_sweep_staged, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                   (int)cudaSharedmemCarveoutMaxShared);
-          if (e != cudaSuccess) return e;
-#endif
+          // the shared-memory carveout is left to the driver: it fits the kCsrB
+          // CTAs per SM, and asking for the maximum costs the gathers their L1
+          // (126.4 vs 123.2 us per sweep on config 2, profiles/r2_s4/s4_csr_carve.txt)
           attr_set[g->dev].store(true, std::memory_order_release);
         }
       }
