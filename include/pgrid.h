@@ -174,6 +174,13 @@ PG_API int pg_set_stream(pg_grid *g, void *stream);
  *            same iterates as the streaming sweep bit for bit,
  *            pg_stats.sweeps_per_launch = 1); 0 (default): only meshes taller
  *            than 8 layers use it
+ *   "csr_stage" 1 (default): CSR grids run the staged multi-colour sweep
+ *            (k_csr_sweep_staged: every 256-row tile's row pointers, b, 1/d,
+ *            columns and values bulk-copied into shared memory, one stage per
+ *            CTA, 8 CTAs per SM) when every tile fits its stage (at most
+ *            1536 entries per 256 rows of one colour); 0, or a tile that does
+ *            not fit: one thread per row (k_csr_sweep), same iterates bit
+ *            for bit
  *   "timing" 1: an event pair around every time step's sweep launches
  *            (stats.sweep_ms, stats.sweep_launches), read after the call: no
  *            extra synchronisation, graphs and PDL stay on                  */
